@@ -1,0 +1,288 @@
+"""bench.py — throughput of the block-simulation hot path on B200.
+
+One step = sv_reset(e_0) + the whole seeded circuit of the workload applied through the
+C ABI (every gate kernel of the path).  metric: amplitude-updates/s (sum over gates of the
+amplitudes each gate can change, T_g); achieved HBM GB/s = 32 B x that.
+
+  python bench.py [--gpus N --steps K --warmup W] [--config 4] [--impl ours|reference]
+
+N = 1: config 4 (10 qubits + 6 qutrits + 4 ququarts + 2 ququints, D = 4.78e9, 76 GB) on one
+GPU — the largest single-GPU config, the one north_star's >= 70 % HBM target is stated on.
+N > 1 (torchrun, one process per GPU, NCCL): the same register sharded over N GPUs on its
+most-significant qubits (strong scaling), pairwise NVLink exchanges for sharded targets.
+--impl reference: the CPU oracle (oracle/blocksim.c, O-2) timed on the host cores on a
+bounded sample of the same workload (the tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "amplitude-updates/s and achieved HBM GB/s (vs B200 peak) per gate, 1/2/4/8 GPU"
+UNIT = "amplitude-updates/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def touched_total(dims, gates):
+    """sum_g T_g from the library's host planner (no device work)."""
+    import paper_2410_17876_b200 as P
+    tot = 0
+    for g in gates:
+        tot += int(P.plan_gate(dims, g.target, g.U, g.ctrl, g.vals).touched)
+    return tot
+
+
+def cpu_baseline(cfg: int, budget_s: float = 15.0):
+    """O-2 on a bounded sample: the same recipe on a register with fewer qubits (3), gates
+    applied in order until ~budget_s of CPU time."""
+    from oracle import blocksim as O2
+    from sv_inputs import config_circuit
+    nq = {3: 4, 4: 3, 5: 2}.get(cfg, None)
+    dims, gates = config_circuit(cfg, nqubits=nq)
+    D = int(np.prod(dims))
+    psi = np.zeros(D, dtype=np.complex128)
+    psi[0] = 1.0
+    import paper_2410_17876_b200 as P
+    t0 = time.perf_counter()
+    upd, ng = 0, 0
+    for g in gates:
+        O2.apply(psi, dims, g)
+        upd += int(P.plan_gate(dims, g.target, g.U, g.ctrl, g.vals).touched)
+        ng += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": upd / dt, "unit": UNIT, "cores": O2.num_threads(), "kind": "oracle",
+            "sample": f"config {cfg} recipe with {nq} qubits (D={D}), first {ng} of {len(gates)} gates, "
+                      f"{dt:.1f} s on the host"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    b = cpu_baseline(args.config, budget_s=max(5.0, 60.0 / max(1, args.steps + args.warmup)))
+    from sv_inputs import CONFIG_NAMES
+    line = {"impl": "reference", "metric": METRIC, "value": b["value"], "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": CONFIG_NAMES[args.config]},
+            "cpu_baseline": b,
+            "e2e": {"value": b["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 direct, 2 tiled")
+    ap.add_argument("--no-fuse", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ngates", type=int, default=None)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2410_17876_b200 as P
+    from sv_inputs import config_circuit, CONFIG_NAMES
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    dims, gates = config_circuit(args.config, ngates=args.ngates)
+    fuse = not args.no_fuse
+    T_step = touched_total(dims, gates)                       # global amplitude updates / step
+
+    if world > 1:
+        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(P.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        st = P.State.sharded(dims, rank, world, bytes(idt.cpu().numpy()), device=local_rank)
+    else:
+        st = P.State(dims, device=local_rank)
+    st.set_option(P.sv.SV_OPT_KERNEL, args.kernel)
+    ga = P.sv._GateArray(gates)
+    info = st.info()
+    ext = torch.cuda.ExternalStream(info.cuda_stream)
+
+    def step():
+        st.reset(0)
+        st.apply_circuit(ga, fuse=fuse, check=False)
+
+    for _ in range(args.warmup):
+        step()
+    st.sync()
+    # ---- timed region: K steps, barrier + sync on both sides, CUDA events on the library stream
+    st.set_option(P.sv.SV_OPT_PROFILE, 1)
+    st.profile_read(reset=True)
+    launches0 = st.info().kernel_launches
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local_rank) as clk:
+        e0.record(ext)
+        for _ in range(args.steps):
+            step()
+        e1.record(ext)
+        st.sync()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    prof = st.profile_read(reset=True)
+    st.set_option(P.sv.SV_OPT_PROFILE, 0)
+    launches = st.info().kernel_launches - launches0
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = T_step * args.steps / (ms / 1e3)
+
+    # ---- e2e: the public API end to end with host buffers (gate matrices in, norm + the
+    # first 4096 amplitudes out), timed on the same stream
+    out = np.empty(4096, dtype=np.complex128)
+    h2d = sum(16 * g.U.size + 8 * len(g.ctrl) + 8 for g in gates)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        st.reset(0)
+        st.apply_circuit(gates, fuse=fuse, check=True)      # marshals host gates each step
+        nrm = st.norm()
+        st.amplitudes(0, 4096, out)
+    t_e2e = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_e2e = float(t.item())
+    e2e = {"value": T_step * args.steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": int(8 + 16 * 4096), "norm": nrm}
+
+    hbm, hbm_src = peaks()
+    bytes_per_launch = prof.algorithmic_bytes / max(1, prof.launches)
+    ms_per_launch = prof.kernel_ms / max(1, prof.launches)
+    achieved = bytes_per_launch / (ms_per_launch / 1e3) / 1e9 if prof.launches else None
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tr_path):
+        try:
+            traffic = json.load(open(tr_path)).get(f"config{args.config}")
+        except Exception:
+            traffic = None
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": CONFIG_NAMES[args.config], "dims_q0_first": dims,
+                       "D": int(np.prod(dims, dtype=object)), "gates": len(gates), "fuse": fuse,
+                       "kernel": args.kernel, "sharded_ranks": world,
+                       "l2": "state (%.1f GB) >> L2 (126 MB): no flush needed" % (16 * np.prod(dims, dtype=object) / 1e9)},
+            "hbm_gbs": 32.0 * value / 1e9,
+            "hbm_frac_of_measured": 32.0 * value / 1e9 / hbm if world == 1 else None,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
+                         "peak_source": hbm_src, "kernel": "gate kernels (all launches of the step)",
+                         "bytes_per_launch": bytes_per_launch, "ms_per_launch": ms_per_launch,
+                         "launches_timed": int(prof.launches)},
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(args.config)
+        print(json.dumps(line), flush=True)
+    st.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

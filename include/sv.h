@@ -1,0 +1,233 @@
+/*
+ * sv.h — C ABI of the B200 mixed-radix statevector engine (arXiv 2410.17876 hot path).
+ *
+ * The library applies single-qudit gates, optionally (multi-)controlled, to a dense
+ * complex128 statevector resident in HBM by the paper's block method: for a gate on
+ * qudit q_k it visits every equivalence class (the d_k amplitudes that differ only in
+ * q_k, Table tab:eq_classes), replaces the class vector x by U x
+ * (PAPER.md:222), and stores it back in place.  Controlled gates touch only classes whose
+ * control digits match.  No tensor product and no D×D operator is
+ * ever formed.
+ *
+ * Conventions (binding for every entry point):
+ *   - dims[] lists the qudits q_0 FIRST; q_0 is the least-significant digit.
+ *     Basis index i = sum_k q_k * b_k with block size b_k = prod_{t<k} d_t.
+ *   - 2 <= d_k <= 16; 1 <= n <= 64; D = prod d_k must fit in uint64.
+ *   - Amplitudes are interleaved (re, im) doubles; index arguments are uint64.
+ *   - U is d×d complex, ROW-major, interleaved (re, im): y_r = sum_c U[r][c] x_c, so column
+ *     c of U is the image of |c>.
+ *   - A control (c, v) fires when floor(i / b_c) mod d_c == v; all controls
+ *     of a gate are ANDed.  A control may not equal the target or repeat.
+ *
+ * Ownership: every host input (dims, ctrl, ctrl_vals, U, gates, amplitude buffers) is read
+ * or copied before the call returns; the caller keeps ownership.  The library owns the
+ * device statevector unless it was adopted with sv_create_ex(ext_device_buf), in which
+ * case the caller's buffer must outlive the handle.
+ *
+ * Errors: every call returns sv_status.  Arguments are validated before any device work,
+ * so on a validation error the state is unchanged.  Asynchronous CUDA faults are sticky:
+ * the next call on the handle reports SV_ERR_CUDA and the handle is unusable afterwards.
+ * sv_last_error() returns a thread-local message for the last failing call.
+ *
+ * Concurrency: one call at a time per handle.  Gate kernels run asynchronously on the
+ * handle's stream; sv_norm, sv_amplitudes, sv_set_amplitudes and sv_sync synchronise it.
+ * Sharded handles are SPMD: every rank makes the same calls with identical arguments.
+ */
+#ifndef SV_H_
+#define SV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(SV_BUILD_LIB) && defined(__GNUC__)
+#define SV_API __attribute__((visibility("default")))
+#else
+#define SV_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sv_state_s *sv_handle;
+
+typedef enum { SV_C128 = 0, SV_C64 = 1 /* not yet supported: SV_ERR_UNSUPPORTED */ } sv_dtype;
+
+typedef enum {
+    SV_OK = 0,
+    SV_ERR_INVALID_ARG = 1,   /* null pointer, bad count, bad handle                     */
+    SV_ERR_DIM = 2,           /* n < 1, n > 64, or some d < 2 or d > 16                  */
+    SV_ERR_OVERFLOW = 3,      /* D = prod d_k overflows uint64                           */
+    SV_ERR_QUDIT_RANGE = 4,   /* target or control index outside [0, n)                  */
+    SV_ERR_CTRL_OVERLAP = 5,  /* a control equals the target                             */
+    SV_ERR_CTRL_DUP = 6,      /* a control qudit repeats                                 */
+    SV_ERR_CTRL_VALUE = 7,    /* control value outside [0, d_c)                          */
+    SV_ERR_NOT_UNITARY = 8,   /* max |U^dag U - I| > 1e-12, or a non-finite entry        */
+    SV_ERR_INDEX_RANGE = 9,   /* basis index / amplitude range outside [0, D)            */
+    SV_ERR_NOMEM = 10,        /* device allocation failed                                */
+    SV_ERR_CUDA = 11,         /* CUDA error (sticky)                                     */
+    SV_ERR_NCCL = 12,         /* NCCL error (sharded mode)                               */
+    SV_ERR_UNSUPPORTED = 13   /* valid request outside what this build implements       */
+} sv_status;
+
+/* One gate of a circuit (sv_apply_circuit).  Pointers are read during the call only. */
+typedef struct {
+    int32_t target;
+    int32_t nctrl;
+    const int32_t *ctrl;
+    const int32_t *ctrl_vals;
+    const double *U;          /* d_target × d_target complex, row-major, interleaved */
+} sv_gate;
+
+/* sv_apply_circuit flags */
+#define SV_FUSE      1u   /* merge same-qudit runs and adjacent-qudit pairs (d_k*d_{k+1} <= 16)
+                             into one gate each before launching          */
+#define SV_NO_CHECK  2u   /* skip the unitarity check (structure checks still run)            */
+#define SV_GRAPH     4u   /* capture the launches in a CUDA graph and replay it               */
+
+/* ---- lifecycle ------------------------------------------------------------------------ */
+
+/* Create a single-GPU state on the current device with its own stream; state = e_0
+ * (PAPER.md:247).  dims: n entries, q_0 first.  *out receives the handle. */
+SV_API sv_status sv_create(const int32_t *dims, int32_t n, sv_dtype dt, sv_handle *out);
+
+/* As sv_create, on `device`, launching on `cuda_stream` (a cudaStream_t, or NULL for a new
+ * stream owned by the handle).  If ext_device_buf is non-NULL it is adopted as the state
+ * (must hold >= 16*D bytes, 16-byte aligned, on `device`; the caller keeps ownership, e.g.
+ * a torch tensor).  The state is set to e_0. */
+SV_API sv_status sv_create_ex(const int32_t *dims, int32_t n, sv_dtype dt, int device,
+                       void *cuda_stream, void *ext_device_buf, size_t ext_bytes,
+                       sv_handle *out);
+
+/* Sharded state over nranks = 2^s GPUs (one process per GPU).  The s most-significant
+ * digits must be qubits; rank r owns global indices [r*D/P, (r+1)*D/P).
+ * nccl_unique_id: the 128-byte ncclUniqueId produced by sv_nccl_unique_id on rank 0 and
+ * broadcast by the caller (e.g. through torch.distributed).  cuda_stream as in sv_create_ex.
+ * rank = -1 creates a LOOPBACK handle: all nranks slices live in this one handle on one
+ * device and the pairwise exchange runs through device copies instead of NCCL (same shard
+ * planner, rank predicates, chunking and combine kernel; a single-GPU testing aid).
+ * nranks = 1 is an ordinary single-GPU state.  Errors: SV_ERR_UNSUPPORTED if the s top
+ * digits are not qubits; SV_ERR_NCCL if NCCL cannot be loaded or initialised. */
+SV_API sv_status sv_create_sharded(const int32_t *dims, int32_t n, sv_dtype dt, int32_t rank,
+                            int32_t nranks, const void *nccl_unique_id, int device,
+                            void *cuda_stream, sv_handle *out);
+SV_API sv_status sv_nccl_unique_id(void *out128);
+
+SV_API sv_status sv_destroy(sv_handle h);
+
+/* State = basis vector e_{basis_index}.  SV_ERR_INDEX_RANGE if basis_index >= D. */
+SV_API sv_status sv_reset(sv_handle h, uint64_t basis_index);
+
+/* ---- the hot path --------------------------------------------------------------------- */
+
+/* Apply U on qudit `target`, controlled on ctrl[0..nctrl) having values ctrl_vals[...]
+ * (ctrl/ctrl_vals may be NULL when nctrl == 0).  Asynchronous on the handle's stream. */
+SV_API sv_status sv_apply_gate(sv_handle h, int32_t target, const int32_t *ctrl,
+                        const int32_t *ctrl_vals, int32_t nctrl, const double *U);
+
+/* Validate all gates first (state untouched on any error), then apply them in order
+ * (gate after gate).  flags: SV_FUSE | SV_NO_CHECK | SV_GRAPH. */
+SV_API sv_status sv_apply_circuit(sv_handle h, const sv_gate *gates, int64_t ngates, uint32_t flags);
+
+/* ---- readback ------------------------------------------------------------------------- */
+
+/* Copy amplitudes [first, first+count) to out (2*count doubles).  Synchronises.
+ * Sharded handles: global indices; collective (the owning ranks broadcast). */
+SV_API sv_status sv_amplitudes(sv_handle h, uint64_t first, uint64_t count, double *out);
+
+/* Overwrite amplitudes [first, first+count) from in (2*count doubles).  Synchronises.
+ * Sharded: global indices; each rank writes the part it owns (collective call). */
+SV_API sv_status sv_set_amplitudes(sv_handle h, uint64_t first, uint64_t count, const double *in);
+
+/* *out = sqrt(sum_i |psi_i|^2), fp64, deterministic two-level tree.  Synchronises.
+ * Sharded: collective (all-reduce of the squared partial norms). */
+SV_API sv_status sv_norm(sv_handle h, double *out);
+
+SV_API sv_status sv_sync(sv_handle h);
+
+SV_API const char *sv_last_error(void);
+
+/* ---- introspection (tests, bench) -------------------------------------------------------- */
+
+typedef struct {
+    uint64_t D;              /* global register size                                    */
+    uint64_t local_D;        /* amplitudes held by this handle (D / nranks)             */
+    int32_t n;
+    int32_t rank, nranks;
+    void *device_ptr;        /* the device statevector (local slice)                    */
+    void *cuda_stream;
+    uint64_t kernel_launches;/* number of this library's kernels launched so far        */
+    uint64_t exchanges;      /* sharded: pairwise exchanges performed                    */
+} sv_info;
+
+SV_API sv_status sv_get_info(sv_handle h, sv_info *out);
+
+/* Engine options (tests/bench): SV_OPT_KERNEL selects the gate kernel family. */
+#define SV_OPT_KERNEL       1   /* 0 = auto, 1 = direct (per-fibre), 2 = tiled (TMA bulk)      */
+#define SV_OPT_TILE_ELEMS   2   /* amplitudes per smem tile (tiled kernel)                       */
+#define SV_OPT_TILE_STAGES  3   /* smem pipeline stages (tiled kernel)                           */
+#define SV_OPT_CTAS_PER_SM  4   /* resident CTAs per SM (tiled kernel)                           */
+#define SV_OPT_PROFILE      5   /* 1 = bracket every gate kernel with CUDA events on the handle's
+                                   stream (read back with sv_profile_read)                        */
+SV_API sv_status sv_set_option(sv_handle h, int32_t option, int64_t value);
+
+/* Per-launch timing of the gate kernels recorded while SV_OPT_PROFILE is on: the summed
+ * device time between the events bracketing each gate launch, the number of launches, and
+ * the algorithmic bytes those launches move (32 B per touched amplitude: one 16 B read and
+ * one 16 B write).  Synchronises; reset != 0 clears the record. */
+typedef struct {
+    uint64_t launches;
+    double kernel_ms;
+    double algorithmic_bytes;
+    double touched;          /* amplitude updates (sum of T over the launched gates)        */
+} sv_profile;
+SV_API sv_status sv_profile_read(sv_handle h, int32_t reset, sv_profile *out);
+
+/* Host-only gate analysis (no device work; usable without a GPU).  Fills `out` with the
+ * classification and launch plan the library would use for this gate on this register. */
+typedef struct {
+    int32_t kind;            /* 0 = general, 1 = monomial (phase/permutation, §2.1-2.2) */
+    int32_t d;               /* target dimension                                           */
+    uint64_t b;              /* target block size b_k                                      */
+    uint64_t fibres;         /* number of control-satisfying classes F = D/(d*prod d_c)      */
+    uint64_t touched;        /* amplitudes that can change (T)               */
+    uint32_t active_mask;    /* monomial: members that move or scale                        */
+    int32_t sigma[16];       /* monomial: member j goes to sigma[j]                         */
+    double unitarity_err;    /* max |U^dag U - I|                                          */
+} sv_gate_plan;
+
+SV_API sv_status sv_plan_gate(const int32_t *dims, int32_t n, int32_t target, const int32_t *ctrl,
+                       const int32_t *ctrl_vals, int32_t nctrl, const double *U,
+                       sv_gate_plan *out);
+
+/* Host-only: the first `count` class representatives (member j = 0 of each
+ * control-satisfying class) in the enumeration order the kernels use, starting at class
+ * id `first` — the mixed-radix digit-insertion decomposer of SURVEY.md §8 a3. */
+SV_API sv_status sv_enumerate_fibres(const int32_t *dims, int32_t n, int32_t target,
+                              const int32_t *ctrl, const int32_t *ctrl_vals, int32_t nctrl,
+                              uint64_t first, uint64_t count, uint64_t *out);
+
+/* Host-only: run the fusion planner (SV_FUSE) on a gate list and return the fused list.
+ * out_gates / out_ctrl / out_vals / out_U are caller arrays with room for ngates gates,
+ * sum(nctrl) controls and ngates*256 complex entries; *out_n receives the fused count.
+ * out_gates[i].target is the LOWER qudit of a fused adjacent pair; out_dims[i] holds the
+ * fused dimension (d_k or d_k*d_{k+1}), out_span[i] = 1 or 2 qudits. */
+SV_API sv_status sv_fuse_plan(const int32_t *dims, int32_t n, const sv_gate *gates, int64_t ngates,
+                       int32_t *out_target, int32_t *out_span, int32_t *out_dim,
+                       int32_t *out_nctrl, int32_t *out_ctrl, int32_t *out_vals,
+                       double *out_U, int64_t *out_n);
+
+/* Host-only (sharded planning): what rank `rank` of `nranks` does for a
+ * gate.  *action: 0 = local apply, 1 = skip (a sharded control is unmet on this rank),
+ * 2 = pairwise exchange with *partner on sharded target qubit.  *beta = this rank's digit
+ * of the sharded target (action 2). */
+SV_API sv_status sv_shard_plan(const int32_t *dims, int32_t n, int32_t nranks, int32_t rank,
+                        int32_t target, const int32_t *ctrl, const int32_t *ctrl_vals,
+                        int32_t nctrl, int32_t *action, int32_t *partner, int32_t *beta);
+
+SV_API const char *sv_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SV_H_ */

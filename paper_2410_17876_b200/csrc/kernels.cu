@@ -1,0 +1,230 @@
+// kernels.cu — sm_100a kernels of the block method (§2.1-2.4).
+//
+// Every kernel visits equivalence classes: the d amplitudes
+// base + j*b_k, j < d, that differ only in the target digit.  The class representatives
+// `base` are produced by the digit-insertion decomposer from a dense
+// class id f in [0, F), so control-unsatisfying classes are never visited (PAPER.md:228
+// brute-force filter replaced by direct enumeration).
+#include <cuda_runtime.h>
+
+#include "sv_internal.h"
+#include "shard.h"
+
+namespace svi {
+
+namespace {
+
+// complex fma helpers: acc += u * x
+__device__ __forceinline__ void cfma(double2 &acc, const double2 u, const double2 x) {
+    acc.x = fma(u.x, x.x, acc.x);
+    acc.x = fma(-u.y, x.y, acc.x);
+    acc.y = fma(u.x, x.y, acc.y);
+    acc.y = fma(u.y, x.x, acc.y);
+}
+__device__ __forceinline__ double2 cmul(const double2 u, const double2 x) {
+    return make_double2(fma(u.x, x.x, -u.y * x.y), fma(u.x, x.y, u.y * x.x));
+}
+
+// ------------------------------------------------------------------------------------------
+// Direct kernel: one class per thread iteration, grid-stride over the class ids.
+// Gather x_j = psi[base + j b_k], y = U x, scatter in place.
+// Coalesced when the lowest removed stride is >= 32 amplitudes (consecutive class ids map to
+// consecutive addresses within each block).
+// ------------------------------------------------------------------------------------------
+template <int DIM, int MD, int KIND>
+__global__ void __launch_bounds__(256) k_gate_direct(const __grid_constant__ GateParams<MD> p) {
+    const int d = DIM ? DIM : p.d;
+    const uint64_t bk = p.bk;
+    const uint64_t step = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t f = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; f < p.F; f += step) {
+        double2 *ptr = p.psi + insert_digits(f, p.nrem, p.rem);
+        double2 x[MD];
+        if (KIND == kGeneral) {
+#pragma unroll
+            for (int j = 0; j < MD; ++j)
+                if (DIM || j < d) x[j] = ptr[(uint64_t)j * bk];
+#pragma unroll
+            for (int i = 0; i < MD; ++i) {
+                if (DIM || i < d) {
+                    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int j = 0; j < MD; ++j)
+                        if (DIM || j < d) cfma(acc, p.U[i * MD + j], x[j]);
+                    ptr[(uint64_t)i * bk] = acc;
+                }
+            }
+        } else {
+            // monomial (§2.1 phase / §2.2 permutation): y_{sigma(j)} = c_j x_j, only
+            // for the members that move or scale.
+#pragma unroll
+            for (int j = 0; j < MD; ++j)
+                if ((DIM || j < d) && ((p.active >> j) & 1)) x[j] = ptr[(uint64_t)j * bk];
+#pragma unroll
+            for (int j = 0; j < MD; ++j)
+                if ((DIM || j < d) && ((p.active >> j) & 1))
+                    ptr[(uint64_t)p.sigma[j] * bk] = cmul(p.U[j], x[j]);
+        }
+    }
+}
+
+template <int MD>
+void fill_params(GateParams<MD> &q, const GatePlan &p, double2 *psi) {
+    q.psi = psi;
+    q.F = p.F;
+    q.bk = p.bk;
+    q.d = p.d;
+    q.kind = p.kind;
+    q.active = p.active;
+    q.nrem = p.nrem;
+    for (int i = 0; i < MD; ++i) q.sigma[i] = (i < p.d) ? p.sigma[i] : i;
+    for (int i = 0; i < p.nrem; ++i) q.rem[i] = p.rem[i];
+    for (int i = 0; i < MD * MD; ++i) q.U[i] = make_double2(0.0, 0.0);
+    if (p.kind == kGeneral) {
+        for (int i = 0; i < p.d; ++i)
+            for (int j = 0; j < p.d; ++j) q.U[i * MD + j] = p.U[i * p.d + j];
+    } else {
+        for (int j = 0; j < p.d; ++j) q.U[j] = p.U[j];
+    }
+}
+
+template <int DIM, int MD>
+cudaError_t launch_direct_t(const GatePlan &p, double2 *psi, cudaStream_t st, const LaunchCfg &cfg) {
+    GateParams<MD> q;
+    fill_params<MD>(q, p, psi);
+    const uint64_t want = (p.F + 255) / 256;
+    const uint64_t cap = (uint64_t)cfg.num_sms * 16;
+    const unsigned blocks = (unsigned)(want < cap ? want : cap);
+    if (p.kind == kGeneral)
+        k_gate_direct<DIM, MD, kGeneral><<<blocks, 256, 0, st>>>(q);
+    else
+        k_gate_direct<DIM, MD, kMonomial><<<blocks, 256, 0, st>>>(q);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// Norm: deterministic two-level tree (fixed partition, fixed reduction order).
+// ------------------------------------------------------------------------------------------
+constexpr int kNormParts = 1184;   // 8 per SM on 148 SMs
+constexpr int kNormThreads = 256;
+
+__global__ void __launch_bounds__(kNormThreads) k_norm_partial(const double2 *__restrict__ psi,
+                                                               uint64_t D, double *partial) {
+    __shared__ double red[kNormThreads];
+    const uint64_t chunk = (D + gridDim.x - 1) / gridDim.x;
+    const uint64_t lo = (uint64_t)blockIdx.x * chunk;
+    const uint64_t hi = lo + chunk < D ? lo + chunk : D;
+    double s = 0.0;
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += kNormThreads) {
+        const double2 a = psi[i];
+        s = fma(a.x, a.x, s);
+        s = fma(a.y, a.y, s);
+    }
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = kNormThreads / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+__global__ void __launch_bounds__(kNormThreads) k_norm_final(const double *partial, int n, double *out) {
+    __shared__ double red[kNormThreads];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += kNormThreads) s += partial[i];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = kNormThreads / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = red[0];
+}
+
+
+// ------------------------------------------------------------------------------------------
+// Sharded exchange combine (SURVEY.md §8(e) rule iii): the class of a sharded target qubit
+// has one member on this rank and one on the partner, at the same local index.
+// psi_loc <- a psi_loc + b psi_partner where the local control digits match.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_combine(double2 *__restrict__ loc,
+                                                 const double2 *__restrict__ par, uint64_t n,
+                                                 uint64_t base, double2 a, double2 b,
+                                                 const __grid_constant__ CombineCtrl cc) {
+    const uint64_t step = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += step) {
+        bool ok = true;
+        for (int c = 0; c < cc.nctrl; ++c) {
+            uint64_t r, r2;
+            const uint64_t q = fastdiv64(base + i, cc.b[c], cc.mb[c], r);
+            fastdiv64(q, cc.d[c], cc.md[c], r2);
+            ok = ok && (r2 == cc.v[c]);
+        }
+        if (ok) {
+            const double2 x = loc[i], z = par[i];
+            double2 y = make_double2(0.0, 0.0);
+            cfma(y, a, x);
+            cfma(y, b, z);
+            loc[i] = y;
+        }
+    }
+}
+
+__global__ void k_set_one(double2 *psi, uint64_t idx) { psi[idx] = make_double2(1.0, 0.0); }
+
+}  // namespace
+
+cudaError_t launch_tiled(const GatePlan &p, double2 *psi, cudaStream_t st, const LaunchCfg &cfg,
+                         uint64_t *launches, bool *handled);
+
+cudaError_t launch_gate(const GatePlan &p, double2 *psi, cudaStream_t st, const LaunchCfg &cfg,
+                        uint64_t *launches) {
+    if (p.F == 0) return cudaSuccess;
+    if (cfg.kernel != 1) {
+        bool handled = false;
+        cudaError_t e = launch_tiled(p, psi, st, cfg, launches, &handled);
+        if (handled || e != cudaSuccess) return e;
+    }
+    cudaError_t e;
+    switch (p.d) {
+        case 2: e = launch_direct_t<2, 2>(p, psi, st, cfg); break;
+        case 3: e = launch_direct_t<3, 3>(p, psi, st, cfg); break;
+        case 4: e = launch_direct_t<4, 4>(p, psi, st, cfg); break;
+        case 5: e = launch_direct_t<5, 5>(p, psi, st, cfg); break;
+        default: e = launch_direct_t<0, kMaxDim>(p, psi, st, cfg); break;
+    }
+    if (e == cudaSuccess && launches) ++*launches;
+    return e;
+}
+
+cudaError_t launch_set_basis(double2 *psi, uint64_t D, uint64_t idx, cudaStream_t st,
+                             uint64_t *launches) {
+    cudaError_t e = cudaMemsetAsync(psi, 0, D * sizeof(double2), st);
+    if (e != cudaSuccess) return e;
+    k_set_one<<<1, 1, 0, st>>>(psi, idx);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+}
+
+int norm_parts() { return kNormParts; }
+
+cudaError_t launch_combine(double2 *loc, const double2 *partner, uint64_t n, uint64_t base,
+                           double2 a, double2 b, const CombineCtrl &cc, cudaStream_t st,
+                           uint64_t *launches) {
+    if (n == 0) return cudaSuccess;
+    const uint64_t want = (n + 255) / 256;
+    const unsigned blocks = (unsigned)(want < 148 * 16 ? want : 148 * 16);
+    k_combine<<<blocks, 256, 0, st>>>(loc, partner, n, base, a, b, cc);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_norm2(const double2 *psi, uint64_t D, double *partial, int nparts, double *out,
+                         cudaStream_t st, uint64_t *launches) {
+    k_norm_partial<<<nparts, kNormThreads, 0, st>>>(psi, D, partial);
+    k_norm_final<<<1, kNormThreads, 0, st>>>(partial, nparts, out);
+    if (launches) *launches += 2;
+    return cudaGetLastError();
+}
+
+}  // namespace svi

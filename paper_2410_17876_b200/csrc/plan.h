@@ -1,0 +1,61 @@
+// plan.h — host-side register model, gate validation/classification and launch planning.
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "sv_internal.h"
+#include "../../include/sv.h"
+
+namespace svi {
+
+// Register model: dims q_0 first, b_k = prod_{t<k} d_t, D.
+struct Register {
+    int n = 0;
+    int dims[64];
+    uint64_t b[64];
+    uint64_t D = 0;
+};
+
+sv_status make_register(const int32_t *dims, int32_t n, Register *reg, std::string *err);
+
+struct CtrlSpec {
+    int q;
+    int v;
+};
+
+// A gate whose target occupies `span` consecutive qudits starting at `target` (span 2 =
+// fused adjacent pair, dimension d_k*d_{k+1}, combined digit j_k + d_k*j_{k+1}).
+struct GateSpec {
+    int target = 0;
+    int span = 1;
+    int d = 0;
+    std::vector<CtrlSpec> ctrl;
+    std::vector<double2> U;   // d*d row-major
+};
+
+// Structural validation (ranges, overlap, duplicates, control values).
+sv_status validate_gate(const Register &reg, int target, const int32_t *ctrl,
+                        const int32_t *vals, int nctrl, const double *U, std::string *err);
+
+// max |U^dag U - I| (NaN/Inf -> +inf)
+double unitarity_error(const double2 *U, int d);
+
+// Build the launch plan (classification per PAPER.md §2.1-2.3, fibre decomposer §8 a3).
+sv_status plan_gate(const Register &reg, const GateSpec &g, bool check_unitary, GatePlan *out,
+                    std::string *err);
+
+// Greedy fusion of consecutive same-qudit / adjacent-qudit gates with identical controls
+// into one gate of dimension <= 16.
+std::vector<GateSpec> fuse_gates(const Register &reg, const std::vector<GateSpec> &in);
+
+// Shard planning.  s = log2(nranks) top digits are sharded qubits.
+struct ShardAction {
+    int action;    // 0 local, 1 skip, 2 exchange
+    int partner;
+    int beta;
+};
+sv_status shard_plan(const Register &reg, int nranks, int rank, int target,
+                     const std::vector<CtrlSpec> &ctrl, ShardAction *out, std::string *err);
+
+}  // namespace svi

@@ -1,0 +1,437 @@
+// shard.cpp — sharded mode over P = 2^s GPUs.
+//
+// The state is split on its s most-significant digits, which must be qubits: rank r owns
+// the contiguous slice [r L, (r+1) L), L = D/P, and bit j of r is the digit of q_{n-s+j}.
+// Local strides are unchanged because the sharded digits sit above every local one.
+//   (i)   target and controls local        -> the ordinary local kernel on the slice;
+//   (ii)  a control on a sharded digit     -> rank predicate (skip when unmet);
+//   (iii) target on sharded qubit j        -> pairwise exchange with r ^ 2^j and the combine
+//         psi_loc <- U[beta][beta] psi_loc + U[beta][1-beta] psi_partner on the local indices
+//         whose local control digits match (beta = this rank's digit of q_target): the class
+//         of PAPER.md:198-222 now spans two ranks and the partner holds the other member.
+// Transport: NCCL send/recv over NVLink (one process per GPU; NCCL is dlopen'ed so the core
+// library loads without it), chunked and double-buffered on a comm stream so the transfer of
+// chunk c+1 overlaps the combine of chunk c.  A loopback transport (all P slices in one
+// process on one device, device copies instead of NCCL) exercises the same planner, rank
+// predicates, chunking and combine kernel on a single GPU.
+#include <dlfcn.h>
+
+#include <cstring>
+#include <string>
+
+#include "nccl.h"
+#include "shard.h"
+#include "state.h"
+
+namespace svi {
+
+namespace {
+
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *);
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int);
+    ncclResult_t (*CommDestroy)(ncclComm_t);
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*GroupStart)();
+    ncclResult_t (*GroupEnd)();
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t);
+    ncclResult_t (*Broadcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t,
+                              cudaStream_t);
+    const char *(*GetErrorString)(ncclResult_t);
+};
+
+NcclApi &nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (tried) return api;
+    tried = true;
+    void *lib = nullptr;
+    const char *env = getenv("SV_NCCL_LIB");
+    const char *cands[] = {env, "libnccl.so.2", SV_NCCL_WHEEL_LIB};
+    for (const char *c : cands)
+        if (c && !lib) lib = dlopen(c, RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) { api.why = "libnccl.so.2 not found"; return api; }
+#define SV_SYM(f, name)                                              \
+    api.f = reinterpret_cast<decltype(api.f)>(dlsym(lib, name));     \
+    if (!api.f) { api.why = std::string("missing ") + name; return api; }
+    SV_SYM(GetUniqueId, "ncclGetUniqueId");
+    SV_SYM(CommInitRank, "ncclCommInitRank");
+    SV_SYM(CommDestroy, "ncclCommDestroy");
+    SV_SYM(Send, "ncclSend");
+    SV_SYM(Recv, "ncclRecv");
+    SV_SYM(GroupStart, "ncclGroupStart");
+    SV_SYM(GroupEnd, "ncclGroupEnd");
+    SV_SYM(AllReduce, "ncclAllReduce");
+    SV_SYM(Broadcast, "ncclBroadcast");
+    SV_SYM(GetErrorString, "ncclGetErrorString");
+#undef SV_SYM
+    api.ok = true;
+    return api;
+}
+
+sv_status nccl_fail(sv_handle h, ncclResult_t r, const char *where) {
+    if (h) h->broken = true;
+    return fail_msg(SV_ERR_NCCL, std::string(where) + ": " + nccl().GetErrorString(r));
+}
+
+}  // namespace
+
+struct ShardCtx {
+    int P = 1;
+    int s = 0;
+    int rank = 0;                  // -1: loopback (all ranks in this handle)
+    ncclComm_t comm = nullptr;
+    std::vector<double2 *> slices; // loopback: P slices (slices[0] is h->psi); NCCL: {h->psi}
+    double2 *stage[2] = {nullptr, nullptr};
+    uint64_t chunk = 0;            // amplitudes per exchange chunk
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_recv[2] = {nullptr, nullptr};
+    cudaEvent_t ev_done[2] = {nullptr, nullptr};
+    cudaEvent_t ev_start = nullptr;
+    double *d_scalar = nullptr;
+    bool loopback() const { return rank < 0; }
+};
+
+void shard_destroy(ShardCtx *c) {
+    if (!c) return;
+    if (c->comm) nccl().CommDestroy(c->comm);
+    for (size_t i = 1; i < c->slices.size(); ++i) cudaFree(c->slices[i]);
+    for (double2 *p : c->stage) if (p) cudaFree(p);
+    for (cudaEvent_t e : c->ev_recv) if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->ev_done) if (e) cudaEventDestroy(e);
+    if (c->ev_start) cudaEventDestroy(c->ev_start);
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    if (c->d_scalar) cudaFree(c->d_scalar);
+    delete c;
+}
+
+int shard_rank(const ShardCtx *c) { return c->rank; }
+int shard_nranks(const ShardCtx *c) { return c->P; }
+
+namespace {
+
+std::vector<int> ranks_of(const ShardCtx *c) {
+    std::vector<int> r;
+    if (c->loopback())
+        for (int i = 0; i < c->P; ++i) r.push_back(i);
+    else
+        r.push_back(c->rank);
+    return r;
+}
+
+double2 *slice_of(const ShardCtx *c, int r) { return c->loopback() ? c->slices[r] : c->slices[0]; }
+
+CombineCtrl local_ctrl(const Register &local, const std::vector<CtrlSpec> &ctrl) {
+    CombineCtrl cc;
+    std::memset(&cc, 0, sizeof(cc));
+    for (const auto &c : ctrl) {
+        if (c.q >= local.n) continue;                 // sharded controls: rank predicate
+        const int i = cc.nctrl++;
+        cc.b[i] = local.b[c.q];
+        cc.mb[i] = make_fastdiv64(cc.b[i]).m;
+        cc.d[i] = (uint64_t)local.dims[c.q];
+        cc.md[i] = make_fastdiv64(cc.d[i]).m;
+        cc.v[i] = (uint64_t)c.v;
+    }
+    return cc;
+}
+
+sv_status exchange_nccl(sv_handle h, const GateSpec &g, const ShardAction &a) {
+    ShardCtx *c = h->shard;
+    const double2 A = g.U[a.beta * 2 + a.beta], B = g.U[a.beta * 2 + (1 - a.beta)];
+    const CombineCtrl cc = local_ctrl(h->local, g.ctrl);
+    const uint64_t L = h->local.D;
+    cudaError_t e = cudaEventRecord(c->ev_start, h->stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->comm_stream, c->ev_start, 0);
+    if (e != cudaSuccess) return cuda_fail_h(h, e, "exchange setup");
+    uint64_t k = 0;
+    for (uint64_t off = 0; off < L; off += c->chunk, ++k) {
+        const uint64_t len = (L - off < c->chunk) ? L - off : c->chunk;
+        const int sb = (int)(k & 1);
+        if (k >= 2) cudaStreamWaitEvent(c->comm_stream, c->ev_done[sb], 0);   // stage free again
+        ncclResult_t r = nccl().GroupStart();
+        if (r == ncclSuccess) r = nccl().Send(c->slices[0] + off, 2 * len, ncclFloat64, a.partner, c->comm, c->comm_stream);
+        if (r == ncclSuccess) r = nccl().Recv(c->stage[sb], 2 * len, ncclFloat64, a.partner, c->comm, c->comm_stream);
+        ncclResult_t r2 = nccl().GroupEnd();
+        if (r != ncclSuccess) return nccl_fail(h, r, "ncclSend/Recv");
+        if (r2 != ncclSuccess) return nccl_fail(h, r2, "ncclGroupEnd");
+        e = cudaEventRecord(c->ev_recv[sb], c->comm_stream);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(h->stream, c->ev_recv[sb], 0);
+        if (e == cudaSuccess)
+            e = launch_combine(c->slices[0] + off, c->stage[sb], len, off, A, B, cc, h->stream, &h->launches);
+        if (e == cudaSuccess) e = cudaEventRecord(c->ev_done[sb], h->stream);
+        if (e != cudaSuccess) return cuda_fail_h(h, e, "exchange chunk");
+    }
+    ++h->exchanges;
+    return SV_OK;
+}
+
+sv_status exchange_loopback(sv_handle h, const GateSpec &g, int r, const ShardAction &a,
+                            const ShardAction &ap) {
+    ShardCtx *c = h->shard;
+    const int p = a.partner;
+    const double2 Ar = g.U[a.beta * 2 + a.beta], Br = g.U[a.beta * 2 + (1 - a.beta)];
+    const double2 Ap = g.U[ap.beta * 2 + ap.beta], Bp = g.U[ap.beta * 2 + (1 - ap.beta)];
+    const CombineCtrl cc = local_ctrl(h->local, g.ctrl);
+    const uint64_t L = h->local.D;
+    for (uint64_t off = 0; off < L; off += c->chunk) {
+        const uint64_t len = (L - off < c->chunk) ? L - off : c->chunk;
+        cudaError_t e = cudaMemcpyAsync(c->stage[0], c->slices[r] + off, len * sizeof(double2),
+                                        cudaMemcpyDeviceToDevice, h->stream);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(c->stage[1], c->slices[p] + off, len * sizeof(double2),
+                                cudaMemcpyDeviceToDevice, h->stream);
+        if (e == cudaSuccess)
+            e = launch_combine(c->slices[r] + off, c->stage[1], len, off, Ar, Br, cc, h->stream, &h->launches);
+        if (e == cudaSuccess)
+            e = launch_combine(c->slices[p] + off, c->stage[0], len, off, Ap, Bp, cc, h->stream, &h->launches);
+        if (e != cudaSuccess) return cuda_fail_h(h, e, "loopback exchange");
+    }
+    ++h->exchanges;
+    return SV_OK;
+}
+
+}  // namespace
+
+sv_status shard_apply(sv_handle h, const GateSpec &g, bool check_unitary) {
+    ShardCtx *c = h->shard;
+    std::string *err = err_slot();
+    if (check_unitary) {
+        const double ue = unitarity_error(g.U.data(), g.d);
+        if (!(ue <= 1e-12)) return fail_msg(SV_ERR_NOT_UNITARY, "U is not unitary");
+    }
+    // local view of the gate (sharded controls become the rank predicate)
+    GateSpec gl = g;
+    gl.ctrl.clear();
+    for (const auto &cs : g.ctrl)
+        if (cs.q < h->local.n) gl.ctrl.push_back(cs);
+    std::vector<int> done(c->P, 0);
+    for (int r : ranks_of(c)) {
+        if (done[r]) continue;
+        ShardAction a;
+        sv_status s = shard_plan(h->reg, c->P, r, g.target, g.ctrl, &a, err);
+        if (s != SV_OK) return s;
+        if (a.action == 1) continue;
+        if (a.action == 0) {
+            GatePlan p;
+            s = plan_gate(h->local, gl, false, &p, err);
+            if (s != SV_OK) return s;
+            s = launch_on(h, p, slice_of(c, r));
+            if (s != SV_OK) return s;
+            continue;
+        }
+        if (c->loopback()) {
+            ShardAction ap;
+            s = shard_plan(h->reg, c->P, a.partner, g.target, g.ctrl, &ap, err);
+            if (s != SV_OK) return s;
+            s = exchange_loopback(h, g, r, a, ap);
+            done[a.partner] = 1;
+        } else {
+            s = exchange_nccl(h, g, a);
+        }
+        if (s != SV_OK) return s;
+    }
+    return SV_OK;
+}
+
+sv_status shard_apply_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_t flags) {
+    // Fusion only inside runs of purely local gates (no sharded target or control).
+    std::vector<GateSpec> run;
+    auto flush = [&]() -> sv_status {
+        if (run.empty()) return SV_OK;
+        std::vector<GateSpec> f = (flags & SV_FUSE) ? fuse_gates(h->local, run) : run;
+        run.clear();
+        for (const GateSpec &g : f) {
+            GatePlan p;
+            sv_status s = plan_gate(h->local, g, false, &p, err_slot());
+            if (s != SV_OK) return s;
+            for (int r : ranks_of(h->shard)) {
+                sv_status s2 = launch_on(h, p, slice_of(h->shard, r));
+                if (s2 != SV_OK) return s2;
+            }
+        }
+        return SV_OK;
+    };
+    for (const GateSpec &g : specs) {
+        bool local = g.target < h->local.n;
+        for (const auto &c : g.ctrl) local = local && c.q < h->local.n;
+        if (local) { run.push_back(g); continue; }
+        sv_status s = flush();
+        if (s != SV_OK) return s;
+        s = shard_apply(h, g, false);
+        if (s != SV_OK) return s;
+    }
+    return flush();
+}
+
+sv_status shard_reset(sv_handle h, uint64_t idx) {
+    ShardCtx *c = h->shard;
+    const uint64_t L = h->local.D;
+    const int owner = (int)(idx / L);
+    for (int r : ranks_of(c)) {
+        cudaError_t e;
+        if (r == owner)
+            e = launch_set_basis(slice_of(c, r), L, idx - (uint64_t)owner * L, h->stream, &h->launches);
+        else
+            e = cudaMemsetAsync(slice_of(c, r), 0, L * sizeof(double2), h->stream);
+        if (e != cudaSuccess) return cuda_fail_h(h, e, "sharded reset");
+    }
+    return SV_OK;
+}
+
+sv_status shard_set_amplitudes(sv_handle h, uint64_t first, uint64_t count, const double *in) {
+    ShardCtx *c = h->shard;
+    const uint64_t L = h->local.D;
+    for (int r : ranks_of(c)) {
+        const uint64_t lo = (uint64_t)r * L, hi = lo + L;
+        const uint64_t a = first > lo ? first : lo, b = (first + count) < hi ? first + count : hi;
+        if (a >= b) continue;
+        cudaError_t e = cudaMemcpyAsync(slice_of(c, r) + (a - lo), in + 2 * (a - first),
+                                        (b - a) * sizeof(double2), cudaMemcpyHostToDevice, h->stream);
+        if (e != cudaSuccess) return cuda_fail_h(h, e, "sharded upload");
+    }
+    cudaError_t e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return cuda_fail_h(h, e, "sharded upload");
+    return SV_OK;
+}
+
+sv_status shard_amplitudes(sv_handle h, uint64_t first, uint64_t count, double *out) {
+    ShardCtx *c = h->shard;
+    const uint64_t L = h->local.D;
+    for (int r = 0; r < c->P; ++r) {
+        const uint64_t lo = (uint64_t)r * L, hi = lo + L;
+        const uint64_t a = first > lo ? first : lo, b = (first + count) < hi ? first + count : hi;
+        if (a >= b) continue;
+        if (c->loopback()) {
+            cudaError_t e = cudaMemcpyAsync(out + 2 * (a - first), c->slices[r] + (a - lo),
+                                            (b - a) * sizeof(double2), cudaMemcpyDeviceToHost, h->stream);
+            if (e != cudaSuccess) return cuda_fail_h(h, e, "sharded readback");
+            continue;
+        }
+        for (uint64_t p = a; p < b; p += c->chunk) {     // owner broadcasts, chunk by chunk
+            const uint64_t len = (b - p < c->chunk) ? b - p : c->chunk;
+            const void *src = (r == c->rank) ? (const void *)(c->slices[0] + (p - lo)) : nullptr;
+            ncclResult_t rr = nccl().Broadcast(src ? src : c->stage[0], c->stage[0], 2 * len,
+                                               ncclFloat64, r, c->comm, h->stream);
+            if (rr != ncclSuccess) return nccl_fail(h, rr, "ncclBroadcast");
+            cudaError_t e = cudaMemcpyAsync(out + 2 * (p - first), c->stage[0], len * sizeof(double2),
+                                            cudaMemcpyDeviceToHost, h->stream);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+            if (e != cudaSuccess) return cuda_fail_h(h, e, "sharded readback");
+        }
+    }
+    cudaError_t e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return cuda_fail_h(h, e, "sharded readback");
+    return SV_OK;
+}
+
+sv_status shard_allreduce_sum(sv_handle h, double *v) {
+    ShardCtx *c = h->shard;
+    if (c->loopback()) {   // local_norm2 covered slice 0; add the others
+        double2 *keep = h->psi;
+        for (int r = 1; r < c->P; ++r) {
+            double s2 = 0.0;
+            h->psi = c->slices[r];
+            sv_status s = local_norm2(h, &s2);
+            h->psi = keep;
+            if (s != SV_OK) return s;
+            *v += s2;
+        }
+        return SV_OK;
+    }
+    cudaError_t e = cudaMemcpyAsync(c->d_scalar, v, sizeof(double), cudaMemcpyHostToDevice, h->stream);
+    if (e != cudaSuccess) return cuda_fail_h(h, e, "allreduce");
+    ncclResult_t r = nccl().AllReduce(c->d_scalar, c->d_scalar, 1, ncclFloat64, ncclSum, c->comm, h->stream);
+    if (r != ncclSuccess) return nccl_fail(h, r, "ncclAllReduce");
+    e = cudaMemcpyAsync(v, c->d_scalar, sizeof(double), cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return cuda_fail_h(h, e, "allreduce");
+    return SV_OK;
+}
+
+}  // namespace svi
+
+using namespace svi;
+
+extern "C" {
+
+sv_status sv_nccl_unique_id(void *out128) {
+    if (!out128) return fail_msg(SV_ERR_INVALID_ARG, "null out");
+    if (!nccl().ok) return fail_msg(SV_ERR_NCCL, nccl().why);
+    ncclUniqueId id;
+    ncclResult_t r = nccl().GetUniqueId(&id);
+    if (r != ncclSuccess) return nccl_fail(nullptr, r, "ncclGetUniqueId");
+    std::memcpy(out128, &id, sizeof(id));
+    return SV_OK;
+}
+
+sv_status sv_create_sharded(const int32_t *dims, int32_t n, sv_dtype dt, int32_t rank, int32_t nranks,
+                            const void *nccl_unique_id, int device, void *cuda_stream, sv_handle *out) {
+    if (!out) return fail_msg(SV_ERR_INVALID_ARG, "null out");
+    *out = nullptr;
+    if (nranks == 1 && rank <= 0)
+        return sv_create_ex(dims, n, dt, device, cuda_stream, nullptr, 0, out);
+    if (dt != SV_C128) return fail_msg(SV_ERR_UNSUPPORTED, "only complex128 is implemented");
+    if (nranks < 1 || (nranks & (nranks - 1))) return fail_msg(SV_ERR_INVALID_ARG, "nranks must be a power of two");
+    if (rank < -1 || rank >= nranks) return fail_msg(SV_ERR_INVALID_ARG, "rank out of range");
+    sv_handle h = new (std::nothrow) sv_state_s();
+    if (!h) return fail_msg(SV_ERR_NOMEM, "host allocation");
+    std::string *err = err_slot();
+    sv_status s = make_register(dims, n, &h->reg, err);
+    if (s != SV_OK) { delete h; return s; }
+    int sh = 0;
+    while ((1 << sh) < nranks) ++sh;
+    if (sh >= n) { delete h; return fail_msg(SV_ERR_UNSUPPORTED, "need at least one local qudit"); }
+    for (int k = n - sh; k < n; ++k)
+        if (dims[k] != 2) { delete h; return fail_msg(SV_ERR_UNSUPPORTED, "sharded digits must be qubits"); }
+    s = make_register(dims, n - sh, &h->local, err);
+    if (s != SV_OK) { delete h; return s; }
+    ShardCtx *c = new ShardCtx();
+    c->P = nranks;
+    c->s = sh;
+    c->rank = rank;
+    h->shard = c;
+    s = state_init_device(h, device, cuda_stream, nullptr, 0);
+    if (s != SV_OK) { state_free(h); return s; }
+    c->slices.push_back(h->psi);
+    const uint64_t L = h->local.D;
+    cudaError_t e = cudaSuccess;
+    if (c->loopback()) {
+        for (int r = 1; r < nranks && e == cudaSuccess; ++r) {
+            double2 *p = nullptr;
+            e = cudaMalloc(&p, L * sizeof(double2));
+            if (e == cudaSuccess) c->slices.push_back(p);
+        }
+        if (e != cudaSuccess) { cudaGetLastError(); state_free(h); return fail_msg(SV_ERR_NOMEM, "slice allocation"); }
+    } else {
+        if (!nccl_unique_id) { state_free(h); return fail_msg(SV_ERR_INVALID_ARG, "null nccl id"); }
+        if (!nccl().ok) { state_free(h); return fail_msg(SV_ERR_NCCL, nccl().why); }
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_unique_id, sizeof(id));
+        ncclResult_t r = nccl().CommInitRank(&c->comm, nranks, id, rank);
+        if (r != ncclSuccess) { s = nccl_fail(nullptr, r, "ncclCommInitRank"); c->comm = nullptr; state_free(h); return s; }
+    }
+    const char *ch = getenv("SV_EXCHANGE_CHUNK");
+    c->chunk = ch ? strtoull(ch, nullptr, 10) : (16ull << 20);     // 16 Mi amplitudes = 256 MiB
+    if (c->chunk == 0) c->chunk = 16ull << 20;
+    if (c->chunk > L) c->chunk = L;
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaMalloc(&c->stage[i], c->chunk * sizeof(double2));
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_scalar, sizeof(double));
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+        e = cudaEventCreateWithFlags(&c->ev_recv[i], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming);
+    if (e != cudaSuccess) { cudaGetLastError(); state_free(h); return fail_msg(SV_ERR_NOMEM, "exchange buffers"); }
+    s = shard_reset(h, 0);
+    if (s != SV_OK) { state_free(h); return s; }
+    *out = h;
+    return SV_OK;
+}
+
+}  // extern "C"

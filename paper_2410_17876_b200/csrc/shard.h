@@ -1,0 +1,48 @@
+// shard.h — sharded mode: the state is split on its s most-significant
+// qubit digits over P = 2^s ranks; rank r owns global indices [r D/P, (r+1) D/P).
+#pragma once
+
+#include <vector>
+
+#include "plan.h"
+
+struct sv_state_s;
+typedef struct sv_state_s *sv_handle;
+
+namespace svi {
+
+struct ShardCtx;
+
+// implemented in sv_api.cpp
+sv_status state_init_device(sv_handle h, int device, void *cuda_stream, void *ext, size_t ext_bytes);
+void state_free(sv_handle h);
+sv_status local_norm2(sv_handle h, double *out);
+sv_status local_apply(sv_handle h, const GatePlan &p);
+sv_status launch_on(sv_handle h, const GatePlan &p, double2 *buf);
+
+// implemented in shard.cpp
+void shard_destroy(ShardCtx *c);
+int shard_rank(const ShardCtx *c);
+int shard_nranks(const ShardCtx *c);
+sv_status shard_reset(sv_handle h, uint64_t idx);
+sv_status shard_apply(sv_handle h, const GateSpec &g, bool check_unitary);
+sv_status shard_apply_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_t flags);
+sv_status shard_amplitudes(sv_handle h, uint64_t first, uint64_t count, double *out);
+sv_status shard_set_amplitudes(sv_handle h, uint64_t first, uint64_t count, const double *in);
+sv_status shard_allreduce_sum(sv_handle h, double *v);
+
+// device side of the exchange (kernels.cu): psi_loc <- a psi_loc + b psi_partner on the
+// local indices [base, base+n) whose local control digits match.
+struct CombineCtrl {
+    int32_t nctrl;
+    uint64_t b[kMaxRem];
+    uint64_t mb[kMaxRem];     // magic for division by b
+    uint64_t d[kMaxRem];
+    uint64_t md[kMaxRem];     // magic for division by d
+    uint64_t v[kMaxRem];
+};
+cudaError_t launch_combine(double2 *loc, const double2 *partner, uint64_t n, uint64_t base,
+                           double2 a, double2 b, const CombineCtrl &cc, cudaStream_t st,
+                           uint64_t *launches);
+
+}  // namespace svi

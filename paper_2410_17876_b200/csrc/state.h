@@ -1,0 +1,39 @@
+// state.h — the handle behind sv_handle (shared by sv_api.cpp and shard.cpp).
+#pragma once
+
+#include "plan.h"
+#include "shard.h"
+
+#include <vector>
+
+using svi::Register;
+using svi::LaunchCfg;
+using svi::ShardCtx;
+
+struct sv_state_s {
+    Register reg;          // global register
+    Register local;        // register of the local slice (sharded: top s digits removed)
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    double2 *psi = nullptr;
+    bool own_buf = false;
+    double *d_partial = nullptr;   // norm partials + 1 result slot
+    uint64_t launches = 0;
+    uint64_t exchanges = 0;
+    bool broken = false;
+    LaunchCfg cfg{};
+    ShardCtx *shard = nullptr;     // non-null for sharded handles
+    // SV_OPT_PROFILE: events bracketing each gate launch
+    bool profile = false;
+    struct ProfRec { cudaEvent_t a, b; double bytes; double touched; };
+    std::vector<ProfRec> prof;
+    std::vector<cudaEvent_t> ev_pool;
+    // gate-time errors are reported through the thread-local message in sv_api.cpp
+};
+
+namespace svi {
+sv_status fail_msg(sv_status s, const std::string &msg);
+sv_status cuda_fail_h(sv_handle h, cudaError_t e, const char *where);
+std::string *err_slot();
+}

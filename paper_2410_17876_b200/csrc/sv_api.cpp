@@ -1,0 +1,491 @@
+// sv_api.cpp — the C ABI (include/sv.h): handles, validation, planning, launch driver,
+// readback.  Every step of the hot path runs in this library's CUDA kernels; there is no
+// CPU fallback.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "plan.h"
+#include "shard.h"
+#include "state.h"
+
+using namespace svi;
+
+namespace {
+thread_local std::string g_err;
+
+sv_status fail(sv_status s, const std::string &msg) {
+    g_err = msg;
+    return s;
+}
+}  // namespace
+
+
+
+namespace {
+
+sv_status cuda_fail(sv_handle h, cudaError_t e, const char *where) {
+    if (h) h->broken = true;
+    return fail(SV_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+sv_status check_handle(sv_handle h) {
+    if (!h) return fail(SV_ERR_INVALID_ARG, "null handle");
+    if (h->broken) return fail(SV_ERR_CUDA, "handle is unusable after an earlier CUDA fault");
+    return SV_OK;
+}
+
+GateSpec make_spec(const Register &reg, int target, const int32_t *ctrl, const int32_t *vals,
+                   int nctrl, const double *U) {
+    GateSpec g;
+    g.target = target;
+    g.span = 1;
+    g.d = reg.dims[target];
+    for (int i = 0; i < nctrl; ++i) g.ctrl.push_back({ctrl[i], vals[i]});
+    g.U.resize((size_t)g.d * g.d);
+    for (int i = 0; i < g.d * g.d; ++i) g.U[i] = make_double2(U[2 * i], U[2 * i + 1]);
+    return g;
+}
+
+void default_cfg(LaunchCfg &c, int device) {
+    int sms = 148;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) sms = 148;
+    c.kernel = 0;
+    c.tile_elems = 2048;
+    c.tile_stages = 4;
+    c.ctas_per_sm = 2;
+    c.num_sms = sms;
+}
+
+}  // namespace
+
+// --------------------------------------------------------------------- shared internals
+namespace svi {
+
+sv_status fail_msg(sv_status s, const std::string &msg) { return fail(s, msg); }
+sv_status cuda_fail_h(sv_handle h, cudaError_t e, const char *where) { return cuda_fail(h, e, where); }
+std::string *err_slot() { return &g_err; }
+
+sv_status state_init_device(sv_handle h, int device, void *cuda_stream, void *ext, size_t ext_bytes) {
+    h->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaSetDevice");
+    default_cfg(h->cfg, device);
+    if (cuda_stream) {
+        h->stream = (cudaStream_t)cuda_stream;
+    } else {
+        e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaStreamCreate");
+        h->own_stream = true;
+    }
+    const uint64_t bytes = h->local.D * sizeof(double2);
+    if (ext) {
+        if (ext_bytes < bytes || ((uintptr_t)ext & 15))
+            return fail(SV_ERR_INVALID_ARG, "external buffer too small or misaligned");
+        h->psi = (double2 *)ext;
+    } else {
+        e = cudaMalloc(&h->psi, bytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(SV_ERR_NOMEM, "cudaMalloc of " + std::to_string(bytes) + " bytes failed");
+        }
+        h->own_buf = true;
+    }
+    e = cudaMalloc(&h->d_partial, (norm_parts() + 1) * sizeof(double));
+    if (e != cudaSuccess) { cudaGetLastError(); return fail(SV_ERR_NOMEM, "cudaMalloc (norm scratch)"); }
+    return SV_OK;
+}
+
+void state_free(sv_handle h) {
+    if (!h) return;
+    for (auto &r : h->prof) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
+    if (h->shard) shard_destroy(h->shard);
+    if (h->own_buf && h->psi) cudaFree(h->psi);
+    if (h->d_partial) cudaFree(h->d_partial);
+    if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+}
+
+// local sum of squares (device -> host), synchronising
+sv_status local_norm2(sv_handle h, double *out) {
+    cudaError_t e = launch_norm2(h->psi, h->local.D, h->d_partial, norm_parts(),
+                                 h->d_partial + norm_parts(), h->stream, &h->launches);
+    if (e != cudaSuccess) return cuda_fail(h, e, "norm kernel");
+    e = cudaMemcpyAsync(out, h->d_partial + norm_parts(), sizeof(double), cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "norm readback");
+    return SV_OK;
+}
+
+static cudaEvent_t pool_event(sv_handle h) {
+    if (!h->ev_pool.empty()) {
+        cudaEvent_t e = h->ev_pool.back();
+        h->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+sv_status launch_on(sv_handle h, const GatePlan &p, double2 *buf) {
+    if (p.F == 0) return SV_OK;
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (h->profile) {
+        a = pool_event(h);
+        b = pool_event(h);
+        cudaEventRecord(a, h->stream);
+    }
+    cudaError_t e = launch_gate(p, buf, h->stream, h->cfg, &h->launches);
+    if (e != cudaSuccess) return cuda_fail(h, e, "gate kernel launch");
+    if (h->profile) {
+        cudaEventRecord(b, h->stream);
+        h->prof.push_back({a, b, 32.0 * (double)p.touched, (double)p.touched});
+    }
+    return SV_OK;
+}
+
+sv_status local_apply(sv_handle h, const GatePlan &p) { return launch_on(h, p, h->psi); }
+
+}  // namespace svi
+
+// ------------------------------------------------------------------------------ ABI
+extern "C" {
+
+const char *sv_last_error(void) { return g_err.c_str(); }
+
+const char *sv_version(void) { return "paper_2410_17876_b200 sv 0.1 (sm_100a)"; }
+
+sv_status sv_create_ex(const int32_t *dims, int32_t n, sv_dtype dt, int device, void *cuda_stream,
+                       void *ext_device_buf, size_t ext_bytes, sv_handle *out) {
+    if (!out) return fail(SV_ERR_INVALID_ARG, "null out");
+    *out = nullptr;
+    if (dt == SV_C64) return fail(SV_ERR_UNSUPPORTED, "complex64 is not implemented yet");
+    if (dt != SV_C128) return fail(SV_ERR_INVALID_ARG, "unknown dtype");
+    sv_handle h = new (std::nothrow) sv_state_s();
+    if (!h) return fail(SV_ERR_NOMEM, "host allocation");
+    sv_status s = make_register(dims, n, &h->reg, &g_err);
+    if (s != SV_OK) { delete h; return s; }
+    h->local = h->reg;
+    if (h->reg.D > (UINT64_MAX >> 5)) { delete h; return fail(SV_ERR_NOMEM, "state too large"); }
+    s = state_init_device(h, device, cuda_stream, ext_device_buf, ext_bytes);
+    if (s != SV_OK) { state_free(h); return s; }
+    s = sv_reset(h, 0);
+    if (s != SV_OK) { state_free(h); return s; }
+    *out = h;
+    return SV_OK;
+}
+
+sv_status sv_create(const int32_t *dims, int32_t n, sv_dtype dt, sv_handle *out) {
+    Register probe;                       // validate before touching the device
+    sv_status s = make_register(dims, n, &probe, &g_err);
+    if (s != SV_OK) return s;
+    if (!out) return fail(SV_ERR_INVALID_ARG, "null out");
+    if (dt == SV_C64) return fail(SV_ERR_UNSUPPORTED, "complex64 is not implemented yet");
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) { cudaGetLastError(); return fail(SV_ERR_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e)); }
+    return sv_create_ex(dims, n, dt, dev, nullptr, nullptr, 0, out);
+}
+
+sv_status sv_destroy(sv_handle h) {
+    if (!h) return fail(SV_ERR_INVALID_ARG, "null handle");
+    if (h->stream && !h->broken) cudaStreamSynchronize(h->stream);
+    state_free(h);
+    return SV_OK;
+}
+
+sv_status sv_reset(sv_handle h, uint64_t basis_index) {
+    sv_status s = check_handle(h);
+    if (s != SV_OK) return s;
+    if (basis_index >= h->reg.D) return fail(SV_ERR_INDEX_RANGE, "basis index >= D");
+    if (h->shard) return shard_reset(h, basis_index);
+    cudaError_t e = launch_set_basis(h->psi, h->local.D, basis_index, h->stream, &h->launches);
+    if (e != cudaSuccess) return cuda_fail(h, e, "reset");
+    return SV_OK;
+}
+
+sv_status sv_apply_gate(sv_handle h, int32_t target, const int32_t *ctrl, const int32_t *ctrl_vals,
+                        int32_t nctrl, const double *U) {
+    sv_status s = check_handle(h);
+    if (s != SV_OK) return s;
+    s = validate_gate(h->reg, target, ctrl, ctrl_vals, nctrl, U, &g_err);
+    if (s != SV_OK) return s;
+    GateSpec g = make_spec(h->reg, target, ctrl, ctrl_vals, nctrl, U);
+    if (h->shard) return shard_apply(h, g, true);
+    GatePlan p;
+    s = plan_gate(h->local, g, true, &p, &g_err);
+    if (s != SV_OK) return s;
+    return local_apply(h, p);
+}
+
+sv_status sv_apply_circuit(sv_handle h, const sv_gate *gates, int64_t ngates, uint32_t flags) {
+    sv_status s = check_handle(h);
+    if (s != SV_OK) return s;
+    if (ngates < 0 || (ngates > 0 && !gates)) return fail(SV_ERR_INVALID_ARG, "bad gate list");
+    std::vector<GateSpec> specs;
+    specs.reserve((size_t)ngates);
+    for (int64_t i = 0; i < ngates; ++i) {
+        const sv_gate &g = gates[i];
+        s = validate_gate(h->reg, g.target, g.ctrl, g.ctrl_vals, g.nctrl, g.U, &g_err);
+        if (s != SV_OK) { g_err = "gate " + std::to_string(i) + ": " + g_err; return s; }
+        specs.push_back(make_spec(h->reg, g.target, g.ctrl, g.ctrl_vals, g.nctrl, g.U));
+        if (!(flags & SV_NO_CHECK)) {
+            const double err = unitarity_error(specs.back().U.data(), specs.back().d);
+            if (!(err <= 1e-12))
+                return fail(SV_ERR_NOT_UNITARY, "gate " + std::to_string(i) + ": U is not unitary");
+        }
+    }
+    if (h->shard) return shard_apply_circuit(h, specs, flags);
+    if (flags & SV_FUSE) specs = fuse_gates(h->local, specs);
+    std::vector<GatePlan> plans(specs.size());
+    for (size_t i = 0; i < specs.size(); ++i) {
+        s = plan_gate(h->local, specs[i], false, &plans[i], &g_err);
+        if (s != SV_OK) return s;
+    }
+    if (flags & SV_GRAPH) {
+        cudaGraph_t graph;
+        cudaGraphExec_t exec;
+        cudaError_t e = cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal);
+        if (e != cudaSuccess) return cuda_fail(h, e, "graph capture begin");
+        uint64_t n0 = h->launches;
+        for (const GatePlan &p : plans) {
+            if (p.F == 0) continue;
+            e = launch_gate(p, h->psi, h->stream, h->cfg, &h->launches);
+            if (e != cudaSuccess) break;
+        }
+        cudaError_t e2 = cudaStreamEndCapture(h->stream, &graph);
+        if (e != cudaSuccess) return cuda_fail(h, e, "graph capture");
+        if (e2 != cudaSuccess) return cuda_fail(h, e2, "graph capture end");
+        e = cudaGraphInstantiate(&exec, graph, 0);
+        if (e == cudaSuccess) e = cudaGraphLaunch(exec, h->stream);
+        cudaGraphExecDestroy(exec);
+        cudaGraphDestroy(graph);
+        (void)n0;
+        if (e != cudaSuccess) return cuda_fail(h, e, "graph launch");
+        return SV_OK;
+    }
+    for (const GatePlan &p : plans) {
+        s = local_apply(h, p);
+        if (s != SV_OK) return s;
+    }
+    return SV_OK;
+}
+
+sv_status sv_amplitudes(sv_handle h, uint64_t first, uint64_t count, double *out) {
+    sv_status s = check_handle(h);
+    if (s != SV_OK) return s;
+    if (count == 0) return SV_OK;
+    if (!out) return fail(SV_ERR_INVALID_ARG, "null out");
+    if (first >= h->reg.D || count > h->reg.D - first) return fail(SV_ERR_INDEX_RANGE, "range outside [0, D)");
+    if (h->shard) return shard_amplitudes(h, first, count, out);
+    cudaError_t e = cudaMemcpyAsync(out, h->psi + first, count * sizeof(double2), cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "amplitude readback");
+    return SV_OK;
+}
+
+sv_status sv_set_amplitudes(sv_handle h, uint64_t first, uint64_t count, const double *in) {
+    sv_status s = check_handle(h);
+    if (s != SV_OK) return s;
+    if (count == 0) return SV_OK;
+    if (!in) return fail(SV_ERR_INVALID_ARG, "null in");
+    if (first >= h->reg.D || count > h->reg.D - first) return fail(SV_ERR_INDEX_RANGE, "range outside [0, D)");
+    if (h->shard) return shard_set_amplitudes(h, first, count, in);
+    cudaError_t e = cudaMemcpyAsync(h->psi + first, in, count * sizeof(double2), cudaMemcpyHostToDevice, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "amplitude upload");
+    return SV_OK;
+}
+
+sv_status sv_norm(sv_handle h, double *out) {
+    sv_status s = check_handle(h);
+    if (s != SV_OK) return s;
+    if (!out) return fail(SV_ERR_INVALID_ARG, "null out");
+    double s2 = 0.0;
+    s = local_norm2(h, &s2);
+    if (s != SV_OK) return s;
+    if (h->shard) {
+        s = shard_allreduce_sum(h, &s2);
+        if (s != SV_OK) return s;
+    }
+    *out = std::sqrt(s2);
+    return SV_OK;
+}
+
+sv_status sv_sync(sv_handle h) {
+    sv_status s = check_handle(h);
+    if (s != SV_OK) return s;
+    cudaError_t e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "sync");
+    return SV_OK;
+}
+
+sv_status sv_get_info(sv_handle h, sv_info *out) {
+    if (!h || !out) return fail(SV_ERR_INVALID_ARG, "null handle/out");
+    out->D = h->reg.D;
+    out->local_D = h->local.D;
+    out->n = h->reg.n;
+    out->rank = h->shard ? shard_rank(h->shard) : 0;
+    out->nranks = h->shard ? shard_nranks(h->shard) : 1;
+    out->device_ptr = h->psi;
+    out->cuda_stream = h->stream;
+    out->kernel_launches = h->launches;
+    out->exchanges = h->exchanges;
+    return SV_OK;
+}
+
+sv_status sv_set_option(sv_handle h, int32_t option, int64_t value) {
+    if (!h) return fail(SV_ERR_INVALID_ARG, "null handle");
+    switch (option) {
+        case SV_OPT_KERNEL:
+            if (value < 0 || value > 2) return fail(SV_ERR_INVALID_ARG, "kernel must be 0..2");
+            h->cfg.kernel = (int)value;
+            return SV_OK;
+        case SV_OPT_TILE_ELEMS:
+            if (value < 256 || value > 8192 || (value & 63)) return fail(SV_ERR_INVALID_ARG, "tile elems 256..8192, multiple of 64");
+            h->cfg.tile_elems = (int)value;
+            return SV_OK;
+        case SV_OPT_TILE_STAGES:
+            if (value < 2 || value > 8) return fail(SV_ERR_INVALID_ARG, "stages 2..8");
+            h->cfg.tile_stages = (int)value;
+            return SV_OK;
+        case SV_OPT_PROFILE:
+            h->profile = value != 0;
+            return SV_OK;
+        case SV_OPT_CTAS_PER_SM:
+            if (value < 1 || value > 8) return fail(SV_ERR_INVALID_ARG, "ctas per SM 1..8");
+            h->cfg.ctas_per_sm = (int)value;
+            return SV_OK;
+        default:
+            return fail(SV_ERR_INVALID_ARG, "unknown option");
+    }
+}
+
+sv_status sv_profile_read(sv_handle h, int32_t reset, sv_profile *out) {
+    sv_status s = check_handle(h);
+    if (s != SV_OK) return s;
+    if (!out) return fail(SV_ERR_INVALID_ARG, "null out");
+    cudaError_t e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "profile sync");
+    out->launches = h->prof.size();
+    out->kernel_ms = 0.0;
+    out->algorithmic_bytes = 0.0;
+    out->touched = 0.0;
+    for (auto &r : h->prof) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) out->kernel_ms += ms;
+        out->algorithmic_bytes += r.bytes;
+        out->touched += r.touched;
+    }
+    if (reset) {
+        for (auto &r : h->prof) { h->ev_pool.push_back(r.a); h->ev_pool.push_back(r.b); }
+        h->prof.clear();
+    }
+    return SV_OK;
+}
+
+// ------------------------------------------------------------------ host-only planning
+sv_status sv_plan_gate(const int32_t *dims, int32_t n, int32_t target, const int32_t *ctrl,
+                       const int32_t *ctrl_vals, int32_t nctrl, const double *U, sv_gate_plan *out) {
+    if (!out) return fail(SV_ERR_INVALID_ARG, "null out");
+    Register reg;
+    sv_status s = make_register(dims, n, &reg, &g_err);
+    if (s != SV_OK) return s;
+    s = validate_gate(reg, target, ctrl, ctrl_vals, nctrl, U, &g_err);
+    if (s != SV_OK) return s;
+    GateSpec g = make_spec(reg, target, ctrl, ctrl_vals, nctrl, U);
+    GatePlan p;
+    s = plan_gate(reg, g, false, &p, &g_err);
+    if (s != SV_OK) return s;
+    out->kind = p.kind;
+    out->d = p.d;
+    out->b = p.bk;
+    out->fibres = p.F;
+    out->touched = p.touched;
+    out->active_mask = p.active;
+    for (int j = 0; j < 16; ++j) out->sigma[j] = j < p.d ? p.sigma[j] : j;
+    out->unitarity_err = p.uerr;
+    return SV_OK;
+}
+
+sv_status sv_enumerate_fibres(const int32_t *dims, int32_t n, int32_t target, const int32_t *ctrl,
+                              const int32_t *ctrl_vals, int32_t nctrl, uint64_t first,
+                              uint64_t count, uint64_t *out) {
+    Register reg;
+    sv_status s = make_register(dims, n, &reg, &g_err);
+    if (s != SV_OK) return s;
+    if (reg.D >= (1ull << 62)) return fail(SV_ERR_UNSUPPORTED, "enumeration needs D < 2^62");
+    std::vector<double> I(2 * 16 * 16, 0.0);
+    for (int j = 0; j < reg.dims[target < 0 || target >= n ? 0 : target]; ++j) I[2 * (j * reg.dims[target] + j)] = 1.0;
+    s = validate_gate(reg, target, ctrl, ctrl_vals, nctrl, I.data(), &g_err);
+    if (s != SV_OK) return s;
+    GateSpec g = make_spec(reg, target, ctrl, ctrl_vals, nctrl, I.data());
+    g.U[0] = make_double2(0.0, 0.0);    // make it "general" so F counts all classes
+    g.U[1] = make_double2(1.0, 0.0);
+    GatePlan p;
+    s = plan_gate(reg, g, false, &p, &g_err);
+    if (s != SV_OK) return s;
+    if (first > p.F || count > p.F - first) return fail(SV_ERR_INDEX_RANGE, "class ids outside [0, F)");
+    if (count && !out) return fail(SV_ERR_INVALID_ARG, "null out");
+    for (uint64_t i = 0; i < count; ++i) out[i] = insert_digits(first + i, p.nrem, p.rem);
+    return SV_OK;
+}
+
+sv_status sv_fuse_plan(const int32_t *dims, int32_t n, const sv_gate *gates, int64_t ngates,
+                       int32_t *out_target, int32_t *out_span, int32_t *out_dim, int32_t *out_nctrl,
+                       int32_t *out_ctrl, int32_t *out_vals, double *out_U, int64_t *out_n) {
+    Register reg;
+    sv_status s = make_register(dims, n, &reg, &g_err);
+    if (s != SV_OK) return s;
+    if (ngates < 0 || (ngates && !gates) || !out_n) return fail(SV_ERR_INVALID_ARG, "bad arguments");
+    std::vector<GateSpec> specs;
+    for (int64_t i = 0; i < ngates; ++i) {
+        const sv_gate &g = gates[i];
+        s = validate_gate(reg, g.target, g.ctrl, g.ctrl_vals, g.nctrl, g.U, &g_err);
+        if (s != SV_OK) return s;
+        specs.push_back(make_spec(reg, g.target, g.ctrl, g.ctrl_vals, g.nctrl, g.U));
+    }
+    std::vector<GateSpec> f = fuse_gates(reg, specs);
+    int64_t co = 0;
+    for (size_t i = 0; i < f.size(); ++i) {
+        out_target[i] = f[i].target;
+        out_span[i] = f[i].span;
+        out_dim[i] = f[i].d;
+        out_nctrl[i] = (int32_t)f[i].ctrl.size();
+        for (const auto &c : f[i].ctrl) { out_ctrl[co] = c.q; out_vals[co] = c.v; ++co; }
+        for (int k = 0; k < f[i].d * f[i].d; ++k) {
+            out_U[i * 512 + 2 * k] = f[i].U[k].x;
+            out_U[i * 512 + 2 * k + 1] = f[i].U[k].y;
+        }
+    }
+    *out_n = (int64_t)f.size();
+    return SV_OK;
+}
+
+sv_status sv_shard_plan(const int32_t *dims, int32_t n, int32_t nranks, int32_t rank, int32_t target,
+                        const int32_t *ctrl, const int32_t *ctrl_vals, int32_t nctrl,
+                        int32_t *action, int32_t *partner, int32_t *beta) {
+    Register reg;
+    sv_status s = make_register(dims, n, &reg, &g_err);
+    if (s != SV_OK) return s;
+    std::vector<double> I(2 * 256, 0.0);
+    s = validate_gate(reg, target, ctrl, ctrl_vals, nctrl, I.data(), &g_err);
+    if (s != SV_OK) return s;
+    std::vector<CtrlSpec> cs;
+    for (int i = 0; i < nctrl; ++i) cs.push_back({ctrl[i], ctrl_vals[i]});
+    ShardAction a;
+    s = shard_plan(reg, nranks, rank, target, cs, &a, &g_err);
+    if (s != SV_OK) return s;
+    *action = a.action;
+    *partner = a.partner;
+    *beta = a.beta;
+    return SV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,152 @@
+// sv_internal.h — types shared by the host planner (plan.cpp, sv_api.cpp) and the sm_100a
+// kernels (kernels.cu).  Product code; never includes or links anything from oracle/.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace svi {
+
+constexpr int kMaxDim = 16;     // largest (fused) target dimension a kernel accepts
+constexpr int kMaxRem = 32;     // removed-digit runs (target + pinned controls), merged
+constexpr int kMaxInner = 8;    // predicated (inner) controls in the tiled kernel
+
+// ---------------------------------------------------------------------------------------
+// Invariant-divisor 64-bit division (no hardware div in the inner loop).
+// m = floor(2^64 / d) + 1 for d >= 2 gives q_est = umulhi(x, m) in {q, q+1} for every
+// x < 2^63; one signed-remainder test fixes it.  d == 1 is encoded as m == 0.
+// ---------------------------------------------------------------------------------------
+struct FastDiv64 {
+    uint64_t d;
+    uint64_t m;
+};
+
+inline FastDiv64 make_fastdiv64(uint64_t d) {
+    FastDiv64 f;
+    f.d = d;
+    f.m = (d <= 1) ? 0 : (uint64_t)(((unsigned __int128)1 << 64) / d) + 1;
+    return f;
+}
+
+__host__ __device__ __forceinline__ uint64_t umulhi64(uint64_t a, uint64_t b) {
+#ifdef __CUDA_ARCH__
+    return __umul64hi(a, b);
+#else
+    return (uint64_t)(((unsigned __int128)a * b) >> 64);
+#endif
+}
+
+// q = x / f.d, r = x % f.d
+__host__ __device__ __forceinline__ uint64_t fastdiv64(uint64_t x, uint64_t d, uint64_t m,
+                                                      uint64_t &r) {
+    if (m == 0) { r = 0; return x; }
+    uint64_t q = umulhi64(x, m);
+    uint64_t rr = x - q * d;
+    if ((int64_t)rr < 0) { --q; rr += d; }
+    r = rr;
+    return q;
+}
+
+// 32-bit flavour for in-tile arithmetic (x < 2^31).
+struct FastDiv32 {
+    uint32_t d;
+    uint32_t m;
+};
+inline FastDiv32 make_fastdiv32(uint32_t d) {
+    FastDiv32 f;
+    f.d = d;
+    f.m = (d <= 1) ? 0 : (uint32_t)((((uint64_t)1) << 32) / d) + 1;
+    return f;
+}
+__host__ __device__ __forceinline__ uint32_t fastdiv32(uint32_t x, uint32_t d, uint32_t m,
+                                                      uint32_t &r) {
+    if (m == 0) { r = 0; return x; }
+#ifdef __CUDA_ARCH__
+    uint32_t q = __umulhi(x, m);
+#else
+    uint32_t q = (uint32_t)(((uint64_t)x * m) >> 32);
+#endif
+    uint32_t rr = x - q * d;
+    if ((int32_t)rr < 0) { --q; rr += d; }
+    r = rr;
+    return q;
+}
+
+// ---------------------------------------------------------------------------------------
+// One removed-digit run of the fibre decomposer.  Removing the target digit (pin 0) and
+// every pinned control digit (pin v) from the index leaves the "compressed" class id
+// f in [0, F); re-inserting them in ascending stride order rebuilds the class
+// representative:  base <- (base / b) * (b*d) + pin*b + base % b.
+// Consecutive removed positions are merged into one run (dims multiply, pins combine).
+// ---------------------------------------------------------------------------------------
+struct RemovedRun {
+    uint64_t b;      // global stride of the run's lowest digit
+    uint64_t bd;     // b * (product of the run's dims)
+    uint64_t pinb;   // pin * b
+    uint64_t m;      // magic for division by b
+};
+
+__host__ __device__ __forceinline__ uint64_t insert_digits(uint64_t f, int nrem,
+                                                          const RemovedRun *rem) {
+    uint64_t base = f;
+    for (int i = 0; i < nrem; ++i) {
+        uint64_t r;
+        uint64_t q = fastdiv64(base, rem[i].b, rem[i].m, r);
+        base = q * rem[i].bd + rem[i].pinb + r;
+    }
+    return base;
+}
+
+enum GateKind : int32_t { kGeneral = 0, kMonomial = 1 };
+
+// Kernel parameters of one gate launch, passed by value (__grid_constant__).  MD is the
+// compile-time capacity of the target dimension.
+template <int MD>
+struct GateParams {
+    double2 *psi;
+    uint64_t F;          // classes to visit (control-satisfying)
+    uint64_t bk;         // target stride b_k
+    int32_t d;           // target dimension (<= MD)
+    int32_t kind;        // GateKind
+    uint32_t active;     // monomial: members that move / scale
+    int32_t nrem;
+    int32_t sigma[MD];   // monomial: member j -> sigma[j]
+    RemovedRun rem[kMaxRem];
+    double2 U[MD * MD];  // general: row-major U; monomial: U[j] = coefficient of member j
+};
+
+// Host-side plan of one (possibly fused) gate on a (local) register.
+struct GatePlan {
+    int32_t kind;
+    int32_t d;
+    uint64_t bk;
+    uint64_t F;
+    uint64_t touched;
+    uint32_t active;
+    int32_t sigma[kMaxDim];
+    double2 U[kMaxDim * kMaxDim];   // general: row-major; monomial: coefficients
+    double uerr;
+    int32_t nrem;
+    RemovedRun rem[kMaxRem];
+    // tiled-kernel extras (inner controls are checked per class instead of enumerated)
+    int32_t ninner;
+};
+
+// Device entry points (kernels.cu).
+struct LaunchCfg {
+    int kernel;        // 1 = direct, 2 = tiled
+    int tile_elems;
+    int tile_stages;
+    int ctas_per_sm;
+    int num_sms;
+};
+
+cudaError_t launch_gate(const GatePlan &p, double2 *psi, cudaStream_t st, const LaunchCfg &cfg,
+                        uint64_t *launches);
+cudaError_t launch_set_basis(double2 *psi, uint64_t D, uint64_t idx, cudaStream_t st,
+                             uint64_t *launches);
+cudaError_t launch_norm2(const double2 *psi, uint64_t D, double *partial, int nparts,
+                         double *out, cudaStream_t st, uint64_t *launches);
+int norm_parts();
+
+}  // namespace svi

@@ -1,0 +1,302 @@
+"""Thin ctypes binding of the C ABI (include/sv.h) — argument marshalling only.
+
+Every step of the hot path runs in libsv.so's CUDA kernels.  There is no CPU fallback:
+if libsv.so is missing or cannot be loaded, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Iterable, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsv.so")
+
+SV_C128, SV_C64 = 0, 1
+SV_FUSE, SV_NO_CHECK, SV_GRAPH = 1, 2, 4
+SV_OPT_KERNEL, SV_OPT_TILE_ELEMS, SV_OPT_TILE_STAGES, SV_OPT_CTAS_PER_SM, SV_OPT_PROFILE = 1, 2, 3, 4, 5
+
+STATUS = {0: "SV_OK", 1: "SV_ERR_INVALID_ARG", 2: "SV_ERR_DIM", 3: "SV_ERR_OVERFLOW",
+          4: "SV_ERR_QUDIT_RANGE", 5: "SV_ERR_CTRL_OVERLAP", 6: "SV_ERR_CTRL_DUP",
+          7: "SV_ERR_CTRL_VALUE", 8: "SV_ERR_NOT_UNITARY", 9: "SV_ERR_INDEX_RANGE",
+          10: "SV_ERR_NOMEM", 11: "SV_ERR_CUDA", 12: "SV_ERR_NCCL", 13: "SV_ERR_UNSUPPORTED"}
+
+
+class SVError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+class sv_gate(C.Structure):
+    _fields_ = [("target", C.c_int32), ("nctrl", C.c_int32),
+                ("ctrl", C.POINTER(C.c_int32)), ("ctrl_vals", C.POINTER(C.c_int32)),
+                ("U", C.POINTER(C.c_double))]
+
+
+class sv_info(C.Structure):
+    _fields_ = [("D", C.c_uint64), ("local_D", C.c_uint64), ("n", C.c_int32),
+                ("rank", C.c_int32), ("nranks", C.c_int32), ("device_ptr", C.c_void_p),
+                ("cuda_stream", C.c_void_p), ("kernel_launches", C.c_uint64),
+                ("exchanges", C.c_uint64)]
+
+
+class sv_profile(C.Structure):
+    _fields_ = [("launches", C.c_uint64), ("kernel_ms", C.c_double),
+                ("algorithmic_bytes", C.c_double), ("touched", C.c_double)]
+
+
+class sv_gate_plan(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("d", C.c_int32), ("b", C.c_uint64), ("fibres", C.c_uint64),
+                ("touched", C.c_uint64), ("active_mask", C.c_uint32), ("sigma", C.c_int32 * 16),
+                ("unitarity_err", C.c_double)]
+
+
+_i32p = C.POINTER(C.c_int32)
+_dp = C.POINTER(C.c_double)
+_u64p = C.POINTER(C.c_uint64)
+_h = C.c_void_p
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                      "(there is no CPU fallback)")
+_lib = C.CDLL(LIB_PATH)
+
+
+def _sig(name, args, res=C.c_int):
+    f = getattr(_lib, name)
+    f.argtypes = args
+    f.restype = res
+    return f
+
+
+_sig("sv_create", [_i32p, C.c_int32, C.c_int, C.POINTER(_h)])
+_sig("sv_create_ex", [_i32p, C.c_int32, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(_h)])
+_sig("sv_create_sharded", [_i32p, C.c_int32, C.c_int, C.c_int32, C.c_int32, C.c_void_p, C.c_int,
+                           C.c_void_p, C.POINTER(_h)])
+_sig("sv_nccl_unique_id", [C.c_void_p])
+_sig("sv_destroy", [_h])
+_sig("sv_reset", [_h, C.c_uint64])
+_sig("sv_apply_gate", [_h, C.c_int32, _i32p, _i32p, C.c_int32, _dp])
+_sig("sv_apply_circuit", [_h, C.POINTER(sv_gate), C.c_int64, C.c_uint32])
+_sig("sv_amplitudes", [_h, C.c_uint64, C.c_uint64, _dp])
+_sig("sv_set_amplitudes", [_h, C.c_uint64, C.c_uint64, _dp])
+_sig("sv_norm", [_h, _dp])
+_sig("sv_sync", [_h])
+_sig("sv_last_error", [], C.c_char_p)
+_sig("sv_get_info", [_h, C.POINTER(sv_info)])
+_sig("sv_set_option", [_h, C.c_int32, C.c_int64])
+_sig("sv_plan_gate", [_i32p, C.c_int32, C.c_int32, _i32p, _i32p, C.c_int32, _dp, C.POINTER(sv_gate_plan)])
+_sig("sv_enumerate_fibres", [_i32p, C.c_int32, C.c_int32, _i32p, _i32p, C.c_int32, C.c_uint64,
+                             C.c_uint64, _u64p])
+_sig("sv_fuse_plan", [_i32p, C.c_int32, C.POINTER(sv_gate), C.c_int64, _i32p, _i32p, _i32p, _i32p,
+                      _i32p, _i32p, _dp, C.POINTER(C.c_int64)])
+_sig("sv_shard_plan", [_i32p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _i32p, _i32p, C.c_int32,
+                       _i32p, _i32p, _i32p])
+_sig("sv_version", [], C.c_char_p)
+_sig("sv_profile_read", [_h, C.c_int32, C.POINTER(sv_profile)])
+
+EXPORTS = ["sv_create", "sv_create_ex", "sv_create_sharded", "sv_nccl_unique_id", "sv_destroy",
+           "sv_reset", "sv_apply_gate", "sv_apply_circuit", "sv_amplitudes", "sv_set_amplitudes",
+           "sv_norm", "sv_sync", "sv_last_error", "sv_get_info", "sv_set_option", "sv_plan_gate",
+           "sv_enumerate_fibres", "sv_fuse_plan", "sv_shard_plan", "sv_version", "sv_profile_read"]
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise SVError(rc, (_lib.sv_last_error() or b"").decode())
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(list(a) if not isinstance(a, np.ndarray) else a,
+                                           dtype=np.int32).reshape(-1))
+
+
+def _cplx(U) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(U, dtype=np.complex128))
+
+
+def _p(a, t):
+    return a.ctypes.data_as(t) if a is not None and a.size else None
+
+
+def version() -> str:
+    return _lib.sv_version().decode()
+
+
+class _GateArray:
+    """Marshals gate objects (target, ctrl, vals, U attributes) into an sv_gate array."""
+
+    def __init__(self, gates: Iterable):
+        gates = list(gates)
+        self.keep = []
+        self.arr = (sv_gate * max(1, len(gates)))()
+        for i, g in enumerate(gates):
+            c, v, U = _i32(g.ctrl), _i32(g.vals), _cplx(g.U)
+            self.keep += [c, v, U]
+            self.arr[i].target = int(g.target)
+            self.arr[i].nctrl = int(c.size)
+            self.arr[i].ctrl = _p(c, _i32p)
+            self.arr[i].ctrl_vals = _p(v, _i32p)
+            self.arr[i].U = U.view(np.float64).ctypes.data_as(_dp)
+        self.n = len(gates)
+
+
+class State:
+    """A dense complex128 statevector on one B200 (or one shard of a sharded state)."""
+
+    def __init__(self, dims: Sequence[int], device: int = 0, stream=None, ext_buffer=None,
+                 ext_bytes: int = 0, _handle=None):
+        self.dims = [int(d) for d in dims]
+        if _handle is not None:
+            self._h = _handle
+            return
+        d = _i32(self.dims)
+        h = _h()
+        _check(_lib.sv_create_ex(d.ctypes.data_as(_i32p), d.size, SV_C128, int(device),
+                                 C.c_void_p(stream) if stream else None,
+                                 C.c_void_p(ext_buffer) if ext_buffer else None,
+                                 int(ext_bytes), C.byref(h)))
+        self._h = h
+
+    @classmethod
+    def sharded(cls, dims, rank: int, nranks: int, nccl_id: bytes | None, device: int = 0,
+                stream=None) -> "State":
+        d = _i32(dims)
+        h = _h()
+        idbuf = C.create_string_buffer(bytes(nccl_id), 128) if nccl_id else None
+        _check(_lib.sv_create_sharded(d.ctypes.data_as(_i32p), d.size, SV_C128, int(rank), int(nranks),
+                                      idbuf, int(device), C.c_void_p(stream) if stream else None,
+                                      C.byref(h)))
+        return cls(dims, _handle=h)
+
+    @classmethod
+    def loopback(cls, dims, nranks: int, device: int = 0) -> "State":
+        return cls.sharded(dims, -1, nranks, None, device)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _check(_lib.sv_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def reset(self, index: int = 0):
+        _check(_lib.sv_reset(self._h, int(index)))
+
+    def apply_gate(self, target: int, U, ctrl=(), vals=()):
+        c, v, Uc = _i32(ctrl), _i32(vals), _cplx(U)
+        _check(_lib.sv_apply_gate(self._h, int(target), _p(c, _i32p), _p(v, _i32p), int(c.size),
+                                  Uc.view(np.float64).ctypes.data_as(_dp)))
+
+    def apply_circuit(self, gates, fuse: bool = False, check: bool = True, graph: bool = False):
+        ga = gates if isinstance(gates, _GateArray) else _GateArray(gates)
+        flags = (SV_FUSE if fuse else 0) | (0 if check else SV_NO_CHECK) | (SV_GRAPH if graph else 0)
+        _check(_lib.sv_apply_circuit(self._h, ga.arr, ga.n, flags))
+
+    def amplitudes(self, first: int = 0, count: int | None = None, out: np.ndarray | None = None) -> np.ndarray:
+        if count is None:
+            count = self.info().D - first
+        if out is None:
+            out = np.empty(int(count), dtype=np.complex128)
+        _check(_lib.sv_amplitudes(self._h, int(first), int(count), out.view(np.float64).ctypes.data_as(_dp)))
+        return out
+
+    def set_amplitudes(self, first: int, values) -> None:
+        v = _cplx(values).reshape(-1)
+        _check(_lib.sv_set_amplitudes(self._h, int(first), v.size, v.view(np.float64).ctypes.data_as(_dp)))
+
+    def norm(self) -> float:
+        out = C.c_double()
+        _check(_lib.sv_norm(self._h, C.byref(out)))
+        return out.value
+
+    def sync(self):
+        _check(_lib.sv_sync(self._h))
+
+    def info(self) -> sv_info:
+        i = sv_info()
+        _check(_lib.sv_get_info(self._h, C.byref(i)))
+        return i
+
+    def set_option(self, option: int, value: int):
+        _check(_lib.sv_set_option(self._h, int(option), int(value)))
+
+    def profile_read(self, reset: bool = True) -> sv_profile:
+        p = sv_profile()
+        _check(_lib.sv_profile_read(self._h, 1 if reset else 0, C.byref(p)))
+        return p
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(_lib.sv_nccl_unique_id(buf))
+    return buf.raw
+
+
+def plan_gate(dims, target, U, ctrl=(), vals=()) -> sv_gate_plan:
+    d, c, v, Uc = _i32(dims), _i32(ctrl), _i32(vals), _cplx(U)
+    out = sv_gate_plan()
+    _check(_lib.sv_plan_gate(d.ctypes.data_as(_i32p), d.size, int(target), _p(c, _i32p), _p(v, _i32p),
+                             int(c.size), Uc.view(np.float64).ctypes.data_as(_dp), C.byref(out)))
+    return out
+
+
+def enumerate_fibres(dims, target, ctrl=(), vals=(), first: int = 0, count: int | None = None) -> np.ndarray:
+    d, c, v = _i32(dims), _i32(ctrl), _i32(vals)
+    if count is None:
+        D = int(np.prod([int(x) for x in dims], dtype=object))
+        cp = 1
+        for q in c:
+            cp *= int(dims[int(q)])
+        count = D // (int(dims[int(target)]) * cp) - first
+    out = np.zeros(max(1, int(count)), dtype=np.uint64)
+    _check(_lib.sv_enumerate_fibres(d.ctypes.data_as(_i32p), d.size, int(target), _p(c, _i32p),
+                                    _p(v, _i32p), int(c.size), int(first), int(count),
+                                    out.ctypes.data_as(_u64p)))
+    return out[:int(count)]
+
+
+def fuse_plan(dims, gates):
+    """Host fusion planner: list of (target, span, dim, ctrl tuple, vals tuple, U ndarray)."""
+    gates = list(gates)
+    ga = _GateArray(gates)
+    n = max(1, len(gates))
+    tot_c = max(1, sum(len(g.ctrl) for g in gates))
+    t, sp, dm, nc = (np.zeros(n, np.int32) for _ in range(4))
+    oc, ov = np.zeros(tot_c, np.int32), np.zeros(tot_c, np.int32)
+    U = np.zeros(n * 512, np.float64)
+    nout = C.c_int64()
+    d = _i32(dims)
+    _check(_lib.sv_fuse_plan(d.ctypes.data_as(_i32p), d.size, ga.arr, ga.n, _p(t, _i32p), _p(sp, _i32p),
+                             _p(dm, _i32p), _p(nc, _i32p), _p(oc, _i32p), _p(ov, _i32p),
+                             U.ctypes.data_as(_dp), C.byref(nout)))
+    res, co = [], 0
+    for i in range(nout.value):
+        k = int(dm[i])
+        u = U[i * 512: i * 512 + 2 * k * k].view(np.complex128).reshape(k, k).copy()
+        res.append((int(t[i]), int(sp[i]), k, tuple(int(x) for x in oc[co:co + nc[i]]),
+                    tuple(int(x) for x in ov[co:co + nc[i]]), u))
+        co += int(nc[i])
+    return res
+
+
+def shard_plan(dims, nranks, rank, target, ctrl=(), vals=()):
+    d, c, v = _i32(dims), _i32(ctrl), _i32(vals)
+    a, p, b = C.c_int32(), C.c_int32(), C.c_int32()
+    _check(_lib.sv_shard_plan(d.ctypes.data_as(_i32p), d.size, int(nranks), int(rank), int(target),
+                              _p(c, _i32p), _p(v, _i32p), int(c.size), C.byref(a), C.byref(p), C.byref(b)))
+    return a.value, p.value, b.value

@@ -1,0 +1,189 @@
+"""Host-side tests of the C-ABI library (no GPU needed): the library loads and exports every
+symbol include/sv.h declares; validation, classification, the fibre decomposer, the fusion
+planner and the shard planner are checked against independent definitions / the oracle."""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_2410_17876_b200 as P
+from paper_2410_17876_b200 import sv as S
+from oracle import blocksim as O2
+from sv_inputs import (Gate, shift_x, clock_z, fourier, hadamard, t_gate, haar_unitary,
+                       permutation_matrix, phase_gate, random_circuit, random_state, config_circuit)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "sv.h")).read()
+    declared = set(re.findall(r"^SV_API\s+[^(]*?\b(sv_\w+)\s*\(", hdr, flags=re.M))
+    assert len(declared) >= 20
+    out = subprocess.check_output(["nm", "-D", "--defined-only", S.LIB_PATH]).decode()
+    exported = {l.split()[-1] for l in out.splitlines() if " T " in l}
+    assert declared <= exported, declared - exported
+    assert set(S.EXPORTS) == declared
+    assert "sm_100a" in P.sv.version()
+
+
+def test_library_is_sm100a_only():
+    out = subprocess.check_output(["/usr/local/cuda/bin/cuobjdump", "--list-elf", S.LIB_PATH]).decode()
+    assert "sm_100a" in out
+    assert "sm_90" not in out and "sm_80" not in out
+
+
+def _err(fn, *a, **k):
+    with pytest.raises(P.SVError) as e:
+        fn(*a, **k)
+    return e.value.name
+
+
+def test_register_validation_before_device_work():
+    assert _err(P.State, [2, 1]) == "SV_ERR_DIM"
+    assert _err(P.State, [2, 17]) == "SV_ERR_DIM"
+    assert _err(P.State, []) == "SV_ERR_DIM"
+    assert _err(P.State, [2] * 65) == "SV_ERR_DIM"
+    assert _err(P.plan_gate, [16] * 16 + [2], 0, np.eye(16)) == "SV_ERR_OVERFLOW"
+
+
+def test_gate_validation_codes():
+    dims = [2, 3, 4]
+    H = hadamard()
+    assert _err(P.plan_gate, dims, 3, H) == "SV_ERR_QUDIT_RANGE"
+    assert _err(P.plan_gate, dims, 0, H, ctrl=[0], vals=[1]) == "SV_ERR_CTRL_OVERLAP"
+    assert _err(P.plan_gate, dims, 0, H, ctrl=[1, 1], vals=[0, 0]) == "SV_ERR_CTRL_DUP"
+    assert _err(P.plan_gate, dims, 0, H, ctrl=[1], vals=[3]) == "SV_ERR_CTRL_VALUE"
+    assert _err(P.plan_gate, dims, 0, H, ctrl=[5], vals=[0]) == "SV_ERR_QUDIT_RANGE"
+    p = P.plan_gate(dims, 0, np.array([[1, 0], [0, 2]], complex))
+    assert abs(p.unitarity_err - 3.0) < 1e-15          # |4 - 1|
+
+
+def test_classification_and_touched_counts():
+    dims = [2, 3, 4, 5]
+    D = 120
+    # permutation X_{+1} on q2 (d=4): monomial, sigma = j+1, every member moves
+    p = P.plan_gate(dims, 2, shift_x(4, 1))
+    assert p.kind == 1 and list(p.sigma[:4]) == [1, 2, 3, 0] and p.active_mask == 0b1111
+    assert p.fibres == D // 4 and p.touched == D and p.b == 6
+    # clock Z_3 on q1: diagonal; member 0 has phase exactly 1 -> untouched (T = D (d-1)/d)
+    p = P.plan_gate(dims, 1, clock_z(3, 1))
+    assert p.kind == 1 and p.active_mask == 0b110 and p.touched == D * 2 // 3
+    # T gate on a qubit: only the |1> block
+    p = P.plan_gate(dims, 0, t_gate())
+    assert p.kind == 1 and p.active_mask == 0b10 and p.touched == D // 2
+    # general gates
+    assert P.plan_gate(dims, 3, fourier(5)).kind == 0
+    assert P.plan_gate(dims, 3, haar_unitary(5, np.random.default_rng(0))).kind == 0
+    # CINC qubit->ququint: fibres D/(5*2), touched D/2
+    p = P.plan_gate(dims, 3, shift_x(5, 1), ctrl=[0], vals=[1])
+    assert p.fibres == D // 10 and p.touched == D // 2
+    # identity: nothing to do
+    assert P.plan_gate(dims, 1, np.eye(3)).fibres == 0
+    # monomial with phases (Y-like) is still monomial: y_{sigma(j)} = c_j x_j
+    Y = np.array([[0, -1j], [1j, 0]])
+    assert P.plan_gate(dims, 0, Y).kind == 1
+
+
+def _brute_bases(dims, target, ctrl, vals):
+    D = int(np.prod(dims))
+    i = np.arange(D)
+    digits, rest = [], i.copy()
+    for d in dims:
+        digits.append(rest % d)
+        rest //= d
+    ok = digits[target] == 0
+    for c, v in zip(ctrl, vals):
+        ok &= digits[c] == v
+    return i[ok]
+
+
+def test_fibre_decomposer_matches_brute_force():
+    """digit insertion yields exactly the satisfying class representatives,
+    in ascending order, for random registers and up to 3 controls (incl. adjacent runs)."""
+    rng = np.random.default_rng(123)
+    for trial in range(300):
+        n = int(rng.integers(1, 7))
+        dims = [int(x) for x in rng.integers(2, 7, size=n)]
+        while np.prod(dims) > 20000:
+            dims = dims[:-1]
+        n = len(dims)
+        t = int(rng.integers(n))
+        others = [q for q in range(n) if q != t]
+        nc = int(rng.integers(0, min(3, len(others)) + 1))
+        ctrl = [int(c) for c in rng.choice(others, size=nc, replace=False)] if nc else []
+        vals = [int(rng.integers(dims[c])) for c in ctrl]
+        got = P.enumerate_fibres(dims, t, ctrl, vals)
+        exp = _brute_bases(dims, t, ctrl, vals)
+        assert np.array_equal(got.astype(np.int64), exp), (dims, t, ctrl, vals)
+
+
+def test_fibre_decomposer_64bit_offsets():
+    """Class ids beyond 2^32 on the c4 register (D = 4.78e9): spot-check against the digits."""
+    dims = config_circuit(4, ngates=0)[0]
+    b = np.cumprod([1] + dims[:-1]).astype(object)
+    for t, ctrl, vals in ((0, [], []), (21, [3], [2]), (7, [0, 21], [4, 1]), (12, [13, 14], [1, 0])):
+        F = int(np.prod(dims, dtype=object)) // (dims[t] * int(np.prod([dims[c] for c in ctrl], dtype=object)))
+        for first in (0, F // 3, F - 5):
+            got = P.enumerate_fibres(dims, t, ctrl, vals, first=first, count=5)
+            for x in got:
+                x = int(x)
+                dg = [(x // int(b[k])) % dims[k] for k in range(len(dims))]
+                assert dg[t] == 0 and all(dg[c] == v for c, v in zip(ctrl, vals))
+            if first == F - 5 and t != 21:
+                assert int(got[-1]) > 2 ** 32            # representatives need 64-bit math
+
+
+def _merged_apply(psi, dims, fused):
+    """Apply one fused gate with the oracle: a span-2 gate on (k, k+1) is a single-qudit gate
+    on the register whose qudits k and k+1 are merged into one digit of dim d_k d_{k+1}
+    (same memory layout: stride b_k, digit j_k + d_k j_{k+1})."""
+    t, span, k, ctrl, vals, U = fused
+    if span == 1:
+        O2.apply(psi, dims, Gate(t, ctrl, vals, U))
+        return
+    md = dims[:t] + [dims[t] * dims[t + 1]] + dims[t + 2:]
+    mc = tuple(c if c < t else c - 1 for c in ctrl)
+    O2.apply(psi, md, Gate(t, mc, vals, U))
+
+
+def test_fusion_planner_preserves_the_circuit():
+    rng = np.random.default_rng(31)
+    for s in range(25):
+        dims = [int(x) for x in rng.integers(2, 5, size=5)]
+        _, gates = random_circuit(500 + s, dims, 40, max_ctrl=1)
+        # add same-qudit and adjacent runs so fusion actually fires
+        extra = []
+        for g in gates:
+            extra.append(g)
+            if rng.random() < 0.5 and g.target + 1 < len(dims) and (g.target + 1) not in g.ctrl:
+                extra.append(Gate(g.target + 1, g.ctrl, g.vals, haar_unitary(dims[g.target + 1], rng)))
+        gates = extra
+        fused = P.fuse_plan(dims, gates)
+        assert len(fused) < len(gates)
+        assert all(f[2] <= 16 for f in fused)
+        psi0 = random_state(int(np.prod(dims)), 900 + s)
+        ref = O2.run(dims, gates, psi0)
+        got = psi0.copy()
+        for f in fused:
+            _merged_apply(got, dims, f)
+        assert np.max(np.abs(got - ref)) < 1e-13
+
+
+def test_shard_plan_rules():
+    """sharded controls -> rank predicate; sharded target -> partner r^2^j."""
+    dims = [3, 3, 2, 2, 2, 2]          # P = 4 shards on q_4, q_5
+    P_ = 4
+    for r in range(P_):
+        assert P.shard_plan(dims, P_, r, 0) == (0, r, 0)
+        a, p, b = P.shard_plan(dims, P_, r, 4)
+        assert a == 2 and p == r ^ 1 and b == (r & 1)
+        a, p, b = P.shard_plan(dims, P_, r, 5)
+        assert a == 2 and p == r ^ 2 and b == (r >> 1) & 1
+        a, _, _ = P.shard_plan(dims, P_, r, 1, ctrl=[5], vals=[1])
+        assert a == (0 if (r >> 1) & 1 == 1 else 1)
+        a, p, _ = P.shard_plan(dims, P_, r, 4, ctrl=[5, 0], vals=[0, 2])
+        assert a == (2 if (r >> 1) & 1 == 0 else 1)
+    assert _err(P.shard_plan, [3, 3, 3], 2, 0, 0) == "SV_ERR_UNSUPPORTED"   # top digit not a qubit
+    assert _err(P.shard_plan, dims, 3, 0, 0) == "SV_ERR_INVALID_ARG"

@@ -1,0 +1,346 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element.
+
+Tolerances (north_star): max |dpsi| <= 1e-10 and | ||psi|| - 1 | <= 1e-10 on normalised
+states; bit-exact (==) for index mappings (permutation-only circuits on an index-labelled
+state).  Every case runs for each gate-kernel family (1 = direct per-class, 2 = TMA-tiled)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from oracle import blocksim as O2  # noqa: E402
+from oracle import kron as O1  # noqa: E402
+from sv_inputs import (Gate, shift_x, clock_z, fourier, hadamard, t_gate, haar_unitary,  # noqa: E402
+                       permutation_matrix, phase_gate, ghz_circuit, worked_example,
+                       random_circuit, adjoint_circuit, labelled_state, random_state,
+                       config_circuit)
+
+KERNELS = [1, 2]
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2410_17876_b200 as P
+    return P
+
+
+def run_gpu(P, dims, gates, psi0=None, kernel=0, fuse=False, graph=False, per_gate=False):
+    with P.State(dims) as st:
+        st.set_option(P.sv.SV_OPT_KERNEL, kernel)
+        if psi0 is not None:
+            st.set_amplitudes(0, psi0)
+        n0 = st.info().kernel_launches
+        if per_gate:
+            for g in gates:
+                st.apply_gate(g.target, g.U, g.ctrl, g.vals)
+        else:
+            st.apply_circuit(gates, fuse=fuse, graph=graph)
+        out = st.amplitudes()
+        nrm = st.norm()
+        launched = st.info().kernel_launches - n0
+    return out, nrm, launched
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_worked_example(P, kernel):
+    dims, gates = worked_example()
+    got, nrm, _ = run_gpu(P, dims, gates, kernel=kernel)
+    s = 1.0 / np.sqrt(3.0)
+    exp = np.zeros(6, complex)
+    exp[[0, 2, 5]] = s
+    assert np.max(np.abs(got - exp)) < 1e-15
+    assert np.flatnonzero(got).tolist() == [0, 2, 5]
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("d,n", [(2, 20), (3, 12), (4, 10), (5, 8), (7, 6), (16, 4)])
+def test_ghz_exact(P, kernel, d, n):
+    dims, gates = ghz_circuit(d, n)
+    got, nrm, _ = run_gpu(P, dims, gates, kernel=kernel)
+    rep = sum(d ** k for k in range(n))
+    idx = [v * rep for v in range(d)]
+    s = 1.0 / np.sqrt(d)
+    assert np.flatnonzero(got).tolist() == idx
+    assert all(got[i].real == s and got[i].imag == 0.0 for i in idx)
+    assert abs(nrm - 1.0) <= 1e-10
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("mode", ["plain", "fuse", "graph", "per_gate"])
+def test_c1_against_kronecker(P, kernel, mode):
+    dims, gates = config_circuit(1)
+    ref = O1.run(dims, gates)
+    got, nrm, launched = run_gpu(P, dims, gates, kernel=kernel, fuse=mode in ("fuse", "graph"),
+                                 graph=mode == "graph", per_gate=mode == "per_gate")
+    assert np.max(np.abs(got - ref)) <= 1e-10
+    assert abs(nrm - 1.0) <= 1e-10
+    assert launched > 0
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("fuse", [False, True])
+def test_c2_against_blocksim(P, kernel, fuse):
+    dims, gates = config_circuit(2)
+    ref = O2.run(dims, gates)
+    got, nrm, _ = run_gpu(P, dims, gates, kernel=kernel, fuse=fuse, graph=fuse)
+    assert np.max(np.abs(got - ref)) <= 1e-10
+    assert abs(nrm - 1.0) <= 1e-10
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_c3_reduced_register(P, kernel):
+    dims, gates = config_circuit(3, nqubits=6)
+    ref = O2.run(dims, gates)
+    got, nrm, _ = run_gpu(P, dims, gates, kernel=kernel, fuse=True)
+    assert np.max(np.abs(got - ref)) <= 1e-10
+    assert abs(nrm - 1.0) <= 1e-10
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_c4_reduced_register(P, kernel):
+    dims, gates = config_circuit(4, nqubits=1)        # D = 9.3e6, every dimension class
+    ref = O2.run(dims, gates)
+    got, nrm, _ = run_gpu(P, dims, gates, kernel=kernel)
+    assert np.max(np.abs(got - ref)) <= 1e-10
+    assert abs(nrm - 1.0) <= 1e-10
+
+
+# ------------------------------------------------ (dimension x stride x kind x controls)
+REGISTERS = {
+    # name: (dims, target) -> target stride b_k
+    "b1": lambda d: ([d, 3, 4, 2, 5], 0),                 # b = 1
+    "b5": lambda d: ([5, d, 3, 2, 4], 1),                 # b = 5 (odd, narrow)
+    "b30": lambda d: ([5, 6, d, 3, 2], 2),                # b = 30 (narrow, < 32)
+    "b64": lambda d: ([4, 16, d, 3, 5], 2),               # b = 64
+    "b2304": lambda d: ([16, 16, 9, d, 3], 3),            # b = 2304 (wide, > tile)
+    "top": lambda d: ([3, 16, 5, 7, d], 4),               # most significant, r = 1
+}
+
+
+def _gate_for(kind, d, rng):
+    if kind == "haar":
+        return haar_unitary(d, rng)
+    if kind == "fourier":
+        return fourier(d)
+    if kind == "phase":
+        return phase_gate(rng.uniform(0, 2 * np.pi, size=d))
+    if kind == "perm":
+        return permutation_matrix(rng.permutation(d))
+    if kind == "clock":
+        return clock_z(d, 1)
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("reg", sorted(REGISTERS))
+@pytest.mark.parametrize("d", [2, 3, 4, 5, 7, 16])
+def test_kernel_matrix(P, kernel, reg, d):
+    rng = np.random.default_rng(1000 + d)
+    dims, t = REGISTERS[reg](d)
+    n = len(dims)
+    D = int(np.prod(dims))
+    psi0 = random_state(D, 77 + d)
+    others = [q for q in range(n) if q != t]
+    below = [q for q in others if q < t]
+    above = [q for q in others if q > t]
+    ctrl_sets = [[]]
+    if below:
+        ctrl_sets.append([below[0]])
+        ctrl_sets.append([below[-1]])                     # adjacent below
+    if above:
+        ctrl_sets.append([above[0]])                      # adjacent above
+        ctrl_sets.append([above[-1]])
+    if below and above:
+        ctrl_sets.append([below[0], above[-1]])
+    if len(others) >= 3:
+        ctrl_sets.append(others[:3])
+    with P.State(dims) as st:
+        st.set_option(P.sv.SV_OPT_KERNEL, kernel)
+        for kind in ("haar", "fourier", "phase", "perm", "clock"):
+            for ctrl in ctrl_sets:
+                vals = [int(rng.integers(dims[c])) for c in ctrl]
+                U = _gate_for(kind, d, rng)
+                st.set_amplitudes(0, psi0)
+                st.apply_gate(t, U, ctrl, vals)
+                got = st.amplitudes()
+                ref = psi0.copy()
+                O2.apply(ref, dims, Gate(t, tuple(ctrl), tuple(vals), U))
+                err = np.max(np.abs(got - ref))
+                assert err <= 1e-12, (kind, ctrl, vals, err)
+                if kind in ("perm", "clock") or not ctrl:
+                    pass
+                # untouched classes are bit-exact
+                if ctrl:
+                    digits = [(np.arange(D) // int(np.prod(dims[:q]))) % dims[q] for q in ctrl]
+                    off = np.ones(D, bool)
+                    for dg, v in zip(digits, vals):
+                        off &= dg == v
+                    assert np.array_equal(got[~off], psi0[~off])
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_fused_dimensions(P, kernel):
+    """Adjacent-pair fusion produces every combined dimension 4..16 (2x2 ... 4x4, 3x5)."""
+    rng = np.random.default_rng(5)
+    for dims in ([2, 2, 3, 5, 4, 4, 3], [3, 3, 2, 4, 5, 2, 2], [4, 4, 2, 3, 3, 5]):
+        D = int(np.prod(dims))
+        gates = []
+        for k in range(len(dims) - 1):
+            gates.append(Gate(k, (), (), haar_unitary(dims[k], rng)))
+            gates.append(Gate(k + 1, (), (), haar_unitary(dims[k + 1], rng)))
+            c = (k + 3) % len(dims)
+            if c not in (k, k + 1):
+                gates.append(Gate(k, (c,), (1,), haar_unitary(dims[k], rng)))
+                gates.append(Gate(k + 1, (c,), (1,), haar_unitary(dims[k + 1], rng)))
+        psi0 = random_state(D, 3)
+        ref = O2.run(dims, gates, psi0)
+        fused = P.fuse_plan(dims, gates)
+        assert len(fused) < len(gates)
+        for graph in (False, True):
+            got, _, _ = run_gpu(P, dims, gates, psi0, kernel=kernel, fuse=True, graph=graph)
+            assert np.max(np.abs(got - ref)) <= 1e-12
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_labelled_permutation_circuits_bit_exact(P, kernel):
+    """Index mappings are bit-exact: X_d, CINC, CNOT, multi-controlled X on the labelled state,
+    compared with == to O-2 and to the closed-form map i -> i + (sigma(v) - v) b_k."""
+    rng = np.random.default_rng(17)
+    for cfg in (1, 3, 4):
+        dims = config_circuit(cfg, ngates=0, nqubits=3 if cfg in (3, 4) else None)[0]
+        n, D = len(dims), int(np.prod(dims))
+        gates = []
+        for _ in range(60):
+            t = int(rng.integers(n))
+            others = [q for q in range(n) if q != t]
+            nc = int(rng.integers(0, 4))
+            ctrl = tuple(int(c) for c in rng.choice(others, size=nc, replace=False))
+            vals = tuple(int(rng.integers(dims[c])) for c in ctrl)
+            U = shift_x(dims[t], int(rng.integers(1, dims[t]))) if rng.random() < 0.6 else \
+                permutation_matrix(rng.permutation(dims[t]))
+            gates.append(Gate(t, ctrl, vals, U))
+        psi0 = labelled_state(0, D)
+        ref = O2.run(dims, gates, psi0)
+        got, _, _ = run_gpu(P, dims, gates, psi0, kernel=kernel)
+        assert np.array_equal(got, ref)
+        # closed form for a single gate
+        g = gates[0]
+        one, _, _ = run_gpu(P, dims, [g], psi0, kernel=kernel)
+        b = int(np.prod(dims[:g.target]))
+        i = np.arange(D)
+        dg = lambda q: (i // int(np.prod(dims[:q]))) % dims[q]
+        ok = np.ones(D, bool)
+        for c, v in zip(g.ctrl, g.vals):
+            ok &= dg(c) == v
+        sig = np.argmax(np.abs(g.U), axis=0)
+        v = dg(g.target)
+        dest = np.where(ok, i + (sig[v] - v) * b, i)
+        exp = np.empty_like(psi0)
+        exp[dest] = psi0
+        assert np.array_equal(one, exp)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_random_sweep_against_kronecker(P, kernel):
+    """SPEC.md:587-style sweep: seeded random circuits, n <= 4, dims 2..5, <= 2 controls."""
+    rng = np.random.default_rng(2024)
+    for s in range(60):
+        n = int(rng.integers(1, 5))
+        dims = [int(x) for x in rng.integers(2, 6, size=n)]
+        _, gates = random_circuit(30_000 + s, dims, int(rng.integers(1, 21)), max_ctrl=2)
+        ref = O1.run(dims, gates)
+        got, nrm, _ = run_gpu(P, dims, gates, kernel=kernel)
+        assert np.max(np.abs(got - ref)) <= 1e-10
+        assert abs(nrm - 1.0) <= 1e-10
+
+
+def test_adjoint_returns_to_basis_state(P):
+    dims, gates = config_circuit(3, nqubits=8)
+    with P.State(dims) as st:
+        st.apply_circuit(gates + adjoint_circuit(gates), fuse=True)
+        a = st.amplitudes()
+    assert abs(a[0] - 1.0) <= 1e-10 and np.max(np.abs(a[1:])) <= 1e-10
+
+
+def test_validation_leaves_state_untouched(P):
+    dims = [2, 3, 4]
+    with P.State(dims) as st:
+        st.apply_gate(1, fourier(3))
+        before = st.amplitudes()
+        bad = [
+            lambda: st.apply_gate(3, hadamard()),
+            lambda: st.apply_gate(0, hadamard(), [0], [1]),
+            lambda: st.apply_gate(0, hadamard(), [1, 1], [0, 0]),
+            lambda: st.apply_gate(0, hadamard(), [1], [3]),
+            lambda: st.apply_gate(0, np.array([[1, 0], [0, 2]], complex)),
+            lambda: st.apply_circuit([Gate(0, (), (), hadamard()), Gate(1, (), (), np.eye(3) * 2)]),
+            lambda: st.amplitudes(20, 10),
+            lambda: st.reset(24),
+        ]
+        names = []
+        for f in bad:
+            with pytest.raises(P.SVError) as e:
+                f()
+            names.append(e.value.name)
+        assert names == ["SV_ERR_QUDIT_RANGE", "SV_ERR_CTRL_OVERLAP", "SV_ERR_CTRL_DUP",
+                         "SV_ERR_CTRL_VALUE", "SV_ERR_NOT_UNITARY", "SV_ERR_NOT_UNITARY",
+                         "SV_ERR_INDEX_RANGE", "SV_ERR_INDEX_RANGE"]
+        assert np.array_equal(st.amplitudes(), before)
+        st.reset(23)
+        a = st.amplitudes()
+        assert a[23] == 1.0 and np.count_nonzero(a) == 1
+
+
+def test_external_torch_buffer_and_stream(P):
+    import torch
+    dims, gates = config_circuit(1)
+    buf = torch.empty(2 * 144, dtype=torch.float64, device="cuda")
+    s = torch.cuda.Stream()
+    with P.State(dims, ext_buffer=buf.data_ptr(), ext_bytes=buf.numel() * 8,
+                 stream=s.cuda_stream) as st:
+        st.apply_circuit(gates)
+        st.sync()
+        got = torch.view_as_complex(buf.view(-1, 2)).cpu().numpy()
+    ref = O1.run(dims, gates)
+    assert np.max(np.abs(got - ref)) <= 1e-10
+
+
+@pytest.mark.parametrize("nranks", [2, 4, 8])
+def test_loopback_sharded_matches_single_state(P, nranks):
+    """Sharded mode with the loopback transport: sharded targets exchange,
+    sharded controls predicate, local gates run per slice; small chunks force pipelining."""
+    import os
+    os.environ["SV_EXCHANGE_CHUNK"] = "1000"
+    try:
+        rng = np.random.default_rng(nranks)
+        dims = [3, 3, 4, 2, 2, 2, 2, 2]
+        n, D = len(dims), int(np.prod(dims))
+        _, gates = random_circuit(99 + nranks, dims, 120, max_ctrl=2)
+        gates += [Gate(7, (), (), hadamard()), Gate(6, (0,), (2,), haar_unitary(2, rng)),
+                  Gate(5, (7,), (1,), shift_x(2, 1)), Gate(1, (6, 7), (1, 0), fourier(3))]
+        psi0 = random_state(D, 5)
+        ref = O2.run(dims, gates, psi0)
+        for fuse in (False, True):
+            with P.State.loopback(dims, nranks) as st:
+                st.set_amplitudes(0, psi0)
+                st.apply_circuit(gates, fuse=fuse)
+                got = st.amplitudes()
+                nrm = st.norm()
+                assert st.info().exchanges > 0
+            assert np.max(np.abs(got - ref)) <= 1e-12
+            assert abs(nrm - 1.0) <= 1e-10
+        # bit-exact labelled permutations across shards
+        perm = [Gate(7, (), (), shift_x(2, 1)), Gate(6, (2,), (3,), shift_x(2, 1)),
+                Gate(2, (7,), (1,), shift_x(4, 3)), Gate(5, (6, 0), (0, 1), shift_x(2, 1))]
+        lab = labelled_state(0, D)
+        with P.State.loopback(dims, nranks) as st:
+            st.set_amplitudes(0, lab)
+            for g in perm:
+                st.apply_gate(g.target, g.U, g.ctrl, g.vals)
+            got = st.amplitudes()
+        assert np.array_equal(got, O2.run(dims, perm, lab))
+    finally:
+        del os.environ["SV_EXCHANGE_CHUNK"]
