@@ -140,6 +140,13 @@ sv_status plan_gate(const Register &reg, const GateSpec &g, bool check_unitary, 
         i = j;
     }
     p.nrem = nrem;
+    p.D = reg.D;
+    p.nctrl = (int32_t)g.ctrl.size();
+    for (size_t i = 0; i < g.ctrl.size(); ++i) {
+        p.cb[i] = reg.b[g.ctrl[i].q];
+        p.cd[i] = (uint32_t)reg.dims[g.ctrl[i].q];
+        p.cv[i] = (uint32_t)g.ctrl[i].v;
+    }
     p.F = reg.D / ((uint64_t)d * ctrl_prod);     // classes satisfying every control
     int nact = 0;
     for (int j = 0; j < d; ++j) nact += (p.active >> j) & 1;

@@ -56,7 +56,7 @@ void default_cfg(LaunchCfg &c, int device) {
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) sms = 148;
     c.kernel = 0;
     c.tile_elems = 2048;
-    c.tile_stages = 4;
+    c.tile_stages = 3;
     c.ctas_per_sm = 2;
     c.num_sms = sms;
 }

@@ -128,8 +128,12 @@ struct GatePlan {
     double uerr;
     int32_t nrem;
     RemovedRun rem[kMaxRem];
-    // tiled-kernel extras (inner controls are checked per class instead of enumerated)
-    int32_t ninner;
+    // what the tiled planner needs: the register size and the raw control list
+    uint64_t D;
+    int32_t nctrl;
+    uint64_t cb[64];      // control strides b_c
+    uint32_t cd[64];      // control dims
+    uint32_t cv[64];      // control values
 };
 
 // Device entry points (kernels.cu).
