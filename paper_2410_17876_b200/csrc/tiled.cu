@@ -409,7 +409,9 @@ bool plan_tiled(const GatePlan &g, double2 *psi, const LaunchCfg &cfg, TileParam
         }
         p.nm = nm;
         p.active = g.active;
-        p.kind = pure ? kTPerm : kTMono;
+        // a pure permutation moves whole pieces without touching smem -- only valid when every
+        // class of the tile fires, i.e. no predicated (inner) control
+        p.kind = (pure && p.ninner == 0) ? kTPerm : kTMono;
     }
     const bool modeN = bk < (uint64_t)kRunMin;
     p.mode = modeN ? kModeN : kModeW;
