@@ -21,6 +21,9 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--kinds", default="haar,cinc,phase")
     ap.add_argument("--targets", default=None)
+    ap.add_argument("--te", type=int, default=None)
+    ap.add_argument("--stages", type=int, default=None)
+    ap.add_argument("--cps", type=int, default=None)
     args = ap.parse_args()
     import torch
     import paper_2410_17876_b200 as P
@@ -31,6 +34,12 @@ def main():
     st = P.State(dims)
     ext = torch.cuda.ExternalStream(st.info().cuda_stream)
     targets = range(n) if args.targets is None else [int(x) for x in args.targets.split(",")]
+    if args.te:
+        st.set_option(P.sv.SV_OPT_TILE_ELEMS, args.te)
+    if args.stages:
+        st.set_option(P.sv.SV_OPT_TILE_STAGES, args.stages)
+    if args.cps:
+        st.set_option(P.sv.SV_OPT_CTAS_PER_SM, args.cps)
     for kernel in [int(k) for k in args.kernels.split(",")]:
         st.set_option(P.sv.SV_OPT_KERNEL, kernel)
         for t in targets:
@@ -55,7 +64,7 @@ def main():
                 st.sync()
                 torch.cuda.synchronize()
                 ms = e0.elapsed_time(e1) / args.reps
-                print(json.dumps({"config": args.config, "kernel": kernel, "target": t, "d": d,
+                print(json.dumps({"config": args.config, "kernel": kernel, "te": args.te, "stages": args.stages, "cps": args.cps, "target": t, "d": d,
                                   "b": int(np.prod(dims[:t], dtype=object)), "kind": kind,
                                   "ctrl": list(ctrl), "touched": int(T), "ms": ms,
                                   "GBps": 32.0 * T / (ms / 1e3) / 1e9}), flush=True)
