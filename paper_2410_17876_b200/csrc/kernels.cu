@@ -180,7 +180,17 @@ cudaError_t launch_tiled(const GatePlan &p, double2 *psi, cudaStream_t st, const
 cudaError_t launch_gate(const GatePlan &p, double2 *psi, cudaStream_t st, const LaunchCfg &cfg,
                         uint64_t *launches) {
     if (p.F == 0) return cudaSuccess;
-    if (cfg.kernel != 1) {
+    // auto policy (measured, profiles/r01/gatebench): the tiled kernel wins on every stride
+    // class, except when a control has stride < 32 amplitudes -- the tiled kernel predicates
+    // such controls (moving every amplitude) while the direct kernel visits only the
+    // satisfying classes.
+    bool use_tiled = cfg.kernel == 2;
+    if (cfg.kernel == 0) {
+        use_tiled = true;
+        for (int i = 0; i < p.nctrl; ++i)
+            if (p.cb[i] < 32) use_tiled = false;
+    }
+    if (use_tiled) {
         bool handled = false;
         cudaError_t e = launch_tiled(p, psi, st, cfg, launches, &handled);
         if (handled || e != cudaSuccess) return e;

@@ -46,6 +46,27 @@ def main():
             d = dims[t]
             for kind in args.kinds.split(","):
                 ctrl, vals = (), ()
+                if kind == "pair":           # two gates on (t, t+1) fused into one d_t*d_{t+1} launch
+                    if t + 1 >= n or dims[t] * dims[t + 1] > 16:
+                        continue
+                    from sv_inputs import Gate
+                    pair = [Gate(t, (), (), haar_unitary(d, rng)), Gate(t + 1, (), (), haar_unitary(dims[t + 1], rng))]
+                    ga = P.sv._GateArray(pair)
+                    st.apply_circuit(ga, fuse=True)
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    st.sync()
+                    e0.record(ext)
+                    for _ in range(args.reps):
+                        st.apply_circuit(ga, fuse=True, check=False)
+                    e1.record(ext)
+                    st.sync()
+                    ms = e0.elapsed_time(e1) / args.reps
+                    T = int(np.prod(dims, dtype=object))
+                    print(json.dumps({"config": args.config, "kernel": kernel, "te": args.te, "stages": args.stages,
+                                      "cps": args.cps, "target": t, "d": d * dims[t + 1],
+                                      "b": int(np.prod(dims[:t], dtype=object)), "kind": "pair", "ctrl": [],
+                                      "touched": T, "ms": ms, "GBps": 32.0 * T / (ms / 1e3) / 1e9}), flush=True)
+                    continue
                 if kind == "haar":
                     U = haar_unitary(d, rng)
                 elif kind == "phase":
