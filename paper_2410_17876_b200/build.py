@@ -31,7 +31,7 @@ def needs_build() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(ROOT, "include", "sv.h"),
+    deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "sv.h"),
                                                               os.path.abspath(__file__)]
     return any(os.path.getmtime(p) > t for p in deps)
 
@@ -40,14 +40,25 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     inc, nccl_lib = _nccl_paths()
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xcompiler", "-fvisibility=hidden", "-Xptxas", "-v" if verbose else "-O3",
-           "-I", os.path.join(ROOT, "include"), "-I", inc,
-           f'-DSV_NCCL_WHEEL_LIB="{nccl_lib}"', "-DSV_BUILD_LIB",
-           "-t", "0", "-o", LIB + ".tmp", *sources(), "-ldl"]
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    common = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+              "-Xcompiler", "-fvisibility=hidden", "-I", os.path.join(ROOT, "include"), "-I", inc,
+              f'-DSV_NCCL_WHEEL_LIB="{nccl_lib}"', "-DSV_BUILD_LIB"]
     if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd)
+        common += ["-Xptxas", "-v"]
+    objs, procs = [], []
+    for src in sources():                       # one nvcc per translation unit, in parallel
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        objs.append(obj)
+        cmd = common + ["-c", src, "-o", obj]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        procs.append((src, subprocess.Popen(cmd)))
+    failed = [s for s, p in procs if p.wait() != 0]
+    if failed:
+        raise RuntimeError("nvcc failed for " + ", ".join(failed))
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-ldl"])
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -201,6 +201,13 @@ cudaError_t launch_gate(const GatePlan &p, double2 *psi, cudaStream_t st, const 
         case 3: e = launch_direct_t<3, 3>(p, psi, st, cfg); break;
         case 4: e = launch_direct_t<4, 4>(p, psi, st, cfg); break;
         case 5: e = launch_direct_t<5, 5>(p, psi, st, cfg); break;
+        case 6: e = launch_direct_t<6, 6>(p, psi, st, cfg); break;
+        case 8: e = launch_direct_t<8, 8>(p, psi, st, cfg); break;
+        case 9: e = launch_direct_t<9, 9>(p, psi, st, cfg); break;
+        case 10: e = launch_direct_t<10, 10>(p, psi, st, cfg); break;
+        case 12: e = launch_direct_t<12, 12>(p, psi, st, cfg); break;
+        case 15: e = launch_direct_t<15, 15>(p, psi, st, cfg); break;
+        case 16: e = launch_direct_t<16, 16>(p, psi, st, cfg); break;
         default: e = launch_direct_t<0, kMaxDim>(p, psi, st, cfg); break;
     }
     if (e == cudaSuccess && launches) ++*launches;
