@@ -104,12 +104,12 @@ def touched_total(dims, gates):
     return tot
 
 
-def cpu_baseline(cfg: int, budget_s: float = 15.0):
+def cpu_baseline(cfg: int, budget_s: float = 20.0):
     """O-2 on a bounded sample: the same recipe on a register with fewer qubits (3), gates
     applied in order until ~budget_s of CPU time."""
     from oracle import blocksim as O2
     from sv_inputs import config_circuit
-    nq = {3: 4, 4: 3, 5: 2}.get(cfg, None)
+    nq = {3: 7, 4: 5, 5: 4}.get(cfg, None)
     dims, gates = config_circuit(cfg, nqubits=nq)
     D = int(np.prod(dims))
     psi = np.zeros(D, dtype=np.complex128)

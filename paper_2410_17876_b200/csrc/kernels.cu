@@ -184,9 +184,11 @@ cudaError_t launch_gate(const GatePlan &p, double2 *psi, cudaStream_t st, const 
     // class, except when a control has stride < 32 amplitudes -- the tiled kernel predicates
     // such controls (moving every amplitude) while the direct kernel visits only the
     // satisfying classes.
+    // Fused targets with d >= 10 are FP64-issue heavy; the direct kernel (more warps per SM)
+    // hides that better than the tiled kernel's compute phase (profiles/r01: d=12/16 pairs).
     bool use_tiled = cfg.kernel == 2;
     if (cfg.kernel == 0) {
-        use_tiled = true;
+        use_tiled = p.d <= 9;
         for (int i = 0; i < p.nctrl; ++i)
             if (p.cb[i] < 32) use_tiled = false;
     }
