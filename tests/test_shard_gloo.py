@@ -1,0 +1,95 @@
+"""World-size-2 (and 4) CPU test of the sharded path's host logic over torch.distributed/gloo.
+
+Each process is one rank: it owns the contiguous slice of the state selected by the
+most-significant qubit digits, asks the library's shard planner (sv_shard_plan) what to do
+for every gate, applies local gates to its slice with the oracle (on the local register),
+and for sharded targets exchanges its slice with the partner (gloo send/recv) and combines
+psi <- U[b][b] psi + U[b][1-b] psi_partner on the local indices whose local controls match
+(SURVEY.md §8(e) rule iii; the combine arithmetic is restated here, independently of the
+CUDA combine kernel).  The gathered result must equal O-2 on the full register."""
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import blocksim as O2
+from sv_inputs import Gate, random_circuit, random_state, hadamard, shift_x, haar_unitary
+
+
+def _local_digits(n_local, dims, D_local):
+    i = np.arange(D_local)
+    out = []
+    for q in range(n_local):
+        out.append((i // int(np.prod(dims[:q], dtype=np.int64))) % dims[q])
+    return out
+
+
+def _worker(rank, world, port, dims, gates, psi0, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2410_17876_b200 as P
+    s = int(np.log2(world))
+    n = len(dims)
+    nl = n - s
+    L = int(np.prod(dims[:nl]))
+    psi = psi0[rank * L:(rank + 1) * L].copy()
+    dg = _local_digits(nl, dims, L)
+    exchanges = 0
+    for g in gates:
+        action, partner, beta = P.shard_plan(dims, world, rank, g.target, g.ctrl, g.vals)
+        if action == 1:
+            continue
+        lc = [(c, v) for c, v in zip(g.ctrl, g.vals) if c < nl]
+        if action == 0:
+            O2.apply(psi, dims[:nl], Gate(g.target, tuple(c for c, _ in lc), tuple(v for _, v in lc), g.U))
+            continue
+        other = np.empty_like(psi)
+        mine = torch.from_numpy(psi.view(np.float64).copy())
+        theirs = torch.from_numpy(other.view(np.float64))
+        reqs = [dist.isend(mine, partner), dist.irecv(theirs, partner)]
+        for r in reqs:
+            r.wait()
+        other = theirs.numpy().view(np.complex128)
+        ok = np.ones(L, dtype=bool)
+        for c, v in lc:
+            ok &= dg[c] == v
+        a, b = g.U[beta, beta], g.U[beta, 1 - beta]
+        psi = np.where(ok, a * psi + b * other, psi)
+        exchanges += 1
+    out = [torch.zeros(2 * L, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(out, torch.from_numpy(psi.view(np.float64).copy()))
+    # the NCCL bootstrap path of bench.py: rank 0's 128-byte id reaches every rank
+    idt = torch.arange(128, dtype=torch.uint8) if rank == 0 else torch.zeros(128, dtype=torch.uint8)
+    dist.broadcast(idt, 0)
+    if rank == 0:
+        q.put((np.concatenate([t.numpy().view(np.complex128) for t in out]), exchanges,
+               bool(torch.equal(idt, torch.arange(128, dtype=torch.uint8)))))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_host_logic_gloo(world):
+    dims = [3, 2, 4, 2, 2, 2]
+    D = int(np.prod(dims))
+    _, gates = random_circuit(4242 + world, dims, 80, max_ctrl=2)
+    rng = np.random.default_rng(world)
+    gates += [Gate(5, (), (), hadamard()), Gate(4, (0,), (2,), haar_unitary(2, rng)),
+              Gate(1, (5, 4), (1, 0), shift_x(2, 1)), Gate(5, (3,), (1,), shift_x(2, 1))]
+    psi0 = random_state(D, 11)
+    ref = O2.run(dims, gates, psi0)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + (os.getpid() % 1000) + world
+    procs = [ctx.Process(target=_worker, args=(r, world, port, dims, gates, psi0, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got, exchanges, id_ok = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert exchanges > 0 and id_ok
+    assert np.max(np.abs(got - ref)) < 1e-12
