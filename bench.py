@@ -249,9 +249,14 @@ def main():
     achieved = bytes_per_launch / (ms_per_launch / 1e3) / 1e9 if prof.launches else None
     traffic = None
     tr_path = os.path.join(ROOT, "profiles", "traffic.json")
+    traffic_note = None
     if os.path.exists(tr_path):
         try:
-            traffic = json.load(open(tr_path)).get(f"config{args.config}")
+            tr = json.load(open(tr_path)).get(f"config{args.config}")
+            # DRAM bytes / algorithmic bytes from one `ncu --set full` capture of the dominant
+            # kernel (reduced register), applied to this run's algorithmic bytes per launch
+            traffic = tr["ratio_dram_to_algorithmic"] * bytes_per_launch
+            traffic_note = tr["source"]
         except Exception:
             traffic = None
 
@@ -269,6 +274,7 @@ def main():
             "hbm_frac_of_measured": 32.0 * value / 1e9 / hbm if world == 1 else None,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
+                         "traffic_source": traffic_note,
                          "peak_source": hbm_src, "kernel": "gate kernels (all launches of the step)",
                          "bytes_per_launch": bytes_per_launch, "ms_per_launch": ms_per_launch,
                          "launches_timed": int(prof.launches)},

@@ -84,6 +84,10 @@ typedef struct {
                              into one gate each before launching          */
 #define SV_NO_CHECK  2u   /* skip the unitarity check (structure checks still run)            */
 #define SV_GRAPH     4u   /* capture the launches in a CUDA graph and replay it               */
+#define SV_BLOCK     8u   /* multi-gate cache-blocked passes: gates are grouped
+                             (commuting gates may be pulled forward) so that one HBM pass applies
+                             every gate whose target lies in a shared-memory tile; takes
+                             precedence over SV_FUSE's pair fusion                               */
 
 /* ---- lifecycle ------------------------------------------------------------------------ */
 
@@ -169,6 +173,7 @@ SV_API sv_status sv_get_info(sv_handle h, sv_info *out);
 #define SV_OPT_CTAS_PER_SM  4   /* resident CTAs per SM (tiled kernel)                           */
 #define SV_OPT_PROFILE      5   /* 1 = bracket every gate kernel with CUDA events on the handle's
                                    stream (read back with sv_profile_read)                        */
+#define SV_OPT_PASS_TILE    6   /* amplitudes per shared-memory tile of SV_BLOCK passes (<= 4096)  */
 SV_API sv_status sv_set_option(sv_handle h, int32_t option, int64_t value);
 
 /* Per-launch timing of the gate kernels recorded while SV_OPT_PROFILE is on: the summed
@@ -216,6 +221,14 @@ SV_API sv_status sv_fuse_plan(const int32_t *dims, int32_t n, const sv_gate *gat
                        int32_t *out_target, int32_t *out_span, int32_t *out_dim,
                        int32_t *out_nctrl, int32_t *out_ctrl, int32_t *out_vals,
                        double *out_U, int64_t *out_n);
+
+/* Host-only: run the SV_BLOCK pass planner (without same-qudit merging) on a gate list.
+ * out_order[i] = index of the i-th gate in application order; out_pass[i] = its pass id;
+ * out_tile[p] = amplitudes per shared-memory tile of pass p (room for ngates entries);
+ * *out_npasses = number of passes.  Gates are only reordered across gates they commute with. */
+SV_API sv_status sv_block_plan(const int32_t *dims, int32_t n, const sv_gate *gates, int64_t ngates,
+                               int64_t tile_cap, int64_t *out_order, int64_t *out_pass,
+                               int64_t *out_tile, int64_t *out_npasses);
 
 /* Host-only (sharded planning): what rank `rank` of `nranks` does for a
  * gate.  *action: 0 = local apply, 1 = skip (a sharded control is unmet on this rank),

@@ -236,6 +236,80 @@ std::vector<GateSpec> fuse_gates(const Register &reg, const std::vector<GateSpec
     return out;
 }
 
+std::vector<GateSpec> merge_same_qudit(const std::vector<GateSpec> &in) {
+    std::vector<GateSpec> out;
+    for (const GateSpec &g : in) {
+        if (!out.empty() && out.back().span == 1 && g.span == 1 && out.back().target == g.target &&
+            same_ctrl(out.back().ctrl, g.ctrl)) {
+            out.back().U = matmul(g.U, out.back().U, g.d);
+            continue;
+        }
+        out.push_back(g);
+    }
+    return out;
+}
+
+// ------------------------------------------------------------------- multi-gate passes
+static bool commute(const GateSpec &a, const GateSpec &b) {
+    if (a.target == b.target) return false;
+    for (const auto &c : b.ctrl)
+        if (c.q == a.target) return false;
+    for (const auto &c : a.ctrl)
+        if (c.q == b.target) return false;
+    return true;
+}
+
+std::vector<PassPlan> plan_passes(const Register &reg, const std::vector<GateSpec> &g, uint64_t tile_cap,
+                                  int max_gates, int window) {
+    std::vector<PassPlan> passes;
+    // forced low prefix: every qudit whose stride is < 32 amplitudes
+    int m0 = 0;
+    while (m0 < reg.n && reg.b[m0] < 32) ++m0;
+    const uint64_t base_tile = (m0 < reg.n) ? reg.b[m0] : reg.D;
+    std::vector<char> done(g.size(), 0);
+    size_t first = 0;
+    while (first < g.size()) {
+        while (first < g.size() && done[first]) ++first;
+        if (first >= g.size()) break;
+        PassPlan pp;
+        pp.m0 = m0;
+        std::vector<char> inq(reg.n, 0);
+        uint64_t tile = base_tile;
+        std::vector<size_t> skipped;
+        int seen = 0;
+        for (size_t i = first; i < g.size() && seen < window && (int)pp.gates.size() < max_gates; ++i) {
+            if (done[i]) continue;
+            ++seen;
+            const GateSpec &x = g[i];
+            bool ok = x.span == 1 && x.ctrl.size() <= 4;
+            for (size_t s : skipped)
+                if (ok && !commute(g[s], x)) ok = false;
+            uint64_t need = tile;
+            if (ok && x.target >= m0 && !inq[x.target]) need = tile * (uint64_t)reg.dims[x.target];
+            if (ok && need > tile_cap) ok = false;
+            if (!ok) {
+                skipped.push_back(i);
+                continue;
+            }
+            if (x.target >= m0 && !inq[x.target]) {
+                inq[x.target] = 1;
+                tile = need;
+            }
+            pp.gates.push_back((int)i);
+            done[i] = 1;
+        }
+        if (pp.gates.empty()) {               // first gate not eligible: single-gate pass
+            pp.gates.push_back((int)first);
+            done[first] = 1;
+        }
+        for (int q = m0; q < reg.n; ++q)
+            if (inq[q]) pp.H.push_back(q);
+        pp.tile = tile;
+        passes.push_back(pp);
+    }
+    return passes;
+}
+
 // ------------------------------------------------------------------------- sharding
 sv_status shard_plan(const Register &reg, int nranks, int rank, int target,
                      const std::vector<CtrlSpec> &ctrl, ShardAction *out, std::string *err) {

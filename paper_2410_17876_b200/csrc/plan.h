@@ -49,6 +49,30 @@ sv_status plan_gate(const Register &reg, const GateSpec &g, bool check_unitary, 
 // into one gate of dimension <= 16.
 std::vector<GateSpec> fuse_gates(const Register &reg, const std::vector<GateSpec> &in);
 
+// Consecutive gates on the same target with identical controls -> one matrix product.
+std::vector<GateSpec> merge_same_qudit(const std::vector<GateSpec> &in);
+
+// Multi-gate cache-blocked passes.  A pass applies several gates to every
+// tile of the state while the tile sits in shared memory: the tile holds all digit values of
+// a set Q of "in-tile" qudits (the low prefix q_0..q_{m0-1} whose stride is < 32 is always
+// included, so every copied piece is >= 32 amplitudes) and one value of every other digit.
+// Gates whose target is in Q can be applied in the pass; their controls may be anywhere.
+// Gates are pulled forward past skipped gates only when they commute with them
+// (different targets, neither target controls the other).
+struct PassPlan {
+    std::vector<int> gates;      // indices into the (merged) gate list, in application order
+    std::vector<int> H;          // in-tile qudits above the low prefix (ascending)
+    int m0 = 0;                  // low prefix q_0..q_{m0-1}
+    uint64_t tile = 0;           // amplitudes per tile = b_{m0} * prod_{h in H} d_h
+};
+std::vector<PassPlan> plan_passes(const Register &reg, const std::vector<GateSpec> &g, uint64_t tile_cap,
+                                  int max_gates, int window);
+
+// Launch one multi-gate pass (mgpass.cu).  *handled = false if the pass does not fit the
+// kernel (the caller then applies its gates one by one); *touched = sum of T over its gates.
+cudaError_t run_pass(const Register &reg, const std::vector<GateSpec> &gates, const PassPlan &pp, double2 *psi,
+                     cudaStream_t st, const LaunchCfg &cfg, bool *handled, double *touched);
+
 // Shard planning.  s = log2(nranks) top digits are sharded qubits.
 struct ShardAction {
     int action;    // 0 local, 1 skip, 2 exchange

@@ -239,21 +239,18 @@ sv_status shard_apply(sv_handle h, const GateSpec &g, bool check_unitary) {
 }
 
 sv_status shard_apply_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_t flags) {
-    // Fusion only inside runs of purely local gates (no sharded target or control).
+    // Runs of purely local gates (no sharded target or control) go through the local circuit
+    // driver on every slice this handle owns (fusion / multi-gate passes included).
     std::vector<GateSpec> run;
     auto flush = [&]() -> sv_status {
         if (run.empty()) return SV_OK;
-        std::vector<GateSpec> f = (flags & SV_FUSE) ? fuse_gates(h->local, run) : run;
-        run.clear();
-        for (const GateSpec &g : f) {
-            GatePlan p;
-            sv_status s = plan_gate(h->local, g, false, &p, err_slot());
+        const uint32_t local_flags = flags & (SV_FUSE | SV_BLOCK);
+        for (int r : ranks_of(h->shard)) {
+            std::vector<GateSpec> copy = run;
+            sv_status s = run_local_circuit(h, copy, local_flags, slice_of(h->shard, r));
             if (s != SV_OK) return s;
-            for (int r : ranks_of(h->shard)) {
-                sv_status s2 = launch_on(h, p, slice_of(h->shard, r));
-                if (s2 != SV_OK) return s2;
-            }
         }
+        run.clear();
         return SV_OK;
     };
     for (const GateSpec &g : specs) {

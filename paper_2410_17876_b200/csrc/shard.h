@@ -19,6 +19,7 @@ void state_free(sv_handle h);
 sv_status local_norm2(sv_handle h, double *out);
 sv_status local_apply(sv_handle h, const GatePlan &p);
 sv_status launch_on(sv_handle h, const GatePlan &p, double2 *buf);
+sv_status run_local_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_t flags, double2 *buf);
 
 // implemented in shard.cpp
 void shard_destroy(ShardCtx *c);

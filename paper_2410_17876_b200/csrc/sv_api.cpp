@@ -59,6 +59,7 @@ void default_cfg(LaunchCfg &c, int device) {
     c.tile_stages = 3;
     c.ctas_per_sm = 2;
     c.num_sms = sms;
+    c.pass_tile = 4096;
 }
 
 }  // namespace
@@ -152,6 +153,87 @@ sv_status launch_on(sv_handle h, const GatePlan &p, double2 *buf) {
 
 sv_status local_apply(sv_handle h, const GatePlan &p) { return launch_on(h, p, h->psi); }
 
+// One multi-gate pass (mgpass.cu); falls back to its gates one by one if the pass kernel
+// cannot take it.
+static sv_status launch_pass_on(sv_handle h, const std::vector<GateSpec> &specs, const PassPlan &pp,
+                                double2 *buf) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (h->profile) {
+        a = pool_event(h);
+        b = pool_event(h);
+        cudaEventRecord(a, h->stream);
+    }
+    bool handled = false;
+    double touched = 0.0;
+    cudaError_t e = run_pass(h->local, specs, pp, buf, h->stream, h->cfg, &handled, &touched);
+    if (e != cudaSuccess) return cuda_fail(h, e, "pass kernel launch");
+    if (handled) {
+        ++h->launches;
+        if (h->profile) {
+            cudaEventRecord(b, h->stream);
+            // a pass moves the local state once: 16 B read + 16 B write per amplitude
+            h->prof.push_back({a, b, 32.0 * (double)h->local.D, touched});
+        }
+        return SV_OK;
+    }
+    if (h->profile) { h->ev_pool.push_back(a); h->ev_pool.push_back(b); }
+    for (int gi : pp.gates) {
+        GatePlan p;
+        sv_status s = plan_gate(h->local, specs[gi], false, &p, &g_err);
+        if (s != SV_OK) return s;
+        s = launch_on(h, p, buf);
+        if (s != SV_OK) return s;
+    }
+    return SV_OK;
+}
+
+// The local circuit driver: plain (gate by gate), SV_FUSE (same-qudit runs + adjacent pairs),
+// SV_BLOCK (multi-gate cache-blocked passes), optionally captured into a CUDA graph.
+sv_status run_local_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_t flags, double2 *buf) {
+    sv_status s = SV_OK;
+    std::vector<PassPlan> passes;
+    if (flags & SV_BLOCK) {
+        specs = merge_same_qudit(specs);
+        passes = plan_passes(h->local, specs, (uint64_t)h->cfg.pass_tile, 24, 64);
+    } else {
+        if (flags & SV_FUSE) specs = fuse_gates(h->local, specs);
+        for (size_t i = 0; i < specs.size(); ++i) {
+            PassPlan pp;
+            pp.gates.push_back((int)i);
+            passes.push_back(pp);
+        }
+    }
+    std::vector<GatePlan> singles(passes.size());
+    for (size_t i = 0; i < passes.size(); ++i)
+        if (passes[i].gates.size() == 1) {
+            s = plan_gate(h->local, specs[passes[i].gates[0]], false, &singles[i], &g_err);
+            if (s != SV_OK) return s;
+        }
+    const bool graph = (flags & SV_GRAPH) != 0;
+    const bool keep_profile = h->profile;
+    if (graph) {
+        h->profile = false;       // events cannot be recorded inside a capture for later reads
+        cudaError_t e = cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal);
+        if (e != cudaSuccess) { h->profile = keep_profile; return cuda_fail(h, e, "graph capture begin"); }
+    }
+    for (size_t i = 0; i < passes.size() && s == SV_OK; ++i)
+        s = (passes[i].gates.size() == 1) ? launch_on(h, singles[i], buf) : launch_pass_on(h, specs, passes[i], buf);
+    if (graph) {
+        h->profile = keep_profile;
+        cudaGraph_t g;
+        cudaError_t e2 = cudaStreamEndCapture(h->stream, &g);
+        if (s != SV_OK) return s;
+        if (e2 != cudaSuccess) return cuda_fail(h, e2, "graph capture end");
+        cudaGraphExec_t exec;
+        cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
+        if (e == cudaSuccess) e = cudaGraphLaunch(exec, h->stream);
+        if (e == cudaSuccess) cudaGraphExecDestroy(exec);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return cuda_fail(h, e, "graph launch");
+    }
+    return s;
+}
+
 }  // namespace svi
 
 // ------------------------------------------------------------------------------ ABI
@@ -242,39 +324,7 @@ sv_status sv_apply_circuit(sv_handle h, const sv_gate *gates, int64_t ngates, ui
         }
     }
     if (h->shard) return shard_apply_circuit(h, specs, flags);
-    if (flags & SV_FUSE) specs = fuse_gates(h->local, specs);
-    std::vector<GatePlan> plans(specs.size());
-    for (size_t i = 0; i < specs.size(); ++i) {
-        s = plan_gate(h->local, specs[i], false, &plans[i], &g_err);
-        if (s != SV_OK) return s;
-    }
-    if (flags & SV_GRAPH) {
-        cudaGraph_t graph;
-        cudaGraphExec_t exec;
-        cudaError_t e = cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal);
-        if (e != cudaSuccess) return cuda_fail(h, e, "graph capture begin");
-        uint64_t n0 = h->launches;
-        for (const GatePlan &p : plans) {
-            if (p.F == 0) continue;
-            e = launch_gate(p, h->psi, h->stream, h->cfg, &h->launches);
-            if (e != cudaSuccess) break;
-        }
-        cudaError_t e2 = cudaStreamEndCapture(h->stream, &graph);
-        if (e != cudaSuccess) return cuda_fail(h, e, "graph capture");
-        if (e2 != cudaSuccess) return cuda_fail(h, e2, "graph capture end");
-        e = cudaGraphInstantiate(&exec, graph, 0);
-        if (e == cudaSuccess) e = cudaGraphLaunch(exec, h->stream);
-        cudaGraphExecDestroy(exec);
-        cudaGraphDestroy(graph);
-        (void)n0;
-        if (e != cudaSuccess) return cuda_fail(h, e, "graph launch");
-        return SV_OK;
-    }
-    for (const GatePlan &p : plans) {
-        s = local_apply(h, p);
-        if (s != SV_OK) return s;
-    }
-    return SV_OK;
+    return run_local_circuit(h, specs, flags, h->psi);
 }
 
 sv_status sv_amplitudes(sv_handle h, uint64_t first, uint64_t count, double *out) {
@@ -357,6 +407,10 @@ sv_status sv_set_option(sv_handle h, int32_t option, int64_t value) {
             return SV_OK;
         case SV_OPT_PROFILE:
             h->profile = value != 0;
+            return SV_OK;
+        case SV_OPT_PASS_TILE:
+            if (value < 256 || value > 4096) return fail(SV_ERR_INVALID_ARG, "pass tile 256..4096");
+            h->cfg.pass_tile = (int)value;
             return SV_OK;
         case SV_OPT_CTAS_PER_SM:
             if (value < 1 || value > 8) return fail(SV_ERR_INVALID_ARG, "ctas per SM 1..8");
@@ -465,6 +519,35 @@ sv_status sv_fuse_plan(const int32_t *dims, int32_t n, const sv_gate *gates, int
         }
     }
     *out_n = (int64_t)f.size();
+    return SV_OK;
+}
+
+sv_status sv_block_plan(const int32_t *dims, int32_t n, const sv_gate *gates, int64_t ngates,
+                        int64_t tile_cap, int64_t *out_order, int64_t *out_pass, int64_t *out_tile,
+                        int64_t *out_npasses) {
+    Register reg;
+    sv_status s = make_register(dims, n, &reg, &g_err);
+    if (s != SV_OK) return s;
+    if (ngates < 0 || (ngates && (!gates || !out_order || !out_pass || !out_tile)) || !out_npasses)
+        return fail(SV_ERR_INVALID_ARG, "bad arguments");
+    std::vector<GateSpec> specs;
+    for (int64_t i = 0; i < ngates; ++i) {
+        const sv_gate &g = gates[i];
+        s = validate_gate(reg, g.target, g.ctrl, g.ctrl_vals, g.nctrl, g.U, &g_err);
+        if (s != SV_OK) return s;
+        specs.push_back(make_spec(reg, g.target, g.ctrl, g.ctrl_vals, g.nctrl, g.U));
+    }
+    std::vector<PassPlan> passes = plan_passes(reg, specs, (uint64_t)tile_cap, 24, 64);
+    int64_t k = 0;
+    for (size_t p = 0; p < passes.size(); ++p) {
+        out_tile[p] = (int64_t)passes[p].tile;
+        for (int gi : passes[p].gates) {
+            out_order[k] = gi;
+            out_pass[k] = (int64_t)p;
+            ++k;
+        }
+    }
+    *out_npasses = (int64_t)passes.size();
     return SV_OK;
 }
 

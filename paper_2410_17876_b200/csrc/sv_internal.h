@@ -143,6 +143,7 @@ struct LaunchCfg {
     int tile_stages;
     int ctas_per_sm;
     int num_sms;
+    int pass_tile;     // amplitudes per smem tile of the multi-gate pass kernel
 };
 
 cudaError_t launch_gate(const GatePlan &p, double2 *psi, cudaStream_t st, const LaunchCfg &cfg,

@@ -15,8 +15,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsv.so")
 
 SV_C128, SV_C64 = 0, 1
-SV_FUSE, SV_NO_CHECK, SV_GRAPH = 1, 2, 4
-SV_OPT_KERNEL, SV_OPT_TILE_ELEMS, SV_OPT_TILE_STAGES, SV_OPT_CTAS_PER_SM, SV_OPT_PROFILE = 1, 2, 3, 4, 5
+SV_FUSE, SV_NO_CHECK, SV_GRAPH, SV_BLOCK = 1, 2, 4, 8
+SV_OPT_KERNEL, SV_OPT_TILE_ELEMS, SV_OPT_TILE_STAGES, SV_OPT_CTAS_PER_SM, SV_OPT_PROFILE, SV_OPT_PASS_TILE = 1, 2, 3, 4, 5, 6
 
 STATUS = {0: "SV_OK", 1: "SV_ERR_INVALID_ARG", 2: "SV_ERR_DIM", 3: "SV_ERR_OVERFLOW",
           4: "SV_ERR_QUDIT_RANGE", 5: "SV_ERR_CTRL_OVERLAP", 6: "SV_ERR_CTRL_DUP",
@@ -98,11 +98,13 @@ _sig("sv_shard_plan", [_i32p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _i32p,
                        _i32p, _i32p, _i32p])
 _sig("sv_version", [], C.c_char_p)
 _sig("sv_profile_read", [_h, C.c_int32, C.POINTER(sv_profile)])
+_sig("sv_block_plan", [_i32p, C.c_int32, C.POINTER(sv_gate), C.c_int64, C.c_int64, C.POINTER(C.c_int64),
+                       C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)])
 
 EXPORTS = ["sv_create", "sv_create_ex", "sv_create_sharded", "sv_nccl_unique_id", "sv_destroy",
            "sv_reset", "sv_apply_gate", "sv_apply_circuit", "sv_amplitudes", "sv_set_amplitudes",
            "sv_norm", "sv_sync", "sv_last_error", "sv_get_info", "sv_set_option", "sv_plan_gate",
-           "sv_enumerate_fibres", "sv_fuse_plan", "sv_shard_plan", "sv_version", "sv_profile_read"]
+           "sv_enumerate_fibres", "sv_fuse_plan", "sv_shard_plan", "sv_version", "sv_profile_read", "sv_block_plan"]
 
 
 def _check(rc: int):
@@ -202,9 +204,11 @@ class State:
         _check(_lib.sv_apply_gate(self._h, int(target), _p(c, _i32p), _p(v, _i32p), int(c.size),
                                   Uc.view(np.float64).ctypes.data_as(_dp)))
 
-    def apply_circuit(self, gates, fuse: bool = False, check: bool = True, graph: bool = False):
+    def apply_circuit(self, gates, fuse: bool = False, check: bool = True, graph: bool = False,
+                      block: bool = False):
         ga = gates if isinstance(gates, _GateArray) else _GateArray(gates)
-        flags = (SV_FUSE if fuse else 0) | (0 if check else SV_NO_CHECK) | (SV_GRAPH if graph else 0)
+        flags = (SV_FUSE if fuse else 0) | (0 if check else SV_NO_CHECK) | (SV_GRAPH if graph else 0) | \
+            (SV_BLOCK if block else 0)
         _check(_lib.sv_apply_circuit(self._h, ga.arr, ga.n, flags))
 
     def amplitudes(self, first: int = 0, count: int | None = None, out: np.ndarray | None = None) -> np.ndarray:
@@ -292,6 +296,21 @@ def fuse_plan(dims, gates):
                     tuple(int(x) for x in ov[co:co + nc[i]]), u))
         co += int(nc[i])
     return res
+
+
+def block_plan(dims, gates, tile_cap: int = 4096):
+    """Host pass planner: (order, pass_id, tiles) — gate indices in application order."""
+    gates = list(gates)
+    ga = _GateArray(gates)
+    n = max(1, len(gates))
+    order, pid, tiles = (np.zeros(n, np.int64) for _ in range(3))
+    npass = C.c_int64()
+    d = _i32(dims)
+    p64 = C.POINTER(C.c_int64)
+    _check(_lib.sv_block_plan(d.ctypes.data_as(_i32p), d.size, ga.arr, ga.n, int(tile_cap),
+                              order.ctypes.data_as(p64), pid.ctypes.data_as(p64), tiles.ctypes.data_as(p64),
+                              C.byref(npass)))
+    return order[:len(gates)], pid[:len(gates)], tiles[:npass.value]
 
 
 def shard_plan(dims, nranks, rank, target, ctrl=(), vals=()):

@@ -187,3 +187,34 @@ def test_shard_plan_rules():
         assert a == (2 if (r >> 1) & 1 == 0 else 1)
     assert _err(P.shard_plan, [3, 3, 3], 2, 0, 0) == "SV_ERR_UNSUPPORTED"   # top digit not a qubit
     assert _err(P.shard_plan, dims, 3, 0, 0) == "SV_ERR_INVALID_ARG"
+
+
+def test_block_planner_reorders_only_commuting_gates():
+    """SV_BLOCK's pass planner: applying the gates in its order (O-2) reproduces the original
+    circuit; every pass's tile fits the cap; the planner actually groups gates."""
+    rng = np.random.default_rng(77)
+    for cfg, nq in ((4, 2), (3, 5), (2, None), (1, None)):
+        dims, gates = config_circuit(cfg, nqubits=nq) if cfg in (3, 4) else config_circuit(cfg)
+        gates = gates[:120]
+        for cap in (4096, 2048):
+            order, pid, tiles = P.block_plan(dims, gates, cap)
+            assert sorted(order.tolist()) == list(range(len(gates)))
+            assert all(t <= cap for t in tiles) or len(tiles) == len(gates)
+            assert len(tiles) < len(gates)          # grouping happened
+            assert np.all(np.diff(pid) >= 0)
+            D = int(np.prod(dims))
+            if D > 2_000_000:
+                continue
+            psi0 = random_state(D, 5)
+            ref = O2.run(dims, gates, psi0)
+            got = O2.run(dims, [gates[i] for i in order], psi0)
+            assert np.max(np.abs(got - ref)) < 1e-12
+    # random circuits with controls everywhere
+    for s in range(30):
+        dims = [int(x) for x in rng.integers(2, 6, size=6)]
+        _, gates = random_circuit(800 + s, dims, 60, max_ctrl=2)
+        order, pid, tiles = P.block_plan(dims, gates, 256)
+        psi0 = random_state(int(np.prod(dims)), s)
+        ref = O2.run(dims, gates, psi0)
+        got = O2.run(dims, [gates[i] for i in order], psi0)
+        assert np.max(np.abs(got - ref)) < 1e-12

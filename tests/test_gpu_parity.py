@@ -27,9 +27,12 @@ def P():
     return P
 
 
-def run_gpu(P, dims, gates, psi0=None, kernel=0, fuse=False, graph=False, per_gate=False):
+def run_gpu(P, dims, gates, psi0=None, kernel=0, fuse=False, graph=False, per_gate=False, block=False,
+            pass_tile=None):
     with P.State(dims) as st:
         st.set_option(P.sv.SV_OPT_KERNEL, kernel)
+        if pass_tile:
+            st.set_option(P.sv.SV_OPT_PASS_TILE, pass_tile)
         if psi0 is not None:
             st.set_amplitudes(0, psi0)
         n0 = st.info().kernel_launches
@@ -37,7 +40,7 @@ def run_gpu(P, dims, gates, psi0=None, kernel=0, fuse=False, graph=False, per_ga
             for g in gates:
                 st.apply_gate(g.target, g.U, g.ctrl, g.vals)
         else:
-            st.apply_circuit(gates, fuse=fuse, graph=graph)
+            st.apply_circuit(gates, fuse=fuse, graph=graph, block=block)
         out = st.amplitudes()
         nrm = st.norm()
         launched = st.info().kernel_launches - n0
@@ -69,41 +72,45 @@ def test_ghz_exact(P, kernel, d, n):
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
-@pytest.mark.parametrize("mode", ["plain", "fuse", "graph", "per_gate"])
+@pytest.mark.parametrize("mode", ["plain", "fuse", "graph", "per_gate", "block", "block_graph"])
 def test_c1_against_kronecker(P, kernel, mode):
     dims, gates = config_circuit(1)
     ref = O1.run(dims, gates)
     got, nrm, launched = run_gpu(P, dims, gates, kernel=kernel, fuse=mode in ("fuse", "graph"),
-                                 graph=mode == "graph", per_gate=mode == "per_gate")
+                                 graph=mode in ("graph", "block_graph"), per_gate=mode == "per_gate",
+                                 block=mode.startswith("block"))
     assert np.max(np.abs(got - ref)) <= 1e-10
     assert abs(nrm - 1.0) <= 1e-10
     assert launched > 0
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
-@pytest.mark.parametrize("fuse", [False, True])
+@pytest.mark.parametrize("fuse", [False, True, "block"])
 def test_c2_against_blocksim(P, kernel, fuse):
     dims, gates = config_circuit(2)
     ref = O2.run(dims, gates)
-    got, nrm, _ = run_gpu(P, dims, gates, kernel=kernel, fuse=fuse, graph=fuse)
+    got, nrm, _ = run_gpu(P, dims, gates, kernel=kernel, fuse=fuse is True, graph=bool(fuse),
+                          block=fuse == "block")
     assert np.max(np.abs(got - ref)) <= 1e-10
     assert abs(nrm - 1.0) <= 1e-10
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
-def test_c3_reduced_register(P, kernel):
+@pytest.mark.parametrize("block", [False, True])
+def test_c3_reduced_register(P, kernel, block):
     dims, gates = config_circuit(3, nqubits=6)
     ref = O2.run(dims, gates)
-    got, nrm, _ = run_gpu(P, dims, gates, kernel=kernel, fuse=True)
+    got, nrm, _ = run_gpu(P, dims, gates, kernel=kernel, fuse=True, block=block)
     assert np.max(np.abs(got - ref)) <= 1e-10
     assert abs(nrm - 1.0) <= 1e-10
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
-def test_c4_reduced_register(P, kernel):
+@pytest.mark.parametrize("block", [False, True])
+def test_c4_reduced_register(P, kernel, block):
     dims, gates = config_circuit(4, nqubits=1)        # D = 9.3e6, every dimension class
     ref = O2.run(dims, gates)
-    got, nrm, _ = run_gpu(P, dims, gates, kernel=kernel)
+    got, nrm, _ = run_gpu(P, dims, gates, kernel=kernel, block=block)
     assert np.max(np.abs(got - ref)) <= 1e-10
     assert abs(nrm - 1.0) <= 1e-10
 
@@ -323,10 +330,10 @@ def test_loopback_sharded_matches_single_state(P, nranks):
                   Gate(5, (7,), (1,), shift_x(2, 1)), Gate(1, (6, 7), (1, 0), fourier(3))]
         psi0 = random_state(D, 5)
         ref = O2.run(dims, gates, psi0)
-        for fuse in (False, True):
+        for fuse in (False, True, "block"):
             with P.State.loopback(dims, nranks) as st:
                 st.set_amplitudes(0, psi0)
-                st.apply_circuit(gates, fuse=fuse)
+                st.apply_circuit(gates, fuse=fuse is True, block=fuse == "block")
                 got = st.amplitudes()
                 nrm = st.norm()
                 assert st.info().exchanges > 0
@@ -344,3 +351,41 @@ def test_loopback_sharded_matches_single_state(P, nranks):
         assert np.array_equal(got, O2.run(dims, perm, lab))
     finally:
         del os.environ["SV_EXCHANGE_CHUNK"]
+
+
+@pytest.mark.parametrize("pass_tile", [4096, 1024, 256])
+def test_block_passes_random_sweep(P, pass_tile):
+    """SV_BLOCK multi-gate passes on random registers and circuits with controls inside the
+    tile (in-tile high digits, low digits) and outside it (per-tile predicate), ragged tiles,
+    tiny registers; against O-2."""
+    rng = np.random.default_rng(pass_tile)
+    for s in range(25):
+        n = int(rng.integers(2, 9))
+        dims = [int(x) for x in rng.integers(2, 6, size=n)]
+        while np.prod(dims) > 3_000_000:
+            dims = dims[:-1]
+        _, gates = random_circuit(70_000 + s, dims, 80, max_ctrl=3)
+        psi0 = random_state(int(np.prod(dims)), s)
+        ref = O2.run(dims, gates, psi0)
+        got, nrm, _ = run_gpu(P, dims, gates, psi0, block=True, pass_tile=pass_tile)
+        assert np.max(np.abs(got - ref)) <= 1e-12, (dims, s)
+
+
+def test_block_passes_labelled_bit_exact(P):
+    """Permutation-only circuits through multi-gate passes: bit-exact against O-2."""
+    rng = np.random.default_rng(3)
+    dims = config_circuit(4, ngates=0, nqubits=4)[0]
+    n, D = len(dims), int(np.prod(dims))
+    gates = []
+    for _ in range(150):
+        t = int(rng.integers(n))
+        others = [q for q in range(n) if q != t]
+        nc = int(rng.integers(0, 3))
+        ctrl = tuple(int(c) for c in rng.choice(others, size=nc, replace=False))
+        vals = tuple(int(rng.integers(dims[c])) for c in ctrl)
+        gates.append(Gate(t, ctrl, vals, permutation_matrix(rng.permutation(dims[t]))))
+    psi0 = labelled_state(0, D)
+    ref = O2.run(dims, gates, psi0)
+    got, _, launched = run_gpu(P, dims, gates, psi0, block=True)
+    assert launched < len(gates)
+    assert np.array_equal(got, ref)
