@@ -152,6 +152,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 direct, 2 tiled")
     ap.add_argument("--no-fuse", action="store_true")
+    ap.add_argument("--no-block", action="store_true", help="disable multi-gate passes (SV_BLOCK)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ngates", type=int, default=None)
     args = ap.parse_args()
@@ -173,6 +174,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     dims, gates = config_circuit(args.config, ngates=args.ngates)
     fuse = not args.no_fuse
+    block = not args.no_block
     T_step = touched_total(dims, gates)                       # global amplitude updates / step
 
     if world > 1:
@@ -190,7 +192,7 @@ def main():
 
     def step():
         st.reset(0)
-        st.apply_circuit(ga, fuse=fuse, check=False)
+        st.apply_circuit(ga, fuse=fuse, check=False, block=block)
 
     for _ in range(args.warmup):
         step()
@@ -232,7 +234,7 @@ def main():
     t0 = time.perf_counter()
     for _ in range(args.steps):
         st.reset(0)
-        st.apply_circuit(gates, fuse=fuse, check=True)      # marshals host gates each step
+        st.apply_circuit(gates, fuse=fuse, check=True, block=block)   # marshals host gates each step
         nrm = st.norm()
         st.amplitudes(0, 4096, out)
     t_e2e = time.perf_counter() - t0
@@ -267,7 +269,7 @@ def main():
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": CONFIG_NAMES[args.config], "dims_q0_first": dims,
-                       "D": int(np.prod(dims, dtype=object)), "gates": len(gates), "fuse": fuse,
+                       "D": int(np.prod(dims, dtype=object)), "gates": len(gates), "fuse": fuse, "block_passes": block,
                        "kernel": args.kernel, "sharded_ranks": world,
                        "l2": "state (%.1f GB) >> L2 (126 MB): no flush needed" % (16 * np.prod(dims, dtype=object) / 1e9)},
             "hbm_gbs": 32.0 * value / 1e9,
