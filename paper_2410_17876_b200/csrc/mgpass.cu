@@ -174,46 +174,109 @@ __device__ __noinline__ void apply_class_generic(double2 *buf, uint32_t e0, uint
     }
 }
 
+// member-0 smem index of class c, and whether the class exists (ragged) and fires (controls)
+__device__ __forceinline__ bool class_at(const PassParams &p, const PassGateP &g, const TileInfo &ti,
+                                         const uint32_t (&lowoff)[kMaxPassCtrl], uint32_t c, uint32_t &e0) {
+    uint32_t off;
+    const uint32_t grp = fastdiv32(c, g.st, g.mst, off);
+    e0 = grp * g.st * (uint32_t)g.d + off;
+    uint32_t l;
+    const uint32_t m = fastdiv32(e0, p.LT, p.mLT, l);
+    if (l >= ti.len) return false;                       // ragged last tile of a run
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < kMaxPassCtrl; ++k) {
+        if (k >= g.nctrl) break;
+        const PassCtrl &cc = g.c[k];
+        uint32_t r, r2;
+        if (cc.cls == 0) {
+            const uint32_t q = fastdiv32(m, cc.w, cc.mw, r);
+            fastdiv32(q, cc.d, cc.md, r2);
+            ok = ok && (r2 == cc.v);
+        } else if (cc.cls == 1) {
+            fastdiv32(lowoff[k] + l, cc.M, cc.mM, r);
+            const uint32_t q = fastdiv32(r, cc.w, cc.mw, r2);
+            fastdiv32(q, cc.d, cc.md, r2);
+            ok = ok && (r2 == cc.v);
+        }
+    }
+    return ok;
+}
+
+// two classes per iteration: both gathers are issued before either matvec (ILP)
 template <int D>
+__device__ __forceinline__ void apply_class2(double2 *buf, uint32_t ea, bool oka, uint32_t eb, bool okb,
+                                             uint32_t st, const PassGateP &g, const double2 *U) {
+    double2 xa[D], xb[D];
+    if (g.kind == kGeneral) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            if (oka) xa[j] = buf[ea + j * st];
+            if (okb) xb[j] = buf[eb + j * st];
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            double2 aa = make_double2(0.0, 0.0), ab = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                const double2 u = U[i * D + j];
+                cfma(aa, u, xa[j]);
+                cfma(ab, u, xb[j]);
+            }
+            if (oka) buf[ea + i * st] = aa;
+            if (okb) buf[eb + i * st] = ab;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < D; ++j)
+            if ((g.active >> j) & 1) {
+                if (oka) xa[j] = buf[ea + j * st];
+                if (okb) xb[j] = buf[eb + j * st];
+            }
+#pragma unroll
+        for (int j = 0; j < D; ++j)
+            if ((g.active >> j) & 1) {
+                const double2 u = U[j];
+                if (oka) buf[ea + g.sigma[j] * st] = cmul(u, xa[j]);
+                if (okb) buf[eb + g.sigma[j] * st] = cmul(u, xb[j]);
+            }
+    }
+}
+
+template <int D, int NT>
 __device__ __forceinline__ void apply_gate_tile(const PassParams &p, const PassGateP &g, double2 *buf,
-                                                const TileInfo &ti, const uint32_t *lowoff, int tid) {
+                                                const TileInfo &ti, const uint32_t (&lowoff)[kMaxPassCtrl],
+                                                int tid) {
     const uint32_t nslots = (uint32_t)p.M * p.LT;
     const uint32_t ncls = nslots / (uint32_t)g.d;
     const double2 *U = p.U + g.uoff;
-    for (uint32_t c = tid; c < ncls; c += kPassThreads) {
-        uint32_t off;
-        const uint32_t grp = fastdiv32(c, g.st, g.mst, off);
-        const uint32_t e0 = grp * g.st * (uint32_t)g.d + off;
-        uint32_t l;
-        const uint32_t m = fastdiv32(e0, p.LT, p.mLT, l);
-        if (l >= ti.len) continue;                       // ragged last tile of a run
-        bool ok = true;
-        for (int k = 0; k < g.nctrl; ++k) {
-            const PassCtrl &cc = g.c[k];
-            if (cc.cls == 0) {
-                uint32_t r;
-                const uint32_t q = fastdiv32(m, cc.w, cc.mw, r);
-                fastdiv32(q, cc.d, cc.md, r);
-                ok = ok && (r == cc.v);
-            } else if (cc.cls == 1) {
-                uint32_t r, r2;
-                fastdiv32(lowoff[k] + l, cc.M, cc.mM, r);
-                const uint32_t q = fastdiv32(r, cc.w, cc.mw, r2);
-                fastdiv32(q, cc.d, cc.md, r2);
-                ok = ok && (r2 == cc.v);
-            }
+    if (D == 0) {
+        for (uint32_t c = tid; c < ncls; c += NT) {
+            uint32_t e0;
+            if (class_at(p, g, ti, lowoff, c, e0)) apply_class_generic(buf, e0, g.st, g, U);
         }
-        if (!ok) continue;
-        if (D)
-            apply_class<D>(buf, e0, g.st, g, U, g.d);
-        else
-            apply_class_generic(buf, e0, g.st, g, U);
+        return;
+    }
+    if (D >= 4) {   // the d x d matrix is hoisted into registers: one class per iteration
+        for (uint32_t c = tid; c < ncls; c += NT) {
+            uint32_t e0;
+            if (class_at(p, g, ti, lowoff, c, e0)) apply_class<D ? D : 2>(buf, e0, g.st, g, U, g.d);
+        }
+        return;
+    }
+    for (uint32_t c = tid; c < ncls; c += 2 * NT) {
+        uint32_t ea = 0, eb = 0;
+        const bool oka = class_at(p, g, ti, lowoff, c, ea);
+        const uint32_t c2 = c + NT;
+        const bool okb = c2 < ncls && class_at(p, g, ti, lowoff, c2, eb);
+        apply_class2<D ? D : 2>(buf, ea, oka, eb, okb, g.st, g, U);
     }
 }
 
 }  // namespace
 
-__global__ void __launch_bounds__(kPassThreads, 1) k_gate_pass(const __grid_constant__ PassParams p, int S, int TE) {
+template <int NT>
+__global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_gate_pass(const __grid_constant__ PassParams p, int S, int TE) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double2 *bufs = reinterpret_cast<double2 *>(smem_raw);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + (size_t)S * TE * sizeof(double2));
@@ -241,7 +304,9 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_gate_pass(const __grid_cons
             const PassGateP &g = p.g[gi];
             // per-tile decisions: controls outside the tile; run offsets of low controls
             bool fire = true;
-            for (int k = 0; k < g.nctrl; ++k) {
+#pragma unroll
+            for (int k = 0; k < kMaxPassCtrl; ++k) {
+                if (k >= g.nctrl) break;
                 const PassCtrl &cc = g.c[k];
                 if (cc.cls == 2) {
                     uint64_t r;
@@ -256,11 +321,11 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_gate_pass(const __grid_cons
             }
             if (!fire) continue;                       // uniform across the CTA
             switch (g.d) {
-                case 2: apply_gate_tile<2>(p, g, buf, ti, lowoff, tid); break;
-                case 3: apply_gate_tile<3>(p, g, buf, ti, lowoff, tid); break;
-                case 4: apply_gate_tile<4>(p, g, buf, ti, lowoff, tid); break;
-                case 5: apply_gate_tile<5>(p, g, buf, ti, lowoff, tid); break;
-                default: apply_gate_tile<0>(p, g, buf, ti, lowoff, tid); break;
+                case 2: apply_gate_tile<2, NT>(p, g, buf, ti, lowoff, tid); break;
+                case 3: apply_gate_tile<3, NT>(p, g, buf, ti, lowoff, tid); break;
+                case 4: apply_gate_tile<4, NT>(p, g, buf, ti, lowoff, tid); break;
+                case 5: apply_gate_tile<5, NT>(p, g, buf, ti, lowoff, tid); break;
+                default: apply_gate_tile<0, NT>(p, g, buf, ti, lowoff, tid); break;
             }
             __syncthreads();
         }
@@ -389,19 +454,31 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
     return p.ntiles > 0;
 }
 
-cudaError_t launch_pass(const PassParams &p, cudaStream_t st, const LaunchCfg &cfg) {
-    const int S = 3, TE = cfg.pass_tile;
+template <int NT>
+cudaError_t launch_pass_t(const PassParams &p, cudaStream_t st, const LaunchCfg &cfg) {
+    const int S = cfg.pass_stages, TE = cfg.pass_tile;
     const size_t smem = (size_t)S * TE * sizeof(double2) + (size_t)S * sizeof(uint64_t);
-    static size_t configured = 0;
+    static size_t configured = 0, occ_for = 0;
+    static int occ = 1;
     if (configured < smem) {
-        cudaError_t e = cudaFuncSetAttribute(k_gate_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(k_gate_pass<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         configured = smem;
     }
-    const uint64_t cap = (uint64_t)cfg.num_sms;
+    if (occ_for != smem) {   // resident CTAs per SM at this smem size (persistent grid)
+        int o = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_gate_pass<NT>, NT, smem) != cudaSuccess || o < 1) o = 1;
+        occ = o;
+        occ_for = smem;
+    }
+    const uint64_t cap = (uint64_t)cfg.num_sms * (uint64_t)occ;
     const unsigned grid = (unsigned)(p.ntiles < cap ? p.ntiles : cap);
-    k_gate_pass<<<grid, kPassThreads, smem, st>>>(p, S, TE);
+    k_gate_pass<NT><<<grid, NT, smem, st>>>(p, S, TE);
     return cudaGetLastError();
+}
+
+cudaError_t launch_pass(const PassParams &p, cudaStream_t st, const LaunchCfg &cfg) {
+    return cfg.pass_threads >= 512 ? launch_pass_t<512>(p, st, cfg) : launch_pass_t<256>(p, st, cfg);
 }
 
 cudaError_t run_pass(const Register &reg, const std::vector<GateSpec> &gates, const PassPlan &pp, double2 *psi,

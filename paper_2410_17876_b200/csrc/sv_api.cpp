@@ -60,6 +60,9 @@ void default_cfg(LaunchCfg &c, int device) {
     c.ctas_per_sm = 2;
     c.num_sms = sms;
     c.pass_tile = 4096;
+    c.pass_stages = 3;
+    c.pass_threads = 512;
+    c.pass_gates = 24;
 }
 
 }  // namespace
@@ -194,7 +197,7 @@ sv_status run_local_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_t 
     std::vector<PassPlan> passes;
     if (flags & SV_BLOCK) {
         specs = merge_same_qudit(specs);
-        passes = plan_passes(h->local, specs, (uint64_t)h->cfg.pass_tile, 24, 64);
+        passes = plan_passes(h->local, specs, (uint64_t)h->cfg.pass_tile, h->cfg.pass_gates, 64);
     } else {
         if (flags & SV_FUSE) specs = fuse_gates(h->local, specs);
         for (size_t i = 0; i < specs.size(); ++i) {
@@ -409,8 +412,20 @@ sv_status sv_set_option(sv_handle h, int32_t option, int64_t value) {
             h->profile = value != 0;
             return SV_OK;
         case SV_OPT_PASS_TILE:
-            if (value < 256 || value > 4096) return fail(SV_ERR_INVALID_ARG, "pass tile 256..4096");
+            if (value < 256 || value > 8192) return fail(SV_ERR_INVALID_ARG, "pass tile 256..8192");
             h->cfg.pass_tile = (int)value;
+            return SV_OK;
+        case SV_OPT_PASS_STAGES:
+            if (value < 2 || value > 4) return fail(SV_ERR_INVALID_ARG, "pass stages 2..4");
+            h->cfg.pass_stages = (int)value;
+            return SV_OK;
+        case SV_OPT_PASS_THREADS:
+            if (value != 256 && value != 512) return fail(SV_ERR_INVALID_ARG, "pass threads 256 or 512");
+            h->cfg.pass_threads = (int)value;
+            return SV_OK;
+        case SV_OPT_PASS_GATES:
+            if (value < 1 || value > 24) return fail(SV_ERR_INVALID_ARG, "pass gates 1..24");
+            h->cfg.pass_gates = (int)value;
             return SV_OK;
         case SV_OPT_CTAS_PER_SM:
             if (value < 1 || value > 8) return fail(SV_ERR_INVALID_ARG, "ctas per SM 1..8");

@@ -144,6 +144,9 @@ struct LaunchCfg {
     int ctas_per_sm;
     int num_sms;
     int pass_tile;     // amplitudes per smem tile of the multi-gate pass kernel
+    int pass_stages;   // smem ring stages of the pass kernel
+    int pass_threads;  // threads per CTA of the pass kernel (256 or 512)
+    int pass_gates;    // max gates per pass
 };
 
 cudaError_t launch_gate(const GatePlan &p, double2 *psi, cudaStream_t st, const LaunchCfg &cfg,

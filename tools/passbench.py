@@ -1,0 +1,70 @@
+"""Sweep the multi-gate pass kernel's configuration on a config circuit: one JSON line per
+(tile, stages, threads, max gates) with ms per circuit and the number of launches."""
+from __future__ import annotations
+
+import argparse
+import itertools
+import json
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--nqubits", type=int, default=None)
+    ap.add_argument("--ngates", type=int, default=None)
+    ap.add_argument("--tiles", default="4096,2048")
+    ap.add_argument("--stages", default="3,2")
+    ap.add_argument("--threads", default="512,256")
+    ap.add_argument("--gates", default="24,8,4,2")
+    ap.add_argument("--reps", type=int, default=1)
+    args = ap.parse_args()
+    import torch
+    import paper_2410_17876_b200 as P
+    from sv_inputs import config_circuit
+    dims, gates = config_circuit(args.config, ngates=args.ngates, nqubits=args.nqubits)
+    T = sum(int(P.plan_gate(dims, g.target, g.U, g.ctrl, g.vals).touched) for g in gates)
+    D = int(np.prod(dims, dtype=object))
+    st = P.State(dims)
+    ext = torch.cuda.ExternalStream(st.info().cuda_stream)
+    ga = P.sv._GateArray(gates)
+    cases = [("noblock", 0, 0, 0, 0)]
+    for te, s, nt, ng in itertools.product(*[[int(x) for x in a.split(",")] for a in
+                                             (args.tiles, args.stages, args.threads, args.gates)]):
+        if te * 16 * s > 220 * 1024:
+            continue
+        cases.append(("block", te, s, nt, ng))
+    for kind, te, s, nt, ng in cases:
+        block = kind == "block"
+        if block:
+            st.set_option(P.sv.SV_OPT_PASS_TILE, te)
+            st.set_option(P.sv.SV_OPT_PASS_STAGES, s)
+            st.set_option(P.sv.SV_OPT_PASS_THREADS, nt)
+            st.set_option(P.sv.SV_OPT_PASS_GATES, ng)
+        st.reset(0)
+        st.apply_circuit(ga, fuse=True, check=False, block=block)
+        st.sync()
+        n0 = st.info().kernel_launches
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(ext)
+        for _ in range(args.reps):
+            st.apply_circuit(ga, fuse=True, check=False, block=block)
+        e1.record(ext)
+        st.sync()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.reps
+        launches = (st.info().kernel_launches - n0) // args.reps
+        print(json.dumps({"config": args.config, "D": D, "gates": len(gates), "mode": kind, "tile": te,
+                          "stages": s, "threads": nt, "max_gates": ng, "ms": ms, "launches": launches,
+                          "updates_per_s": T / (ms / 1e3), "equiv_GBps": 32.0 * T / (ms / 1e3) / 1e9,
+                          "pass_GBps": 32.0 * D * launches / (ms / 1e3) / 1e9}), flush=True)
+    st.close()
+
+
+if __name__ == "__main__":
+    main()
