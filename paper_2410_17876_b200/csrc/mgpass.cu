@@ -388,9 +388,12 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
     }
     p.nrem = nr;
     // schedule: runs of the low space below min H, split into tiles of LT elements
+    // The run per member is widened to fill the tile (a multiple of b_{m0}, so low-prefix
+    // classes stay whole, and at most the run R below min H).
     const uint64_t R = pp.H.empty() ? reg.D : reg.b[pp.H[0]];
-    uint64_t LT = pp.H.empty() ? ((uint64_t)TE / L) * L : L;
-    if (LT == 0 || LT > R) LT = R;
+    uint64_t LT = ((uint64_t)TE / M / L) * L;
+    if (LT < L) LT = L;
+    if (LT > R) LT = R;
     p.R = R;
     p.LT = (uint32_t)LT;
     p.mLT = make_fastdiv32(p.LT).m;
