@@ -38,6 +38,7 @@ struct PassCtrl {
 
 struct PassGateP {
     int32_t d, kind, nctrl, uoff;
+    int32_t inctl;        // has controls decided inside the tile (cls 0 / 1)
     uint32_t st, mst;     // smem stride of the target (+ magic)
     uint32_t active;
     int8_t sigma[kMaxDim];
@@ -52,6 +53,7 @@ struct PassParams {
     uint32_t LT, mLT;     // run elements per member in a tile (+ magic)
     int32_t M;            // members per tile
     int32_t ngates;
+    int32_t upool;        // used entries of U (copied to shared memory at kernel start)
     uint64_t moff[kMaxMembers];
     PassGateP g[kMaxPassGates];
     double2 U[kPoolC];    // general: row-major d x d; monomial: coefficient per member
@@ -114,8 +116,42 @@ __device__ __forceinline__ TileInfo tile_info(const PassParams &p, uint64_t t) {
     return ti;
 }
 
-__device__ __forceinline__ void issue_loads(const PassParams &p, uint64_t t, double2 *buf, uint64_t *bar, int lane) {
+// Per-stage record written by warp 0 when it issues a tile's loads (before the mbarrier
+// arrive, so the consumers' acquire-wait sees it): the tile geometry, which gates fire on this
+// tile (controls outside the tile), and the run offsets of the low controls.
+struct StageInfo {
+    TileInfo ti;
+    uint32_t fire;                                   // bit g: gate g's out-of-tile controls hold
+    uint32_t lowoff[kMaxPassGates][kMaxPassCtrl];    // (s0 mod b_c d_c) for low controls
+};
+
+__device__ __forceinline__ void issue_loads(const PassParams &p, uint64_t t, double2 *buf, uint64_t *bar,
+                                            StageInfo *si, int lane) {
     const TileInfo ti = tile_info(p, t);
+    // lane g decides gate g for this tile
+    bool fire = true;
+    if (lane < p.ngates) {
+        const PassGateP &g = p.g[lane];
+        for (int k = 0; k < g.nctrl; ++k) {
+            const PassCtrl &cc = g.c[k];
+            if (cc.cls == 2) {
+                uint64_t r;
+                const uint64_t q = fastdiv64(ti.gbase, cc.b64, cc.mb64, r);
+                fastdiv64(q, cc.d, cc.md64, r);
+                fire = fire && (r == cc.v);
+            } else if (cc.cls == 1) {
+                uint64_t r;
+                fastdiv64(ti.s0, cc.M, cc.mb64, r);
+                si->lowoff[lane][k] = (uint32_t)r;
+            }
+        }
+    }
+    const uint32_t bits = __ballot_sync(0xffffffffu, fire && lane < p.ngates);
+    if (lane == 0) {
+        si->ti = ti;
+        si->fire = bits;
+    }
+    __syncwarp();
     if (lane == 0) mbar_expect_tx(bar, (uint32_t)p.M * ti.len * (uint32_t)sizeof(double2));
     __syncwarp();
     for (int m = lane; m < p.M; m += 32)
@@ -175,14 +211,15 @@ __device__ __noinline__ void apply_class_generic(double2 *buf, uint32_t e0, uint
 }
 
 // member-0 smem index of class c, and whether the class exists (ragged) and fires (controls)
-__device__ __forceinline__ bool class_at(const PassParams &p, const PassGateP &g, const TileInfo &ti,
-                                         const uint32_t (&lowoff)[kMaxPassCtrl], uint32_t c, uint32_t &e0) {
+__device__ __forceinline__ bool class_at(const PassParams &p, const PassGateP &g, uint32_t len, bool needml,
+                                         const uint32_t *lowoff, uint32_t c, uint32_t &e0) {
     uint32_t off;
     const uint32_t grp = fastdiv32(c, g.st, g.mst, off);
     e0 = grp * g.st * (uint32_t)g.d + off;
+    if (!needml) return true;                            // full tile, no in-tile controls
     uint32_t l;
     const uint32_t m = fastdiv32(e0, p.LT, p.mLT, l);
-    if (l >= ti.len) return false;                       // ragged last tile of a run
+    if (l >= len) return false;                          // ragged last tile of a run
     bool ok = true;
 #pragma unroll
     for (int k = 0; k < kMaxPassCtrl; ++k) {
@@ -245,30 +282,31 @@ __device__ __forceinline__ void apply_class2(double2 *buf, uint32_t ea, bool oka
 
 template <int D, int NT>
 __device__ __forceinline__ void apply_gate_tile(const PassParams &p, const PassGateP &g, double2 *buf,
-                                                const TileInfo &ti, const uint32_t (&lowoff)[kMaxPassCtrl],
+                                                const double2 *Us, uint32_t len, const uint32_t *lowoff,
                                                 int tid) {
     const uint32_t nslots = (uint32_t)p.M * p.LT;
     const uint32_t ncls = nslots / (uint32_t)g.d;
-    const double2 *U = p.U + g.uoff;
+    const double2 *U = Us + g.uoff;       // shared-memory copy: not hoisted into registers
+    const bool needml = g.inctl || len < p.LT;
     if (D == 0) {
         for (uint32_t c = tid; c < ncls; c += NT) {
             uint32_t e0;
-            if (class_at(p, g, ti, lowoff, c, e0)) apply_class_generic(buf, e0, g.st, g, U);
+            if (class_at(p, g, len, needml, lowoff, c, e0)) apply_class_generic(buf, e0, g.st, g, U);
         }
         return;
     }
     if (D >= 4) {   // the d x d matrix is hoisted into registers: one class per iteration
         for (uint32_t c = tid; c < ncls; c += NT) {
             uint32_t e0;
-            if (class_at(p, g, ti, lowoff, c, e0)) apply_class<D ? D : 2>(buf, e0, g.st, g, U, g.d);
+            if (class_at(p, g, len, needml, lowoff, c, e0)) apply_class<D ? D : 2>(buf, e0, g.st, g, U, g.d);
         }
         return;
     }
     for (uint32_t c = tid; c < ncls; c += 2 * NT) {
         uint32_t ea = 0, eb = 0;
-        const bool oka = class_at(p, g, ti, lowoff, c, ea);
+        const bool oka = class_at(p, g, len, needml, lowoff, c, ea);
         const uint32_t c2 = c + NT;
-        const bool okb = c2 < ncls && class_at(p, g, ti, lowoff, c2, eb);
+        const bool okb = c2 < ncls && class_at(p, g, len, needml, lowoff, c2, eb);
         apply_class2<D ? D : 2>(buf, ea, oka, eb, okb, g.st, g, U);
     }
 }
@@ -279,68 +317,56 @@ template <int NT>
 __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_gate_pass(const __grid_constant__ PassParams p, int S, int TE) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double2 *bufs = reinterpret_cast<double2 *>(smem_raw);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + (size_t)S * TE * sizeof(double2));
+    double2 *Us = bufs + (size_t)S * TE;                       // the pass's matrices
+    StageInfo *sinfo = reinterpret_cast<StageInfo *>(Us + p.upool);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sinfo + S);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
     }
+    for (int k = tid; k < p.upool; k += NT) Us[k] = p.U[k];
     __syncthreads();
     const uint64_t first = blockIdx.x, step = gridDim.x;
     if (first >= p.ntiles) return;
     const uint64_t my = (p.ntiles - first + step - 1) / step;
     if (warp == 0)
         for (int i = 0; i < S - 1 && (uint64_t)i < my; ++i)
-            issue_loads(p, first + (uint64_t)i * step, bufs + (size_t)i * TE, &bars[i], lane);
+            issue_loads(p, first + (uint64_t)i * step, bufs + (size_t)i * TE, &bars[i], &sinfo[i], lane);
 
-    uint32_t lowoff[kMaxPassCtrl];
     for (uint64_t i = 0; i < my; ++i) {
         const int s = (int)(i % (uint64_t)S);
-        const uint64_t t = first + i * step;
         double2 *buf = bufs + (size_t)s * TE;
-        const TileInfo ti = tile_info(p, t);
         mbar_wait(&bars[s], (uint32_t)((i / (uint64_t)S) & 1));
+        const StageInfo &si = sinfo[s];
+        const uint32_t len = si.ti.len;
+        const uint32_t fire = si.fire;
         for (int gi = 0; gi < p.ngates; ++gi) {
+            if (!((fire >> gi) & 1)) continue;          // out-of-tile control unmet: uniform skip
             const PassGateP &g = p.g[gi];
-            // per-tile decisions: controls outside the tile; run offsets of low controls
-            bool fire = true;
-#pragma unroll
-            for (int k = 0; k < kMaxPassCtrl; ++k) {
-                if (k >= g.nctrl) break;
-                const PassCtrl &cc = g.c[k];
-                if (cc.cls == 2) {
-                    uint64_t r;
-                    const uint64_t q = fastdiv64(ti.gbase, cc.b64, cc.mb64, r);
-                    fastdiv64(q, cc.d, cc.md64, r);
-                    fire = fire && (r == cc.v);
-                } else if (cc.cls == 1) {
-                    uint64_t r;
-                    fastdiv64(ti.s0, cc.M, cc.mb64, r);
-                    lowoff[k] = (uint32_t)r;
-                }
-            }
-            if (!fire) continue;                       // uniform across the CTA
+            const uint32_t *lo = si.lowoff[gi];
             switch (g.d) {
-                case 2: apply_gate_tile<2, NT>(p, g, buf, ti, lowoff, tid); break;
-                case 3: apply_gate_tile<3, NT>(p, g, buf, ti, lowoff, tid); break;
-                case 4: apply_gate_tile<4, NT>(p, g, buf, ti, lowoff, tid); break;
-                case 5: apply_gate_tile<5, NT>(p, g, buf, ti, lowoff, tid); break;
-                default: apply_gate_tile<0, NT>(p, g, buf, ti, lowoff, tid); break;
+                case 2: apply_gate_tile<2, NT>(p, g, buf, Us, len, lo, tid); break;
+                case 3: apply_gate_tile<3, NT>(p, g, buf, Us, len, lo, tid); break;
+                case 4: apply_gate_tile<4, NT>(p, g, buf, Us, len, lo, tid); break;
+                case 5: apply_gate_tile<5, NT>(p, g, buf, Us, len, lo, tid); break;
+                default: apply_gate_tile<0, NT>(p, g, buf, Us, len, lo, tid); break;
             }
             __syncthreads();
         }
         fence_proxy_async();
         __syncthreads();
         if (warp == 0) {
+            const uint64_t gbase = si.ti.gbase;
             for (int m = lane; m < p.M; m += 32)
-                bulk_store(p.psi + ti.gbase + p.moff[m], buf + (size_t)m * p.LT, ti.len * (uint32_t)sizeof(double2));
+                bulk_store(p.psi + gbase + p.moff[m], buf + (size_t)m * p.LT, len * (uint32_t)sizeof(double2));
             bulk_commit();
             const uint64_t nxt = i + (uint64_t)(S - 1);
             if (nxt < my) {
                 bulk_wait_read_1();
                 __syncwarp();
                 const int sn = (int)(nxt % (uint64_t)S);
-                issue_loads(p, first + nxt * step, bufs + (size_t)sn * TE, &bars[sn], lane);
+                issue_loads(p, first + nxt * step, bufs + (size_t)sn * TE, &bars[sn], &sinfo[sn], lane);
             }
         }
     }
@@ -421,6 +447,7 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
         q.uoff = uoff;
         for (int k = 0; k < need; ++k) p.U[uoff + k] = gp.U[k];
         uoff += need;
+        p.upool = uoff;
         const int t = g.target;
         if (g.span != 1 || (t >= m0 && std::find(pp.H.begin(), pp.H.end(), t) == pp.H.end())) return false;
         const uint64_t st = (t < m0) ? reg.b[t] : W[t] * LT;
@@ -437,10 +464,12 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
             const bool inH = std::find(pp.H.begin(), pp.H.end(), c) != pp.H.end();
             if (inH) {
                 cc.cls = 0;
+                q.inctl = 1;
                 cc.w = (uint32_t)W[c];
                 cc.mw = make_fastdiv32(cc.w).m;
             } else if (reg.b[c] < R) {        // below min H: decided by the run position
                 cc.cls = 1;
+                q.inctl = 1;
                 cc.w = (uint32_t)reg.b[c];
                 cc.mw = make_fastdiv32(cc.w).m;
                 cc.M = cc.w * cc.d;
@@ -460,7 +489,9 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
 template <int NT>
 cudaError_t launch_pass_t(const PassParams &p, cudaStream_t st, const LaunchCfg &cfg) {
     const int S = cfg.pass_stages, TE = cfg.pass_tile;
-    const size_t smem = (size_t)S * TE * sizeof(double2) + (size_t)S * sizeof(uint64_t);
+    // size for the largest matrix pool so the attribute and the occupancy are set once per config
+    const size_t smem = (size_t)S * TE * sizeof(double2) + (size_t)kPoolC * sizeof(double2) +
+                        (size_t)S * sizeof(StageInfo) + (size_t)S * sizeof(uint64_t);
     static size_t configured = 0, occ_for = 0;
     static int occ = 1;
     if (configured < smem) {
