@@ -152,7 +152,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 direct, 2 tiled")
     ap.add_argument("--no-fuse", action="store_true")
-    ap.add_argument("--no-block", action="store_true", help="disable multi-gate passes (SV_BLOCK)")
+    ap.add_argument("--block", action="store_true",
+                    help="multi-gate cache-blocked passes (SV_BLOCK; slower than single-gate passes on c4 so far)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ngates", type=int, default=None)
     args = ap.parse_args()
@@ -174,7 +175,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     dims, gates = config_circuit(args.config, ngates=args.ngates)
     fuse = not args.no_fuse
-    block = not args.no_block
+    block = args.block
     T_step = touched_total(dims, gates)                       # global amplitude updates / step
 
     if world > 1:
