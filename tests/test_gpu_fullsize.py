@@ -1,0 +1,154 @@
+"""Full-size parity at BASELINE.json's configs c3 (6.9 GB) and c4 (76.4 GB), in the launch
+configuration bench.py times (auto kernel policy, SV_FUSE), against the oracle:
+
+  * the state after a prefix of the seeded circuit, compared element by element with O-2
+    run on the host (streamed back in 2 GB chunks);
+  * every target qudit x {Haar U(d), controlled increment with a high / low-stride control,
+    phase} applied to the index-labelled state, checked at sampled windows against the
+    oracle's one-index evaluator (O-2, PAPER.md:222 row v of U times the class vector), then
+    undone with the adjoint (back to the labels);
+  * the whole circuit followed by its adjoint returns to e_0 (closed form), norm preserved.
+Tolerances: normalised states 1e-10 (north_star); the labelled state (values up to 4.8e9)
+relative 1e-13 (R15), permutations bit-exact."""
+import numpy as np
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+from oracle import blocksim as O2  # noqa: E402
+from sv_inputs import (Gate, config_circuit, adjoint_circuit, haar_unitary, shift_x,  # noqa: E402
+                       phase_gate, labelled_state)
+
+CHUNK = 1 << 27          # 2 GB of complex128
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2410_17876_b200 as P
+    return P
+
+
+def _upload_labelled(st, D):
+    for first in range(0, D, CHUNK):
+        st.set_amplitudes(first, labelled_state(first, min(CHUNK, D - first)))
+
+
+def _compare_full(st, ref):
+    D = ref.size
+    worst = 0.0
+    buf = np.empty(CHUNK, dtype=np.complex128)
+    for first in range(0, D, CHUNK):
+        n = min(CHUNK, D - first)
+        got = st.amplitudes(first, n, buf[:n])
+        worst = max(worst, float(np.max(np.abs(got - ref[first:first + n]))))
+    return worst
+
+
+def _windows(D, rng, nwin=48, width=1024):
+    starts = np.sort(rng.integers(0, D - width, size=nwin))
+    starts[0], starts[-1] = 0, D - width          # include both ends of the register
+    return starts, width
+
+
+def _sample(st, starts, width):
+    return np.concatenate([st.amplitudes(int(s), width) for s in starts])
+
+
+def _idx(starts, width):
+    return (starts[:, None] + np.arange(width)[None, :]).ravel().astype(np.uint64)
+
+
+def _prefix_parity(P, cfg, ngates):
+    dims, gates = config_circuit(cfg, ngates=ngates)
+    ref = O2.run(dims, gates)                       # host O-2 on the full register
+    with P.State(dims) as st:
+        st.apply_circuit(gates, fuse=True)
+        err = _compare_full(st, ref)
+        nrm = st.norm()
+    del ref
+    assert err <= 1e-10, err
+    assert abs(nrm - 1.0) <= 1e-10
+
+
+def _labelled_gates(P, cfg):
+    dims = config_circuit(cfg, ngates=0)[0]
+    n, D = len(dims), int(np.prod(dims))
+    rng = np.random.default_rng(100 + cfg)
+    starts, width = _windows(D, rng)
+    idx = _idx(starts, width)
+    exp_lab = np.empty(idx.size, dtype=np.complex128)
+    exp_lab.real = idx.astype(np.float64) + 1.0
+    exp_lab.imag = -(idx.astype(np.float64) + 1.0) / 2.0
+    b = np.cumprod([1] + dims[:-1]).astype(np.float64)
+    with P.State(dims) as st:
+        _upload_labelled(st, D)
+        assert np.array_equal(_sample(st, starts, width), exp_lab)
+        for t in range(n):
+            d = dims[t]
+            # rounding scale of a class: its largest label (members differ by multiples of b_t)
+            scale = idx.astype(np.float64) + d * b[t] + 1.0
+            hi = (t + 1) % n if (t + 1) % n != t else 0
+            cases = [Gate(t, (), (), haar_unitary(d, rng), "haar"),
+                     Gate(t, (hi,), (dims[hi] - 1,), shift_x(d, 1), "cinc_hi"),
+                     Gate(t, (0 if t != 0 else 1,), (1,), shift_x(d, 1), "cinc_lo"),
+                     Gate(t, (), (), phase_gate(rng.uniform(0, 6.28, size=d)), "phase")]
+            for g in cases:
+                st.apply_gate(g.target, g.U, g.ctrl, g.vals)
+                got = _sample(st, starts, width)
+                exp = O2.gate_output_labelled(dims, g, idx)
+                if g.name.startswith("cinc"):
+                    assert np.array_equal(got, exp), (t, g.name)
+                else:
+                    rel = np.max(np.abs(got - exp) / scale)
+                    assert rel <= 1e-13, (t, g.name, rel)
+                # undo with the adjoint: back to the labels
+                st.apply_gate(g.target, g.U.conj().T, g.ctrl, g.vals)
+                back = _sample(st, starts, width)
+                if g.name.startswith("cinc"):
+                    assert np.array_equal(back, exp_lab), (t, g.name)
+                else:
+                    assert np.max(np.abs(back - exp_lab) / scale) <= 1e-13, (t, g.name)
+            if t % 6 == 5:
+                _upload_labelled(st, D)      # reset the accumulated rounding of the round trips
+
+
+def _adjoint_return(P, cfg):
+    dims, gates = config_circuit(cfg)
+    with P.State(dims) as st:
+        st.apply_circuit(gates, fuse=True)
+        nrm = st.norm()
+        st.apply_circuit(adjoint_circuit(gates), fuse=True)
+        a0 = st.amplitudes(0, 4096)
+        D = int(np.prod(dims))
+        tail = st.amplitudes(D - 4096, 4096)
+        nrm2 = st.norm()
+    assert abs(nrm - 1.0) <= 1e-10 and abs(nrm2 - 1.0) <= 1e-10
+    assert abs(a0[0] - 1.0) <= 1e-10
+    assert np.max(np.abs(a0[1:])) <= 1e-10 and np.max(np.abs(tail)) <= 1e-10
+
+
+def test_c3_prefix_parity_full_register(P):
+    _prefix_parity(P, 3, 60)
+
+
+def test_c3_labelled_every_target(P):
+    _labelled_gates(P, 3)
+
+
+def test_c3_circuit_then_adjoint(P):
+    _adjoint_return(P, 3)
+
+
+def test_c4_prefix_parity_full_register(P):
+    _prefix_parity(P, 4, 4)
+
+
+def test_c4_labelled_every_target(P):
+    _labelled_gates(P, 4)
+
+
+def test_c4_circuit_then_adjoint(P):
+    _adjoint_return(P, 4)
