@@ -86,15 +86,20 @@ def _labelled_gates(P, cfg):
     with P.State(dims) as st:
         _upload_labelled(st, D)
         assert np.array_equal(_sample(st, starts, width), exp_lab)
-        for t in range(n):
+        # pass 1: permutations (state stays exactly labelled); pass 2: general and phase gates
+        for t in [t for t in range(n)] + [t + n for t in range(n)]:
+            general = t >= n
+            t = t % n
             d = dims[t]
             # rounding scale of a class: its largest label (members differ by multiples of b_t)
             scale = idx.astype(np.float64) + d * b[t] + 1.0
             hi = (t + 1) % n if (t + 1) % n != t else 0
-            cases = [Gate(t, (), (), haar_unitary(d, rng), "haar"),
-                     Gate(t, (hi,), (dims[hi] - 1,), shift_x(d, 1), "cinc_hi"),
-                     Gate(t, (0 if t != 0 else 1,), (1,), shift_x(d, 1), "cinc_lo"),
-                     Gate(t, (), (), phase_gate(rng.uniform(0, 6.28, size=d)), "phase")]
+            if general:
+                cases = [Gate(t, (), (), haar_unitary(d, rng), "haar"),
+                         Gate(t, (), (), phase_gate(rng.uniform(0, 6.28, size=d)), "phase")]
+            else:
+                cases = [Gate(t, (hi,), (dims[hi] - 1,), shift_x(d, 1), "cinc_hi"),
+                         Gate(t, (0 if t != 0 else 1,), (1,), shift_x(d, 1), "cinc_lo")]
             for g in cases:
                 st.apply_gate(g.target, g.U, g.ctrl, g.vals)
                 got = _sample(st, starts, width)
@@ -111,7 +116,7 @@ def _labelled_gates(P, cfg):
                     assert np.array_equal(back, exp_lab), (t, g.name)
                 else:
                     assert np.max(np.abs(back - exp_lab) / scale) <= 1e-13, (t, g.name)
-            if t % 6 == 5:
+            if general and t % 8 == 7:
                 _upload_labelled(st, D)      # reset the accumulated rounding of the round trips
 
 
