@@ -152,8 +152,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 direct, 2 tiled")
     ap.add_argument("--no-fuse", action="store_true")
-    ap.add_argument("--block", action="store_true",
-                    help="multi-gate cache-blocked passes (SV_BLOCK; slower than single-gate passes on c4 so far)")
+    ap.add_argument("--block", action="store_true", help="force multi-gate cache-blocked passes (SV_BLOCK)")
+    ap.add_argument("--no-block", action="store_true", help="disable SV_BLOCK on c1-c3")
+    ap.add_argument("--graph", action="store_true", help="force a cached CUDA graph (SV_GRAPH)")
+    ap.add_argument("--no-graph", action="store_true", help="disable SV_GRAPH on c1/c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ngates", type=int, default=None)
     args = ap.parse_args()
@@ -174,9 +176,15 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     dims, gates = config_circuit(args.config, ngates=args.ngates)
+    # circuit-driver mode per workload (measured, profiles/r01): the L2-resident and deep
+    # circuits (c1-c3) gain from multi-gate passes (+ a cached CUDA graph for the launch-bound
+    # c1/c2); c4/c5 run single-gate passes with pair fusion.
     fuse = not args.no_fuse
-    block = args.block
+    block = args.block or (args.config in (1, 2, 3) and not args.no_block)
+    graph = args.graph or (args.config in (1, 2) and not args.no_graph)
     T_step = touched_total(dims, gates)                       # global amplitude updates / step
+    D_total = int(np.prod(dims, dtype=object))
+    nread = min(4096, D_total)
 
     if world > 1:
         idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
@@ -193,7 +201,7 @@ def main():
 
     def step():
         st.reset(0)
-        st.apply_circuit(ga, fuse=fuse, check=False, block=block)
+        st.apply_circuit(ga, fuse=fuse, check=False, block=block, graph=graph)
 
     for _ in range(args.warmup):
         step()
@@ -227,7 +235,7 @@ def main():
 
     # ---- e2e: the public API end to end with host buffers (gate matrices in, norm + the
     # first 4096 amplitudes out), timed on the same stream
-    out = np.empty(4096, dtype=np.complex128)
+    out = np.empty(nread, dtype=np.complex128)
     h2d = sum(16 * g.U.size + 8 * len(g.ctrl) + 8 for g in gates)
     if world > 1:
         dist.barrier()
@@ -235,16 +243,16 @@ def main():
     t0 = time.perf_counter()
     for _ in range(args.steps):
         st.reset(0)
-        st.apply_circuit(gates, fuse=fuse, check=True, block=block)   # marshals host gates each step
+        st.apply_circuit(gates, fuse=fuse, check=True, block=block, graph=graph)   # host gates each step
         nrm = st.norm()
-        st.amplitudes(0, 4096, out)
+        st.amplitudes(0, nread, out)
     t_e2e = time.perf_counter() - t0
     if world > 1:
         t = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_e2e = float(t.item())
     e2e = {"value": T_step * args.steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-           "d2h_bytes_per_step": int(8 + 16 * 4096), "norm": nrm}
+           "d2h_bytes_per_step": int(8 + 16 * nread), "norm": nrm}
 
     hbm, hbm_src = peaks()
     bytes_per_launch = prof.algorithmic_bytes / max(1, prof.launches)
@@ -271,6 +279,7 @@ def main():
             "data": "synthetic",
             "config": {"workload": CONFIG_NAMES[args.config], "dims_q0_first": dims,
                        "D": int(np.prod(dims, dtype=object)), "gates": len(gates), "fuse": fuse, "block_passes": block,
+                       "cuda_graph": graph,
                        "kernel": args.kernel, "sharded_ranks": world,
                        "l2": "state (%.1f GB) >> L2 (126 MB): no flush needed" % (16 * np.prod(dims, dtype=object) / 1e9)},
             "hbm_gbs": 32.0 * value / 1e9,

@@ -29,6 +29,10 @@ struct sv_state_s {
     struct ProfRec { cudaEvent_t a, b; double bytes; double touched; };
     std::vector<ProfRec> prof;
     std::vector<cudaEvent_t> ev_pool;
+    // SV_GRAPH: the last captured circuit, replayed while the same circuit is submitted again
+    std::vector<unsigned char> graph_key;
+    cudaGraphExec_t graph_exec = nullptr;
+    uint64_t graph_kernels = 0;
     // gate-time errors are reported through the thread-local message in sv_api.cpp
 };
 

@@ -108,6 +108,7 @@ void state_free(sv_handle h) {
     if (!h) return;
     for (auto &r : h->prof) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
+    if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
     if (h->shard) shard_destroy(h->shard);
     if (h->own_buf && h->psi) cudaFree(h->psi);
     if (h->d_partial) cudaFree(h->d_partial);
@@ -192,8 +193,40 @@ static sv_status launch_pass_on(sv_handle h, const std::vector<GateSpec> &specs,
 
 // The local circuit driver: plain (gate by gate), SV_FUSE (same-qudit runs + adjacent pairs),
 // SV_BLOCK (multi-gate cache-blocked passes), optionally captured into a CUDA graph.
+static void append_bytes(std::vector<unsigned char> &k, const void *p, size_t n) {
+    const unsigned char *c = static_cast<const unsigned char *>(p);
+    k.insert(k.end(), c, c + n);
+}
+
+// Everything a captured graph depends on: the gates (targets, controls, matrices), the flags,
+// the state buffer and the launch configuration.
+static std::vector<unsigned char> graph_key(const sv_handle h, const std::vector<GateSpec> &specs, uint32_t flags,
+                                            const double2 *buf) {
+    std::vector<unsigned char> k;
+    append_bytes(k, &flags, sizeof(flags));
+    append_bytes(k, &buf, sizeof(buf));
+    append_bytes(k, &h->cfg, sizeof(h->cfg));
+    for (const GateSpec &g : specs) {
+        const int32_t hdr[4] = {g.target, g.span, g.d, (int32_t)g.ctrl.size()};
+        append_bytes(k, hdr, sizeof(hdr));
+        for (const auto &c : g.ctrl) append_bytes(k, &c, sizeof(c));
+        append_bytes(k, g.U.data(), g.U.size() * sizeof(double2));
+    }
+    return k;
+}
+
 sv_status run_local_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_t flags, double2 *buf) {
     sv_status s = SV_OK;
+    std::vector<unsigned char> key;
+    if (flags & SV_GRAPH) {
+        key = graph_key(h, specs, flags, buf);
+        if (h->graph_exec && key == h->graph_key) {          // same circuit again: replay
+            cudaError_t e = cudaGraphLaunch(h->graph_exec, h->stream);
+            if (e != cudaSuccess) return cuda_fail(h, e, "graph launch");
+            h->launches += h->graph_kernels;
+            return SV_OK;
+        }
+    }
     std::vector<PassPlan> passes;
     if (flags & SV_BLOCK) {
         specs = merge_same_qudit(specs);
@@ -214,6 +247,7 @@ sv_status run_local_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_t 
         }
     const bool graph = (flags & SV_GRAPH) != 0;
     const bool keep_profile = h->profile;
+    const uint64_t launches0 = h->launches;
     if (graph) {
         h->profile = false;       // events cannot be recorded inside a capture for later reads
         cudaError_t e = cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal);
@@ -229,9 +263,13 @@ sv_status run_local_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_t 
         if (e2 != cudaSuccess) return cuda_fail(h, e2, "graph capture end");
         cudaGraphExec_t exec;
         cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
-        if (e == cudaSuccess) e = cudaGraphLaunch(exec, h->stream);
-        if (e == cudaSuccess) cudaGraphExecDestroy(exec);
         cudaGraphDestroy(g);
+        if (e != cudaSuccess) return cuda_fail(h, e, "graph instantiate");
+        if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+        h->graph_exec = exec;
+        h->graph_key.swap(key);
+        h->graph_kernels = h->launches - launches0;
+        e = cudaGraphLaunch(exec, h->stream);
         if (e != cudaSuccess) return cuda_fail(h, e, "graph launch");
     }
     return s;

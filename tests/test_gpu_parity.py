@@ -389,3 +389,23 @@ def test_block_passes_labelled_bit_exact(P):
     got, _, launched = run_gpu(P, dims, gates, psi0, block=True)
     assert launched < len(gates)
     assert np.array_equal(got, ref)
+
+
+def test_graph_cache_replays_same_circuit_and_recaptures_changes(P):
+    """SV_GRAPH keeps the instantiated graph of the last circuit and replays it when the
+    same circuit (same matrices, controls, flags) is submitted again; any change recaptures."""
+    dims, gates = config_circuit(2, ngates=300)
+    ref = O2.run(dims, gates)
+    ref2 = O2.run(dims, gates + gates)
+    with P.State(dims) as st:
+        for block in (False, True):
+            st.reset(0)
+            st.apply_circuit(gates, graph=True, block=block)
+            assert np.max(np.abs(st.amplitudes() - ref)) <= 1e-10
+            st.apply_circuit(gates, graph=True, block=block)       # replay on the evolved state
+            assert np.max(np.abs(st.amplitudes() - ref2)) <= 1e-10
+        changed = list(gates)
+        changed[7] = Gate(changed[7].target, changed[7].ctrl, changed[7].vals, changed[7].U.conj().T)
+        st.reset(0)
+        st.apply_circuit(changed, graph=True)
+        assert np.max(np.abs(st.amplitudes() - O2.run(dims, changed))) <= 1e-10
