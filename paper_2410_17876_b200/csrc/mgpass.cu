@@ -313,31 +313,63 @@ __device__ __forceinline__ void apply_gate_tile(const PassParams &p, const PassG
 
 }  // namespace
 
+__device__ __forceinline__ void compute_barrier(int nthreads) {   // named barrier 1: compute warps only
+    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Warp-specialised: warps 0..NT/32-1 compute, warp NT/32 is the producer (TMA loads, stage
+// records, TMA stores).  full[s] completes when a tile's bytes have landed; done[s] when the
+// compute warps have finished it (after fence.proxy.async, so the bulk store sees their writes).
 template <int NT>
-__global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_gate_pass(const __grid_constant__ PassParams p, int S, int TE) {
+__global__ void __launch_bounds__(NT + 32, NT <= 256 ? 2 : 1) k_gate_pass(const __grid_constant__ PassParams p, int S, int TE) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double2 *bufs = reinterpret_cast<double2 *>(smem_raw);
     double2 *Us = bufs + (size_t)S * TE;                       // the pass's matrices
     StageInfo *sinfo = reinterpret_cast<StageInfo *>(Us + p.upool);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(sinfo + S);
+    uint64_t *full = reinterpret_cast<uint64_t *>(sinfo + S);
+    uint64_t *done = full + S;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
-        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&done[s], 1); }
         fence_mbar_init();
     }
-    for (int k = tid; k < p.upool; k += NT) Us[k] = p.U[k];
+    for (int k = tid; k < p.upool; k += NT + 32) Us[k] = p.U[k];
     __syncthreads();
     const uint64_t first = blockIdx.x, step = gridDim.x;
     if (first >= p.ntiles) return;
     const uint64_t my = (p.ntiles - first + step - 1) / step;
-    if (warp == 0)
-        for (int i = 0; i < S - 1 && (uint64_t)i < my; ++i)
-            issue_loads(p, first + (uint64_t)i * step, bufs + (size_t)i * TE, &bars[i], &sinfo[i], lane);
 
+    if (warp == NT / 32) {
+        // ---------------- producer warp
+        for (uint64_t i = 0; i < my + (uint64_t)S; ++i) {
+            const int s = (int)(i % (uint64_t)S);
+            if (i >= (uint64_t)S) {                   // drain tile i-S from stage s
+                const uint64_t j = i - (uint64_t)S;
+                if (j >= my) continue;
+                mbar_wait(&done[s], (uint32_t)((j / (uint64_t)S) & 1));
+                const StageInfo &si = sinfo[s];
+                for (int m = lane; m < p.M; m += 32)
+                    bulk_store(p.psi + si.ti.gbase + p.moff[m], bufs + (size_t)s * TE + (size_t)m * p.LT,
+                               si.ti.len * (uint32_t)sizeof(double2));
+                bulk_commit();
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                __syncwarp();
+            }
+            if (i < my)
+                issue_loads(p, first + i * step, bufs + (size_t)s * TE, &full[s], &sinfo[s], lane);
+        }
+        bulk_wait_all();
+        return;
+    }
+
+    // ---------------- compute warps
     for (uint64_t i = 0; i < my; ++i) {
         const int s = (int)(i % (uint64_t)S);
         double2 *buf = bufs + (size_t)s * TE;
-        mbar_wait(&bars[s], (uint32_t)((i / (uint64_t)S) & 1));
+        mbar_wait(&full[s], (uint32_t)((i / (uint64_t)S) & 1));
         const StageInfo &si = sinfo[s];
         const uint32_t len = si.ti.len;
         const uint32_t fire = si.fire;
@@ -352,25 +384,12 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_gate_pass(const __gri
                 case 5: apply_gate_tile<5, NT>(p, g, buf, Us, len, lo, tid); break;
                 default: apply_gate_tile<0, NT>(p, g, buf, Us, len, lo, tid); break;
             }
-            __syncthreads();
+            compute_barrier(NT);
         }
         fence_proxy_async();
-        __syncthreads();
-        if (warp == 0) {
-            const uint64_t gbase = si.ti.gbase;
-            for (int m = lane; m < p.M; m += 32)
-                bulk_store(p.psi + gbase + p.moff[m], buf + (size_t)m * p.LT, len * (uint32_t)sizeof(double2));
-            bulk_commit();
-            const uint64_t nxt = i + (uint64_t)(S - 1);
-            if (nxt < my) {
-                bulk_wait_read_1();
-                __syncwarp();
-                const int sn = (int)(nxt % (uint64_t)S);
-                issue_loads(p, first + nxt * step, bufs + (size_t)sn * TE, &bars[sn], &sinfo[sn], lane);
-            }
-        }
+        compute_barrier(NT);
+        if (tid == 0) mbar_arrive(&done[s]);
     }
-    if (warp == 0) bulk_wait_all();
 }
 
 // ------------------------------------------------------------------------------ host
@@ -491,7 +510,7 @@ cudaError_t launch_pass_t(const PassParams &p, cudaStream_t st, const LaunchCfg 
     const int S = cfg.pass_stages, TE = cfg.pass_tile;
     // size for the largest matrix pool so the attribute and the occupancy are set once per config
     const size_t smem = (size_t)S * TE * sizeof(double2) + (size_t)kPoolC * sizeof(double2) +
-                        (size_t)S * sizeof(StageInfo) + (size_t)S * sizeof(uint64_t);
+                        (size_t)S * sizeof(StageInfo) + (size_t)2 * S * sizeof(uint64_t);
     static size_t configured = 0, occ_for = 0;
     static int occ = 1;
     if (configured < smem) {
@@ -501,13 +520,13 @@ cudaError_t launch_pass_t(const PassParams &p, cudaStream_t st, const LaunchCfg 
     }
     if (occ_for != smem) {   // resident CTAs per SM at this smem size (persistent grid)
         int o = 1;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_gate_pass<NT>, NT, smem) != cudaSuccess || o < 1) o = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_gate_pass<NT>, NT + 32, smem) != cudaSuccess || o < 1) o = 1;
         occ = o;
         occ_for = smem;
     }
     const uint64_t cap = (uint64_t)cfg.num_sms * (uint64_t)occ;
     const unsigned grid = (unsigned)(p.ntiles < cap ? p.ntiles : cap);
-    k_gate_pass<NT><<<grid, NT, smem, st>>>(p, S, TE);
+    k_gate_pass<NT><<<grid, NT + 32, smem, st>>>(p, S, TE);
     return cudaGetLastError();
 }
 
