@@ -324,7 +324,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 // records, TMA stores).  full[s] completes when a tile's bytes have landed; done[s] when the
 // compute warps have finished it (after fence.proxy.async, so the bulk store sees their writes).
 template <int NT>
-__global__ void __launch_bounds__(NT + 32, NT <= 256 ? 2 : 1) k_gate_pass(const __grid_constant__ PassParams p, int S, int TE) {
+__global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant__ PassParams p, int S, int TE) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double2 *bufs = reinterpret_cast<double2 *>(smem_raw);
     double2 *Us = bufs + (size_t)S * TE;                       // the pass's matrices
