@@ -176,11 +176,11 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     dims, gates = config_circuit(args.config, ngates=args.ngates)
-    # circuit-driver mode per workload (measured, profiles/r01): the L2-resident and deep
-    # circuits (c1-c3) gain from multi-gate passes (+ a cached CUDA graph for the launch-bound
-    # c1/c2); c4/c5 run single-gate passes with pair fusion.
+    # circuit-driver mode per workload (measured, profiles/r01/passbench_*): multi-gate passes
+    # (SV_BLOCK) on c1-c4, plus a cached CUDA graph for the launch-bound c1/c2; sharded runs
+    # use single-gate passes with pair fusion on each slice.
     fuse = not args.no_fuse
-    block = args.block or (args.config in (1, 2, 3) and not args.no_block)
+    block = args.block or (args.config in (1, 2, 3, 4) and not args.no_block)
     graph = args.graph or (args.config in (1, 2) and not args.no_graph)
     T_step = touched_total(dims, gates)                       # global amplitude updates / step
     D_total = int(np.prod(dims, dtype=object))

@@ -59,9 +59,9 @@ void default_cfg(LaunchCfg &c, int device) {
     c.tile_stages = 3;
     c.ctas_per_sm = 2;
     c.num_sms = sms;
-    c.pass_tile = 4096;
-    c.pass_stages = 3;
-    c.pass_threads = 512;
+    c.pass_tile = 6144;        // measured best on c3/c4 (profiles/r01/passbench_*)
+    c.pass_stages = 2;
+    c.pass_threads = 256;
     c.pass_gates = 24;
 }
 
