@@ -258,15 +258,18 @@ def main():
     bytes_per_launch = prof.algorithmic_bytes / max(1, prof.launches)
     ms_per_launch = prof.kernel_ms / max(1, prof.launches)
     achieved = bytes_per_launch / (ms_per_launch / 1e3) / 1e9 if prof.launches else None
+    # bytes the launches must move at least (a multi-gate pass: the state once)
+    state_bytes_per_launch = prof.state_bytes / max(1, prof.launches)
+    state_gbs = state_bytes_per_launch / (ms_per_launch / 1e3) / 1e9 if prof.launches else None
     traffic = None
     tr_path = os.path.join(ROOT, "profiles", "traffic.json")
     traffic_note = None
     if os.path.exists(tr_path):
         try:
-            tr = json.load(open(tr_path)).get(f"config{args.config}")
-            # DRAM bytes / algorithmic bytes from one `ncu --set full` capture of the dominant
-            # kernel (reduced register), applied to this run's algorithmic bytes per launch
-            traffic = tr["ratio_dram_to_algorithmic"] * bytes_per_launch
+            tr = json.load(open(tr_path))["block" if block else "single"]
+            # DRAM bytes / minimum bytes from one `ncu --set full` capture of the dominant kernel
+            # (reduced register), applied to this run's minimum bytes per launch
+            traffic = tr["ratio_dram_to_state_bytes"] * state_bytes_per_launch
             traffic_note = tr["source"]
         except Exception:
             traffic = None
@@ -287,8 +290,13 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
                          "traffic_source": traffic_note,
-                         "peak_source": hbm_src, "kernel": "gate kernels (all launches of the step)",
+                         "peak_source": hbm_src,
+                         "kernel": ("k_gate_pass (multi-gate passes) + single-gate kernels" if block
+                                    else "single-gate kernels (k_gate_tiled / k_gate_direct)"),
+                         "algorithmic": "32 B x sum of touched amplitudes of the gates applied (SURVEY.md 8(d))",
                          "bytes_per_launch": bytes_per_launch, "ms_per_launch": ms_per_launch,
+                         "state_bytes_per_launch": state_bytes_per_launch,
+                         "state_gbs": state_gbs,
                          "launches_timed": int(prof.launches)},
             "e2e": e2e,
             "gpu_launches": int(launches),

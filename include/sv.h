@@ -186,8 +186,10 @@ SV_API sv_status sv_set_option(sv_handle h, int32_t option, int64_t value);
 typedef struct {
     uint64_t launches;
     double kernel_ms;
-    double algorithmic_bytes;
-    double touched;          /* amplitude updates (sum of T over the launched gates)        */
+    double algorithmic_bytes;  /* 32 B x sum of T over the gates the launches applied           */
+    double touched;            /* amplitude updates (sum of T over the launched gates)          */
+    double state_bytes;        /* bytes the launches must move at least: a single-gate launch
+                                  32 B x T; a multi-gate pass (SV_BLOCK) 32 B x the state once  */
 } sv_profile;
 SV_API sv_status sv_profile_read(sv_handle h, int32_t reset, sv_profile *out);
 

@@ -26,7 +26,7 @@ struct sv_state_s {
     ShardCtx *shard = nullptr;     // non-null for sharded handles
     // SV_OPT_PROFILE: events bracketing each gate launch
     bool profile = false;
-    struct ProfRec { cudaEvent_t a, b; double bytes; double touched; };
+    struct ProfRec { cudaEvent_t a, b; double bytes; double touched; double state_bytes; };
     std::vector<ProfRec> prof;
     std::vector<cudaEvent_t> ev_pool;
     // SV_GRAPH: the last captured circuit, replayed while the same circuit is submitted again

@@ -150,7 +150,7 @@ sv_status launch_on(sv_handle h, const GatePlan &p, double2 *buf) {
     if (e != cudaSuccess) return cuda_fail(h, e, "gate kernel launch");
     if (h->profile) {
         cudaEventRecord(b, h->stream);
-        h->prof.push_back({a, b, 32.0 * (double)p.touched, (double)p.touched});
+        h->prof.push_back({a, b, 32.0 * (double)p.touched, (double)p.touched, 32.0 * (double)p.touched});
     }
     return SV_OK;
 }
@@ -175,8 +175,9 @@ static sv_status launch_pass_on(sv_handle h, const std::vector<GateSpec> &specs,
         ++h->launches;
         if (h->profile) {
             cudaEventRecord(b, h->stream);
-            // a pass moves the local state once: 16 B read + 16 B write per amplitude
-            h->prof.push_back({a, b, 32.0 * (double)h->local.D, touched});
+            // algorithmic bytes per SURVEY.md §8(d): 32 B per touched amplitude of every gate the
+            // pass applies; the pass itself moves the local state once (16 B read + 16 B write)
+            h->prof.push_back({a, b, 32.0 * touched, touched, 32.0 * (double)h->local.D});
         }
         return SV_OK;
     }
@@ -484,11 +485,13 @@ sv_status sv_profile_read(sv_handle h, int32_t reset, sv_profile *out) {
     out->kernel_ms = 0.0;
     out->algorithmic_bytes = 0.0;
     out->touched = 0.0;
+    out->state_bytes = 0.0;
     for (auto &r : h->prof) {
         float ms = 0.f;
         if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) out->kernel_ms += ms;
         out->algorithmic_bytes += r.bytes;
         out->touched += r.touched;
+        out->state_bytes += r.state_bytes;
     }
     if (reset) {
         for (auto &r : h->prof) { h->ev_pool.push_back(r.a); h->ev_pool.push_back(r.b); }

@@ -47,7 +47,7 @@ class sv_info(C.Structure):
 
 class sv_profile(C.Structure):
     _fields_ = [("launches", C.c_uint64), ("kernel_ms", C.c_double),
-                ("algorithmic_bytes", C.c_double), ("touched", C.c_double)]
+                ("algorithmic_bytes", C.c_double), ("touched", C.c_double), ("state_bytes", C.c_double)]
 
 
 class sv_gate_plan(C.Structure):
