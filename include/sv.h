@@ -51,7 +51,11 @@ extern "C" {
 
 typedef struct sv_state_s *sv_handle;
 
-typedef enum { SV_C128 = 0, SV_C64 = 1 /* not yet supported: SV_ERR_UNSUPPORTED */ } sv_dtype;
+/* Element type of the state.  SV_C128: complex128 (the BASELINE configs).  SV_C64: complex64
+ * (8 B per amplitude, arithmetic in fp32; single-GPU handles only -- sharded SV_C64 returns
+ * SV_ERR_UNSUPPORTED -- and SV_BLOCK falls back to single-gate passes).  The ABI's amplitude
+ * buffers and matrices are always doubles; SV_C64 rounds them on the way in. */
+typedef enum { SV_C128 = 0, SV_C64 = 1 } sv_dtype;
 
 typedef enum {
     SV_OK = 0,

@@ -14,31 +14,20 @@ namespace svi {
 
 namespace {
 
-// complex fma helpers: acc += u * x
-__device__ __forceinline__ void cfma(double2 &acc, const double2 u, const double2 x) {
-    acc.x = fma(u.x, x.x, acc.x);
-    acc.x = fma(-u.y, x.y, acc.x);
-    acc.y = fma(u.x, x.y, acc.y);
-    acc.y = fma(u.y, x.x, acc.y);
-}
-__device__ __forceinline__ double2 cmul(const double2 u, const double2 x) {
-    return make_double2(fma(u.x, x.x, -u.y * x.y), fma(u.x, x.y, u.y * x.x));
-}
-
 // ------------------------------------------------------------------------------------------
 // Direct kernel: one class per thread iteration, grid-stride over the class ids.
 // Gather x_j = psi[base + j b_k], y = U x, scatter in place.
 // Coalesced when the lowest removed stride is >= 32 amplitudes (consecutive class ids map to
-// consecutive addresses within each block).
+// consecutive addresses within each block).  V = double2 (complex128) or float2 (complex64).
 // ------------------------------------------------------------------------------------------
-template <int DIM, int MD, int KIND>
-__global__ void __launch_bounds__(256) k_gate_direct(const __grid_constant__ GateParams<MD> p) {
+template <int DIM, int MD, int KIND, typename V>
+__global__ void __launch_bounds__(256) k_gate_direct(const __grid_constant__ GateParams<MD, V> p) {
     const int d = DIM ? DIM : p.d;
     const uint64_t bk = p.bk;
     const uint64_t step = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t f = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; f < p.F; f += step) {
-        double2 *ptr = p.psi + insert_digits(f, p.nrem, p.rem);
-        double2 x[MD];
+        V *ptr = p.psi + insert_digits(f, p.nrem, p.rem);
+        V x[MD];
         if (KIND == kGeneral) {
 #pragma unroll
             for (int j = 0; j < MD; ++j)
@@ -46,7 +35,7 @@ __global__ void __launch_bounds__(256) k_gate_direct(const __grid_constant__ Gat
 #pragma unroll
             for (int i = 0; i < MD; ++i) {
                 if (DIM || i < d) {
-                    double2 acc = make_double2(0.0, 0.0);
+                    V acc = cz<V>();
 #pragma unroll
                     for (int j = 0; j < MD; ++j)
                         if (DIM || j < d) cfma(acc, p.U[i * MD + j], x[j]);
@@ -67,8 +56,8 @@ __global__ void __launch_bounds__(256) k_gate_direct(const __grid_constant__ Gat
     }
 }
 
-template <int MD>
-void fill_params(GateParams<MD> &q, const GatePlan &p, double2 *psi) {
+template <int MD, typename V>
+void fill_params(GateParams<MD, V> &q, const GatePlan &p, V *psi) {
     q.psi = psi;
     q.F = p.F;
     q.bk = p.bk;
@@ -78,27 +67,33 @@ void fill_params(GateParams<MD> &q, const GatePlan &p, double2 *psi) {
     q.nrem = p.nrem;
     for (int i = 0; i < MD; ++i) q.sigma[i] = (i < p.d) ? p.sigma[i] : i;
     for (int i = 0; i < p.nrem; ++i) q.rem[i] = p.rem[i];
-    for (int i = 0; i < MD * MD; ++i) q.U[i] = make_double2(0.0, 0.0);
+    for (int i = 0; i < MD * MD; ++i) q.U[i] = to_v<V>(make_double2(0.0, 0.0));
     if (p.kind == kGeneral) {
         for (int i = 0; i < p.d; ++i)
-            for (int j = 0; j < p.d; ++j) q.U[i * MD + j] = p.U[i * p.d + j];
+            for (int j = 0; j < p.d; ++j) q.U[i * MD + j] = to_v<V>(p.U[i * p.d + j]);
     } else {
-        for (int j = 0; j < p.d; ++j) q.U[j] = p.U[j];
+        for (int j = 0; j < p.d; ++j) q.U[j] = to_v<V>(p.U[j]);
     }
 }
 
-template <int DIM, int MD>
-cudaError_t launch_direct_t(const GatePlan &p, double2 *psi, cudaStream_t st, const LaunchCfg &cfg) {
-    GateParams<MD> q;
-    fill_params<MD>(q, p, psi);
+template <int DIM, int MD, typename V>
+cudaError_t launch_direct_v(const GatePlan &p, V *psi, cudaStream_t st, const LaunchCfg &cfg) {
+    GateParams<MD, V> q;
+    fill_params<MD, V>(q, p, psi);
     const uint64_t want = (p.F + 255) / 256;
     const uint64_t cap = (uint64_t)cfg.num_sms * 16;
     const unsigned blocks = (unsigned)(want < cap ? want : cap);
     if (p.kind == kGeneral)
-        k_gate_direct<DIM, MD, kGeneral><<<blocks, 256, 0, st>>>(q);
+        k_gate_direct<DIM, MD, kGeneral, V><<<blocks, 256, 0, st>>>(q);
     else
-        k_gate_direct<DIM, MD, kMonomial><<<blocks, 256, 0, st>>>(q);
+        k_gate_direct<DIM, MD, kMonomial, V><<<blocks, 256, 0, st>>>(q);
     return cudaGetLastError();
+}
+
+template <int DIM, int MD>
+cudaError_t launch_direct_t(const GatePlan &p, double2 *psi, cudaStream_t st, const LaunchCfg &cfg) {
+    if (cfg.c64) return launch_direct_v<DIM, MD, float2>(p, reinterpret_cast<float2 *>(psi), st, cfg);
+    return launch_direct_v<DIM, MD, double2>(p, psi, st, cfg);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -107,17 +102,18 @@ cudaError_t launch_direct_t(const GatePlan &p, double2 *psi, cudaStream_t st, co
 constexpr int kNormParts = 1184;   // 8 per SM on 148 SMs
 constexpr int kNormThreads = 256;
 
-__global__ void __launch_bounds__(kNormThreads) k_norm_partial(const double2 *__restrict__ psi,
+template <typename V>
+__global__ void __launch_bounds__(kNormThreads) k_norm_partial(const V *__restrict__ psi,
                                                                uint64_t D, double *partial) {
     __shared__ double red[kNormThreads];
     const uint64_t chunk = (D + gridDim.x - 1) / gridDim.x;
     const uint64_t lo = (uint64_t)blockIdx.x * chunk;
     const uint64_t hi = lo + chunk < D ? lo + chunk : D;
-    double s = 0.0;
+    double s = 0.0;                                   // fp64 accumulation for both precisions
     for (uint64_t i = lo + threadIdx.x; i < hi; i += kNormThreads) {
-        const double2 a = psi[i];
-        s = fma(a.x, a.x, s);
-        s = fma(a.y, a.y, s);
+        const V a = psi[i];
+        s = fma((double)a.x, (double)a.x, s);
+        s = fma((double)a.y, (double)a.y, s);
     }
     red[threadIdx.x] = s;
     __syncthreads();
@@ -170,7 +166,8 @@ __global__ void __launch_bounds__(256) k_combine(double2 *__restrict__ loc,
     }
 }
 
-__global__ void k_set_one(double2 *psi, uint64_t idx) { psi[idx] = make_double2(1.0, 0.0); }
+template <typename V>
+__global__ void k_set_one(V *psi, uint64_t idx) { psi[idx] = to_v<V>(make_double2(1.0, 0.0)); }
 
 }  // namespace
 
@@ -217,10 +214,13 @@ cudaError_t launch_gate(const GatePlan &p, double2 *psi, cudaStream_t st, const 
 }
 
 cudaError_t launch_set_basis(double2 *psi, uint64_t D, uint64_t idx, cudaStream_t st,
-                             uint64_t *launches) {
-    cudaError_t e = cudaMemsetAsync(psi, 0, D * sizeof(double2), st);
+                             uint64_t *launches, bool c64) {
+    cudaError_t e = cudaMemsetAsync(psi, 0, D * (c64 ? sizeof(float2) : sizeof(double2)), st);
     if (e != cudaSuccess) return e;
-    k_set_one<<<1, 1, 0, st>>>(psi, idx);
+    if (c64)
+        k_set_one<float2><<<1, 1, 0, st>>>(reinterpret_cast<float2 *>(psi), idx);
+    else
+        k_set_one<double2><<<1, 1, 0, st>>>(psi, idx);
     if (launches) ++*launches;
     return cudaGetLastError();
 }
@@ -239,8 +239,11 @@ cudaError_t launch_combine(double2 *loc, const double2 *partner, uint64_t n, uin
 }
 
 cudaError_t launch_norm2(const double2 *psi, uint64_t D, double *partial, int nparts, double *out,
-                         cudaStream_t st, uint64_t *launches) {
-    k_norm_partial<<<nparts, kNormThreads, 0, st>>>(psi, D, partial);
+                         cudaStream_t st, uint64_t *launches, bool c64) {
+    if (c64)
+        k_norm_partial<float2><<<nparts, kNormThreads, 0, st>>>(reinterpret_cast<const float2 *>(psi), D, partial);
+    else
+        k_norm_partial<double2><<<nparts, kNormThreads, 0, st>>>(psi, D, partial);
     k_norm_final<<<1, kNormThreads, 0, st>>>(partial, nparts, out);
     if (launches) *launches += 2;
     return cudaGetLastError();

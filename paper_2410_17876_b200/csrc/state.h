@@ -18,6 +18,8 @@ struct sv_state_s {
     bool own_stream = false;
     double2 *psi = nullptr;
     bool own_buf = false;
+    bool c64 = false;              // SV_C64: the state is float2 (8 B per amplitude)
+    size_t elem = 16;              // bytes per amplitude
     double *d_partial = nullptr;   // norm partials + 1 result slot
     uint64_t launches = 0;
     uint64_t exchanges = 0;

@@ -86,7 +86,8 @@ sv_status state_init_device(sv_handle h, int device, void *cuda_stream, void *ex
         if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaStreamCreate");
         h->own_stream = true;
     }
-    const uint64_t bytes = h->local.D * sizeof(double2);
+    h->cfg.c64 = h->c64 ? 1 : 0;
+    const uint64_t bytes = h->local.D * h->elem;
     if (ext) {
         if (ext_bytes < bytes || ((uintptr_t)ext & 15))
             return fail(SV_ERR_INVALID_ARG, "external buffer too small or misaligned");
@@ -119,7 +120,7 @@ void state_free(sv_handle h) {
 // local sum of squares (device -> host), synchronising
 sv_status local_norm2(sv_handle h, double *out) {
     cudaError_t e = launch_norm2(h->psi, h->local.D, h->d_partial, norm_parts(),
-                                 h->d_partial + norm_parts(), h->stream, &h->launches);
+                                 h->d_partial + norm_parts(), h->stream, &h->launches, h->c64);
     if (e != cudaSuccess) return cuda_fail(h, e, "norm kernel");
     e = cudaMemcpyAsync(out, h->d_partial + norm_parts(), sizeof(double), cudaMemcpyDeviceToHost, h->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
@@ -229,6 +230,7 @@ sv_status run_local_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_t 
         }
     }
     std::vector<PassPlan> passes;
+    if ((flags & SV_BLOCK) && h->c64) flags = (flags & ~SV_BLOCK) | SV_FUSE;   // pass kernel: c128 only
     if (flags & SV_BLOCK) {
         specs = merge_same_qudit(specs);
         passes = plan_passes(h->local, specs, (uint64_t)h->cfg.pass_tile, h->cfg.pass_gates, 64);
@@ -289,13 +291,14 @@ sv_status sv_create_ex(const int32_t *dims, int32_t n, sv_dtype dt, int device, 
                        void *ext_device_buf, size_t ext_bytes, sv_handle *out) {
     if (!out) return fail(SV_ERR_INVALID_ARG, "null out");
     *out = nullptr;
-    if (dt == SV_C64) return fail(SV_ERR_UNSUPPORTED, "complex64 is not implemented yet");
-    if (dt != SV_C128) return fail(SV_ERR_INVALID_ARG, "unknown dtype");
+    if (dt != SV_C128 && dt != SV_C64) return fail(SV_ERR_INVALID_ARG, "unknown dtype");
     sv_handle h = new (std::nothrow) sv_state_s();
     if (!h) return fail(SV_ERR_NOMEM, "host allocation");
     sv_status s = make_register(dims, n, &h->reg, &g_err);
     if (s != SV_OK) { delete h; return s; }
     h->local = h->reg;
+    h->c64 = dt == SV_C64;
+    h->elem = h->c64 ? sizeof(float2) : sizeof(double2);
     if (h->reg.D > (UINT64_MAX >> 5)) { delete h; return fail(SV_ERR_NOMEM, "state too large"); }
     s = state_init_device(h, device, cuda_stream, ext_device_buf, ext_bytes);
     if (s != SV_OK) { state_free(h); return s; }
@@ -310,7 +313,6 @@ sv_status sv_create(const int32_t *dims, int32_t n, sv_dtype dt, sv_handle *out)
     sv_status s = make_register(dims, n, &probe, &g_err);
     if (s != SV_OK) return s;
     if (!out) return fail(SV_ERR_INVALID_ARG, "null out");
-    if (dt == SV_C64) return fail(SV_ERR_UNSUPPORTED, "complex64 is not implemented yet");
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) { cudaGetLastError(); return fail(SV_ERR_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e)); }
@@ -329,7 +331,7 @@ sv_status sv_reset(sv_handle h, uint64_t basis_index) {
     if (s != SV_OK) return s;
     if (basis_index >= h->reg.D) return fail(SV_ERR_INDEX_RANGE, "basis index >= D");
     if (h->shard) return shard_reset(h, basis_index);
-    cudaError_t e = launch_set_basis(h->psi, h->local.D, basis_index, h->stream, &h->launches);
+    cudaError_t e = launch_set_basis(h->psi, h->local.D, basis_index, h->stream, &h->launches, h->c64);
     if (e != cudaSuccess) return cuda_fail(h, e, "reset");
     return SV_OK;
 }
@@ -376,6 +378,22 @@ sv_status sv_amplitudes(sv_handle h, uint64_t first, uint64_t count, double *out
     if (!out) return fail(SV_ERR_INVALID_ARG, "null out");
     if (first >= h->reg.D || count > h->reg.D - first) return fail(SV_ERR_INDEX_RANGE, "range outside [0, D)");
     if (h->shard) return shard_amplitudes(h, first, count, out);
+    if (h->c64) {                           // complex64: widen to the ABI's doubles on the host
+        const uint64_t chunk = 1ull << 24;
+        std::vector<float2> tmp((size_t)(count < chunk ? count : chunk));
+        const float2 *src = reinterpret_cast<const float2 *>(h->psi) + first;
+        for (uint64_t o = 0; o < count; o += chunk) {
+            const uint64_t n = count - o < chunk ? count - o : chunk;
+            cudaError_t e = cudaMemcpyAsync(tmp.data(), src + o, n * sizeof(float2), cudaMemcpyDeviceToHost, h->stream);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+            if (e != cudaSuccess) return cuda_fail(h, e, "amplitude readback");
+            for (uint64_t i = 0; i < n; ++i) {
+                out[2 * (o + i)] = tmp[i].x;
+                out[2 * (o + i) + 1] = tmp[i].y;
+            }
+        }
+        return SV_OK;
+    }
     cudaError_t e = cudaMemcpyAsync(out, h->psi + first, count * sizeof(double2), cudaMemcpyDeviceToHost, h->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
     if (e != cudaSuccess) return cuda_fail(h, e, "amplitude readback");
@@ -389,6 +407,20 @@ sv_status sv_set_amplitudes(sv_handle h, uint64_t first, uint64_t count, const d
     if (!in) return fail(SV_ERR_INVALID_ARG, "null in");
     if (first >= h->reg.D || count > h->reg.D - first) return fail(SV_ERR_INDEX_RANGE, "range outside [0, D)");
     if (h->shard) return shard_set_amplitudes(h, first, count, in);
+    if (h->c64) {                           // complex64: round the ABI's doubles on the host
+        const uint64_t chunk = 1ull << 24;
+        std::vector<float2> tmp((size_t)(count < chunk ? count : chunk));
+        float2 *dst = reinterpret_cast<float2 *>(h->psi) + first;
+        for (uint64_t o = 0; o < count; o += chunk) {
+            const uint64_t n = count - o < chunk ? count - o : chunk;
+            for (uint64_t i = 0; i < n; ++i)
+                tmp[i] = make_float2((float)in[2 * (o + i)], (float)in[2 * (o + i) + 1]);
+            cudaError_t e = cudaMemcpyAsync(dst + o, tmp.data(), n * sizeof(float2), cudaMemcpyHostToDevice, h->stream);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+            if (e != cudaSuccess) return cuda_fail(h, e, "amplitude upload");
+        }
+        return SV_OK;
+    }
     cudaError_t e = cudaMemcpyAsync(h->psi + first, in, count * sizeof(double2), cudaMemcpyHostToDevice, h->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
     if (e != cudaSuccess) return cuda_fail(h, e, "amplitude upload");

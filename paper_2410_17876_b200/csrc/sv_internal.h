@@ -99,11 +99,46 @@ __host__ __device__ __forceinline__ uint64_t insert_digits(uint64_t f, int nrem,
 
 enum GateKind : int32_t { kGeneral = 0, kMonomial = 1 };
 
+// complex element types: V = double2 (complex128, SV_C128) or float2 (complex64, SV_C64);
+// the arithmetic is done in V's precision (the paper fixes none; R11).
+template <typename V> struct RealOf;
+template <> struct RealOf<double2> { using type = double; };
+template <> struct RealOf<float2> { using type = float; };
+
+__host__ __device__ __forceinline__ double2 mkv(double x, double y, const double2 *) { return make_double2(x, y); }
+__host__ __device__ __forceinline__ float2 mkv(double x, double y, const float2 *) {
+    return make_float2((float)x, (float)y);
+}
+template <typename V> __host__ __device__ __forceinline__ V to_v(double2 u) { return mkv(u.x, u.y, (const V *)nullptr); }
+template <typename V> __host__ __device__ __forceinline__ V cz() { return mkv(0.0, 0.0, (const V *)nullptr); }
+
+#ifdef __CUDACC__
+// complex fused multiply-add acc += u * x and product u * x, in V's precision
+__device__ __forceinline__ void cfma(double2 &acc, const double2 u, const double2 x) {
+    acc.x = fma(u.x, x.x, acc.x);
+    acc.x = fma(-u.y, x.y, acc.x);
+    acc.y = fma(u.x, x.y, acc.y);
+    acc.y = fma(u.y, x.x, acc.y);
+}
+__device__ __forceinline__ void cfma(float2 &acc, const float2 u, const float2 x) {
+    acc.x = fmaf(u.x, x.x, acc.x);
+    acc.x = fmaf(-u.y, x.y, acc.x);
+    acc.y = fmaf(u.x, x.y, acc.y);
+    acc.y = fmaf(u.y, x.x, acc.y);
+}
+__device__ __forceinline__ double2 cmul(const double2 u, const double2 x) {
+    return make_double2(fma(u.x, x.x, -u.y * x.y), fma(u.x, x.y, u.y * x.x));
+}
+__device__ __forceinline__ float2 cmul(const float2 u, const float2 x) {
+    return make_float2(fmaf(u.x, x.x, -u.y * x.y), fmaf(u.x, x.y, u.y * x.x));
+}
+#endif
+
 // Kernel parameters of one gate launch, passed by value (__grid_constant__).  MD is the
 // compile-time capacity of the target dimension.
-template <int MD>
+template <int MD, typename V = double2>
 struct GateParams {
-    double2 *psi;
+    V *psi;
     uint64_t F;          // classes to visit (control-satisfying)
     uint64_t bk;         // target stride b_k
     int32_t d;           // target dimension (<= MD)
@@ -112,7 +147,7 @@ struct GateParams {
     int32_t nrem;
     int32_t sigma[MD];   // monomial: member j -> sigma[j]
     RemovedRun rem[kMaxRem];
-    double2 U[MD * MD];  // general: row-major U; monomial: U[j] = coefficient of member j
+    V U[MD * MD];        // general: row-major U; monomial: U[j] = coefficient of member j
 };
 
 // Host-side plan of one (possibly fused) gate on a (local) register.
@@ -147,14 +182,16 @@ struct LaunchCfg {
     int pass_stages;   // smem ring stages of the pass kernel
     int pass_threads;  // threads per CTA of the pass kernel (256 or 512)
     int pass_gates;    // max gates per pass
+    int c64;           // 1: the state is complex64 (float2), else complex128 (double2)
 };
 
+// psi points at the state in the handle's element type (cfg.c64 / the c64 flag).
 cudaError_t launch_gate(const GatePlan &p, double2 *psi, cudaStream_t st, const LaunchCfg &cfg,
                         uint64_t *launches);
 cudaError_t launch_set_basis(double2 *psi, uint64_t D, uint64_t idx, cudaStream_t st,
-                             uint64_t *launches);
+                             uint64_t *launches, bool c64 = false);
 cudaError_t launch_norm2(const double2 *psi, uint64_t D, double *partial, int nparts,
-                         double *out, cudaStream_t st, uint64_t *launches);
+                         double *out, cudaStream_t st, uint64_t *launches, bool c64 = false);
 int norm_parts();
 
 }  // namespace svi

@@ -46,9 +46,9 @@ struct InnerCtrl {
     uint32_t v;
 };
 
-template <int MD>
+template <int MD, typename V = double2>
 struct TileParams {
-    double2 *psi;
+    V *psi;
     int32_t mode, kind, d, nm;
     uint64_t bk;
     int32_t nrem;
@@ -69,7 +69,7 @@ struct TileParams {
     uint32_t active;
     int32_t ninner;
     InnerCtrl inner[kMaxInner];
-    double2 U[MD * MD];      // general: row-major (stride MD); monomial: U[j] = coef of member j
+    V U[MD * MD];            // general: row-major (stride MD); monomial: U[j] = coef of member j
 };
 
 struct Piece {
@@ -116,15 +116,6 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
-__device__ __forceinline__ void cfma(double2 &acc, const double2 u, const double2 x) {
-    acc.x = fma(u.x, x.x, acc.x);
-    acc.x = fma(-u.y, x.y, acc.x);
-    acc.y = fma(u.x, x.y, acc.y);
-    acc.y = fma(u.y, x.x, acc.y);
-}
-__device__ __forceinline__ double2 cmul(const double2 u, const double2 x) {
-    return make_double2(fma(u.x, x.x, -u.y * x.y), fma(u.x, x.y, u.y * x.x));
-}
 
 // ------------------------------------------------------------------------------ tiles
 struct TileDesc {
@@ -134,8 +125,8 @@ struct TileDesc {
     uint32_t len;    // classes (W) / elements (N) per run piece
 };
 
-template <int MD>
-__device__ __forceinline__ TileDesc tile_desc(const TileParams<MD> &p, uint64_t t) {
+template <int MD, typename V>
+__device__ __forceinline__ TileDesc tile_desc(const TileParams<MD, V> &p, uint64_t t) {
     TileDesc td;
     if (p.rpt == 1) {
         uint64_t sub;
@@ -156,8 +147,8 @@ __device__ __forceinline__ TileDesc tile_desc(const TileParams<MD> &p, uint64_t 
 }
 
 // warp 0: fill the piece table of a stage and issue the bulk loads
-template <int MD>
-__device__ __forceinline__ void issue_tile_loads(const TileParams<MD> &p, uint64_t t, double2 *buf,
+template <int MD, typename V>
+__device__ __forceinline__ void issue_tile_loads(const TileParams<MD, V> &p, uint64_t t, V *buf,
                                                  Piece *pieces, uint32_t *npieces, uint64_t *bar,
                                                  int lane) {
     const TileDesc td = tile_desc(p, t);
@@ -165,7 +156,7 @@ __device__ __forceinline__ void issue_tile_loads(const TileParams<MD> &p, uint64
     const uint32_t np = td.nr * (uint32_t)nm;
     if (lane == 0) {
         *npieces = np;
-        mbar_expect_tx(bar, np * td.len * (uint32_t)sizeof(double2));
+        mbar_expect_tx(bar, np * td.len * (uint32_t)sizeof(V));
     }
     __syncwarp();
     for (uint32_t q = lane; q < np; q += 32) {
@@ -184,12 +175,12 @@ __device__ __forceinline__ void issue_tile_loads(const TileParams<MD> &p, uint64
         }
         pc.len = td.len;
         pieces[q] = pc;
-        bulk_load(buf + pc.s, p.psi + pc.g, pc.len * (uint32_t)sizeof(double2), bar);
+        bulk_load(buf + pc.s, p.psi + pc.g, pc.len * (uint32_t)sizeof(V), bar);
     }
 }
 
-template <int MD>
-__device__ __forceinline__ bool inner_ok(const TileParams<MD> &p, const uint32_t *offmod, uint32_t pos) {
+template <int MD, typename V>
+__device__ __forceinline__ bool inner_ok(const TileParams<MD, V> &p, const uint32_t *offmod, uint32_t pos) {
     bool ok = true;
 #pragma unroll 1
     for (int c = 0; c < p.ninner; ++c) {
@@ -203,13 +194,13 @@ __device__ __forceinline__ bool inner_ok(const TileParams<MD> &p, const uint32_t
     return ok;
 }
 
-template <int DIM, int MD, int MODE, int KIND>
-__global__ void __launch_bounds__(kTileThreads) k_gate_tiled(const __grid_constant__ TileParams<MD> p,
+template <int DIM, int MD, int MODE, int KIND, typename V>
+__global__ void __launch_bounds__(kTileThreads) k_gate_tiled(const __grid_constant__ TileParams<MD, V> p,
                                                              int S, int TE) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    double2 *bufs = reinterpret_cast<double2 *>(smem_raw);
+    V *bufs = reinterpret_cast<V *>(smem_raw);
     const int maxp = TE / 32;
-    Piece *ptab = reinterpret_cast<Piece *>(smem_raw + (size_t)S * TE * sizeof(double2));
+    Piece *ptab = reinterpret_cast<Piece *>(smem_raw + (size_t)S * TE * sizeof(V));
     uint32_t *npc = reinterpret_cast<uint32_t *>(ptab + (size_t)S * maxp);
     uint64_t *bars = reinterpret_cast<uint64_t *>(npc + ((S + 1) & ~1));
 
@@ -237,7 +228,7 @@ __global__ void __launch_bounds__(kTileThreads) k_gate_tiled(const __grid_consta
     for (uint64_t i = 0; i < my; ++i) {
         const int s = (int)(i % (uint64_t)S);
         const uint64_t t = first + i * step;
-        double2 *buf = bufs + (size_t)s * TE;
+        V *buf = bufs + (size_t)s * TE;
         mbar_wait(&bars[s], (uint32_t)((i / (uint64_t)S) & 1));
 
         if (KIND != kTPerm || MODE == kModeN) {
@@ -259,14 +250,14 @@ __global__ void __launch_bounds__(kTileThreads) k_gate_tiled(const __grid_consta
                         if (!inner_ok(p, offmod, pos)) continue;
                     }
                     if (KIND == kTGeneral) {
-                        double2 x[MD];
+                        V x[MD];
 #pragma unroll
                         for (int j = 0; j < MD; ++j)
                             if (DIM || j < d) x[j] = buf[j * p.MS + c];
 #pragma unroll
                         for (int i2 = 0; i2 < MD; ++i2) {
                             if (DIM || i2 < d) {
-                                double2 acc = make_double2(0.0, 0.0);
+                                V acc = cz<V>();
 #pragma unroll
                                 for (int j = 0; j < MD; ++j)
                                     if (DIM || j < d) cfma(acc, p.U[i2 * MD + j], x[j]);
@@ -274,7 +265,7 @@ __global__ void __launch_bounds__(kTileThreads) k_gate_tiled(const __grid_consta
                             }
                         }
                     } else {   // monomial with coefficients: slot jj holds member members[jj]
-                        double2 x[MD];
+                        V x[MD];
 #pragma unroll
                         for (int jj = 0; jj < MD; ++jj)
                             if (jj < p.nm) x[jj] = buf[jj * p.MS + c];
@@ -298,8 +289,8 @@ __global__ void __launch_bounds__(kTileThreads) k_gate_tiled(const __grid_consta
                         if (td.nr > 1) fastdiv32(e, p.R32, p.mR32, pos);
                         if (!inner_ok(p, offmod, pos)) continue;
                     }
-                    double2 *cls = buf + e;
-                    double2 x[MD];
+                    V *cls = buf + e;
+                    V x[MD];
                     if (KIND == kTGeneral) {
 #pragma unroll
                         for (int j = 0; j < MD; ++j)
@@ -307,7 +298,7 @@ __global__ void __launch_bounds__(kTileThreads) k_gate_tiled(const __grid_consta
 #pragma unroll
                         for (int i2 = 0; i2 < MD; ++i2) {
                             if (DIM || i2 < d) {
-                                double2 acc = make_double2(0.0, 0.0);
+                                V acc = cz<V>();
 #pragma unroll
                                 for (int j = 0; j < MD; ++j)
                                     if (DIM || j < d) cfma(acc, p.U[i2 * MD + j], x[j]);
@@ -340,7 +331,7 @@ __global__ void __launch_bounds__(kTileThreads) k_gate_tiled(const __grid_consta
                     const int j = p.members[jj];
                     g = g + ((uint64_t)p.sigma[j] - (uint64_t)j) * p.bk;
                 }
-                bulk_store(p.psi + g, buf + pc.s, pc.len * (uint32_t)sizeof(double2));
+                bulk_store(p.psi + g, buf + pc.s, pc.len * (uint32_t)sizeof(V));
             }
             bulk_commit();
             // refill the stage of tile i-1 once its store has finished reading smem
@@ -358,8 +349,8 @@ __global__ void __launch_bounds__(kTileThreads) k_gate_tiled(const __grid_consta
 }
 
 // ------------------------------------------------------------------------------ host
-template <int MD>
-bool plan_tiled(const GatePlan &g, double2 *psi, const LaunchCfg &cfg, TileParams<MD> &p) {
+template <int MD, typename V>
+bool plan_tiled(const GatePlan &g, V *psi, const LaunchCfg &cfg, TileParams<MD, V> &p) {
     memset(&p, 0, sizeof(p));
     const int d = g.d;
     const uint64_t bk = g.bk;
@@ -395,14 +386,14 @@ bool plan_tiled(const GatePlan &g, double2 *psi, const LaunchCfg &cfg, TileParam
         p.nm = d;
         for (int j = 0; j < d; ++j) { p.members[j] = j; p.slot_of[j] = j; p.sigma[j] = j; }
         for (int i = 0; i < d; ++i)
-            for (int j = 0; j < d; ++j) p.U[i * MD + j] = g.U[i * d + j];
+            for (int j = 0; j < d; ++j) p.U[i * MD + j] = to_v<V>(g.U[i * d + j]);
     } else {
         bool pure = true;
         int nm = 0;
         for (int j = 0; j < MD; ++j) p.slot_of[j] = -1;
         for (int j = 0; j < d; ++j) {
             p.sigma[j] = g.sigma[j];
-            p.U[j] = g.U[j];
+            p.U[j] = to_v<V>(g.U[j]);
             if ((g.active >> j) & 1) {
                 p.slot_of[j] = nm;
                 p.members[nm++] = j;
@@ -489,15 +480,15 @@ bool plan_tiled(const GatePlan &g, double2 *psi, const LaunchCfg &cfg, TileParam
     return p.ntiles > 0;
 }
 
-template <int DIM, int MD, int MODE, int KIND>
-cudaError_t launch_tiled_k(const TileParams<MD> &p, const LaunchCfg &cfg, cudaStream_t st) {
+template <int DIM, int MD, int MODE, int KIND, typename V>
+cudaError_t launch_tiled_k(const TileParams<MD, V> &p, const LaunchCfg &cfg, cudaStream_t st) {
     const int S = cfg.tile_stages, TE = cfg.tile_elems;
-    const size_t smem = (size_t)S * TE * sizeof(double2) + (size_t)S * (TE / 32) * sizeof(Piece) +
+    const size_t smem = (size_t)S * TE * sizeof(V) + (size_t)S * (TE / 32) * sizeof(Piece) +
                         (size_t)((S + 1) & ~1) * sizeof(uint32_t) + (size_t)S * sizeof(uint64_t);
     static size_t configured = 0;
     static size_t occ_for = 0;
     static int occ = 1;
-    auto kfn = k_gate_tiled<DIM, MD, MODE, KIND>;
+    auto kfn = k_gate_tiled<DIM, MD, MODE, KIND, V>;
     if (configured < smem) {
         cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -516,19 +507,25 @@ cudaError_t launch_tiled_k(const TileParams<MD> &p, const LaunchCfg &cfg, cudaSt
     return cudaGetLastError();
 }
 
-template <int DIM, int MD>
-cudaError_t launch_tiled_d(const GatePlan &g, double2 *psi, cudaStream_t st, const LaunchCfg &cfg, bool *handled) {
-    TileParams<MD> p;
-    if (!plan_tiled<MD>(g, psi, cfg, p)) { *handled = false; return cudaSuccess; }
+template <int DIM, int MD, typename V>
+cudaError_t launch_tiled_v(const GatePlan &g, V *psi, cudaStream_t st, const LaunchCfg &cfg, bool *handled) {
+    TileParams<MD, V> p;
+    if (!plan_tiled<MD, V>(g, psi, cfg, p)) { *handled = false; return cudaSuccess; }
     *handled = true;
     if (p.mode == kModeW) {
-        if (p.kind == kTGeneral) return launch_tiled_k<DIM, MD, kModeW, kTGeneral>(p, cfg, st);
-        if (p.kind == kTMono) return launch_tiled_k<DIM, MD, kModeW, kTMono>(p, cfg, st);
-        return launch_tiled_k<DIM, MD, kModeW, kTPerm>(p, cfg, st);
+        if (p.kind == kTGeneral) return launch_tiled_k<DIM, MD, kModeW, kTGeneral, V>(p, cfg, st);
+        if (p.kind == kTMono) return launch_tiled_k<DIM, MD, kModeW, kTMono, V>(p, cfg, st);
+        return launch_tiled_k<DIM, MD, kModeW, kTPerm, V>(p, cfg, st);
     }
-    if (p.kind == kTGeneral) return launch_tiled_k<DIM, MD, kModeN, kTGeneral>(p, cfg, st);
-    if (p.kind == kTMono) return launch_tiled_k<DIM, MD, kModeN, kTMono>(p, cfg, st);
-    return launch_tiled_k<DIM, MD, kModeN, kTPerm>(p, cfg, st);
+    if (p.kind == kTGeneral) return launch_tiled_k<DIM, MD, kModeN, kTGeneral, V>(p, cfg, st);
+    if (p.kind == kTMono) return launch_tiled_k<DIM, MD, kModeN, kTMono, V>(p, cfg, st);
+    return launch_tiled_k<DIM, MD, kModeN, kTPerm, V>(p, cfg, st);
+}
+
+template <int DIM, int MD>
+cudaError_t launch_tiled_d(const GatePlan &g, double2 *psi, cudaStream_t st, const LaunchCfg &cfg, bool *handled) {
+    if (cfg.c64) return launch_tiled_v<DIM, MD, float2>(g, reinterpret_cast<float2 *>(psi), st, cfg, handled);
+    return launch_tiled_v<DIM, MD, double2>(g, psi, st, cfg, handled);
 }
 
 }  // namespace svi

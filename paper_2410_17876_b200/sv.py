@@ -152,14 +152,16 @@ class State:
     """A dense complex128 statevector on one B200 (or one shard of a sharded state)."""
 
     def __init__(self, dims: Sequence[int], device: int = 0, stream=None, ext_buffer=None,
-                 ext_bytes: int = 0, _handle=None):
+                 ext_bytes: int = 0, _handle=None, dtype: str = "c128"):
         self.dims = [int(d) for d in dims]
         if _handle is not None:
             self._h = _handle
             return
+        if dtype not in ("c128", "c64"):
+            raise ValueError("dtype must be 'c128' or 'c64'")
         d = _i32(self.dims)
         h = _h()
-        _check(_lib.sv_create_ex(d.ctypes.data_as(_i32p), d.size, SV_C128, int(device),
+        _check(_lib.sv_create_ex(d.ctypes.data_as(_i32p), d.size, SV_C128 if dtype == "c128" else SV_C64, int(device),
                                  C.c_void_p(stream) if stream else None,
                                  C.c_void_p(ext_buffer) if ext_buffer else None,
                                  int(ext_bytes), C.byref(h)))

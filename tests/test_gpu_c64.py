@@ -1,0 +1,112 @@
+"""complex64 states (SV_C64) against the fp64 oracle.
+
+Tolerance (R17): one gate rounds every class output y = U x in fp32 with at most
+2d FMAs per component plus the fp32 rounding of U, so ||dy||_2 <= (2d + 1) sqrt(d) u ||x||_2
+with u = 2^-24; unitary gates carry earlier errors unchanged, so after G gates
+||psi_c64 - psi_exact||_2 <= G (2 d_max + 1) sqrt(d_max) 2^-24 (plus the fp32 rounding of the
+input state when one is uploaded).  Permutations move values without arithmetic: bit-exact
+on labelled states whose labels are exact in fp32 (D < 2^24)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from oracle import blocksim as O2  # noqa: E402
+from sv_inputs import (Gate, config_circuit, random_circuit, random_state, labelled_state,  # noqa: E402
+                       permutation_matrix, shift_x, haar_unitary, ghz_circuit)
+
+U32 = 2.0 ** -24
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2410_17876_b200 as P
+    return P
+
+
+def bound(gates, dims, extra=0.0):
+    dmax = max(dims[g.target] for g in gates) if gates else 2
+    return len(gates) * (2 * dmax + 1) * np.sqrt(dmax) * U32 + extra
+
+
+def run_c64(P, dims, gates, psi0=None, kernel=0, fuse=False, block=False):
+    with P.State(dims, dtype="c64") as st:
+        st.set_option(P.sv.SV_OPT_KERNEL, kernel)
+        if psi0 is not None:
+            st.set_amplitudes(0, psi0)
+        st.apply_circuit(gates, fuse=fuse, block=block)
+        return st.amplitudes(), st.norm()
+
+
+@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+def test_configs_c64_against_fp64_oracle(P, kernel, cfg):
+    nq = {3: 6, 4: 1}.get(cfg)
+    dims, gates = config_circuit(cfg, nqubits=nq) if nq else config_circuit(cfg)
+    if cfg == 2:
+        gates = gates[:1200]
+    ref = O2.run(dims, gates)
+    got, nrm = run_c64(P, dims, gates, kernel=kernel, fuse=True, block=True)
+    err = float(np.linalg.norm(got - ref))
+    tol = bound(gates, dims)
+    assert err <= tol, (err, tol)
+    assert abs(nrm - 1.0) <= tol
+
+
+def test_random_sweep_c64(P):
+    rng = np.random.default_rng(64)
+    for s in range(30):
+        n = int(rng.integers(2, 7))
+        dims = [int(x) for x in rng.integers(2, 6, size=n)]
+        _, gates = random_circuit(64_000 + s, dims, 40, max_ctrl=2)
+        psi0 = random_state(int(np.prod(dims)), s)
+        ref = O2.run(dims, gates, psi0)
+        for kernel in (1, 2):
+            got, _ = run_c64(P, dims, gates, psi0, kernel=kernel)
+            # input rounding to fp32 adds at most sqrt(2) u per amplitude (||.||_2 <= sqrt(2) u)
+            assert np.linalg.norm(got - ref) <= bound(gates, dims, np.sqrt(2) * U32)
+
+
+def test_labelled_permutations_bit_exact_c64(P):
+    rng = np.random.default_rng(7)
+    dims = [5, 3, 4, 2, 3, 2, 2, 3]
+    n, D = len(dims), int(np.prod(dims))
+    assert D < 2 ** 24
+    gates = []
+    for _ in range(80):
+        t = int(rng.integers(n))
+        others = [q for q in range(n) if q != t]
+        nc = int(rng.integers(0, 3))
+        ctrl = tuple(int(c) for c in rng.choice(others, size=nc, replace=False))
+        vals = tuple(int(rng.integers(dims[c])) for c in ctrl)
+        gates.append(Gate(t, ctrl, vals, permutation_matrix(rng.permutation(dims[t]))))
+    lab = labelled_state(0, D)
+    ref = O2.run(dims, gates, lab)
+    for kernel in (1, 2):
+        got, _ = run_c64(P, dims, gates, lab, kernel=kernel)
+        assert np.array_equal(got, ref)
+
+
+def test_ghz_c64_exact_to_fp32(P):
+    for d, n in ((2, 20), (3, 12), (5, 8)):
+        dims, gates = ghz_circuit(d, n)
+        got, _ = run_c64(P, dims, gates)
+        rep = sum(d ** k for k in range(n))
+        idx = [v * rep for v in range(d)]
+        s = np.float32(1.0 / np.sqrt(d))
+        assert np.flatnonzero(got).tolist() == idx
+        assert all(got[i].real == float(s) and got[i].imag == 0.0 for i in idx)
+
+
+def test_c64_state_is_half_the_bytes(P):
+    import torch
+    dims = [3] * 12
+    before = torch.cuda.mem_get_info()[0]
+    st = P.State(dims, dtype="c64")
+    used = before - torch.cuda.mem_get_info()[0]
+    st.close()
+    D = 3 ** 12
+    assert used < 16 * D          # 8 B per amplitude (+ small scratch), not 16
