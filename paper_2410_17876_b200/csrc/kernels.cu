@@ -183,8 +183,10 @@ cudaError_t launch_gate(const GatePlan &p, double2 *psi, cudaStream_t st, const 
     // satisfying classes.
     // Fused targets with d >= 10 are FP64-issue heavy; the direct kernel (more warps per SM)
     // hides that better than the tiled kernel's compute phase (profiles/r01: d=12/16 pairs).
-    bool use_tiled = cfg.kernel == 2;
-    if (cfg.kernel == 0) {
+    // complex64: cp.async.bulk needs 16-byte aligned addresses and sizes, which 8-byte
+    // amplitudes at odd offsets violate, so SV_C64 always runs the direct kernel.
+    bool use_tiled = cfg.kernel == 2 && !cfg.c64;
+    if (cfg.kernel == 0 && !cfg.c64) {
         use_tiled = p.d <= 9;
         for (int i = 0; i < p.nctrl; ++i)
             if (p.cb[i] < 32) use_tiled = false;
