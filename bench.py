@@ -184,6 +184,8 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="disable SV_GRAPH on c1/c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ngates", type=int, default=None)
+    ap.add_argument("--dtype", default="c128", choices=["c128", "c64"],
+                    help="state element type (BASELINE configs: c128; c64 = SV_C64, fp32 arithmetic)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -219,7 +221,7 @@ def main():
         dist.broadcast(idt, 0)
         st = P.State.sharded(dims, rank, world, bytes(idt.cpu().numpy()), device=local_rank)
     else:
-        st = P.State(dims, device=local_rank)
+        st = P.State(dims, device=local_rank, dtype=args.dtype)
     st.set_option(P.sv.SV_OPT_KERNEL, args.kernel)
     ga = P.sv._GateArray(gates)
     info = st.info()
@@ -300,19 +302,22 @@ def main():
         except Exception:
             traffic = None
 
+    bpu = 32.0 if args.dtype == "c128" else 16.0      # bytes per amplitude update (read + write)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+            "dtype": "f64" if args.dtype == "c128" else "f32",
             "data": "synthetic",
             "config": {"workload": CONFIG_NAMES[args.config], "dims_q0_first": dims,
+                       "state_dtype": "complex128" if args.dtype == "c128" else "complex64",
                        "D": int(np.prod(dims, dtype=object)), "gates": len(gates), "fuse": fuse, "block_passes": block,
                        "cuda_graph": graph,
                        "kernel": args.kernel, "sharded_ranks": world,
                        "l2": "state (%.1f GB) >> L2 (126 MB): no flush needed" % (16 * np.prod(dims, dtype=object) / 1e9)},
-            "hbm_gbs": 32.0 * value / 1e9,
-            "hbm_frac_of_measured": 32.0 * value / 1e9 / hbm if world == 1 else None,
+            "hbm_gbs": bpu * value / 1e9,
+            "hbm_frac_of_measured": bpu * value / 1e9 / hbm if world == 1 else None,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
                          "traffic_source": traffic_note,

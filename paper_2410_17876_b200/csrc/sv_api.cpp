@@ -151,7 +151,8 @@ sv_status launch_on(sv_handle h, const GatePlan &p, double2 *buf) {
     if (e != cudaSuccess) return cuda_fail(h, e, "gate kernel launch");
     if (h->profile) {
         cudaEventRecord(b, h->stream);
-        h->prof.push_back({a, b, 32.0 * (double)p.touched, (double)p.touched, 32.0 * (double)p.touched});
+        const double bpu = 2.0 * (double)h->elem;     // one read + one write per touched amplitude
+        h->prof.push_back({a, b, bpu * (double)p.touched, (double)p.touched, bpu * (double)p.touched});
     }
     return SV_OK;
 }
