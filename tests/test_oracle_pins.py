@@ -274,3 +274,33 @@ def test_sampled_gate_output_matches_full_apply():
             idx = rng.choice(D, size=200, replace=False)
             got = O2.gate_output_labelled(dims, g, idx)
             assert np.max(np.abs(got - psi[idx]) / np.abs(psi[idx])) < 1e-15
+
+
+# ------------------------------------------------------------------ O-3 (sparse, §2.3)
+def test_sparse_oracle_matches_dense_oracle():
+    from oracle import sparse as O3
+    rng = np.random.default_rng(33)
+    for s in range(60):
+        n = int(rng.integers(1, 6))
+        dims = [int(x) for x in rng.integers(2, 6, size=n)]
+        _, gates = random_circuit(40_000 + s, dims, int(rng.integers(1, 25)), max_ctrl=2)
+        dense = O2.run(dims, gates)
+        sp = O3.run(dims, gates)
+        rebuilt = np.zeros_like(dense)
+        for i, a in sp.items():
+            rebuilt[i] = a
+        assert np.max(np.abs(rebuilt - dense)) < 1e-12           # pruned entries are < 1e-12
+        assert all(abs(a) >= O3.EPS for a in sp.values())
+
+
+@pytest.mark.parametrize("d,n", [(2, 62), (3, 39), (4, 31), (5, 27)])
+def test_sparse_oracle_ghz_at_the_papers_maxima(d, n):
+    """GHZ reaches 62 qubits, 39 qutrits, 31 ququads, 27 ququints (the 64-bit
+    index limit); the state has exactly d entries at v*(1+d+...+d^{n-1}), each fl(1/sqrt d)."""
+    from oracle import sparse as O3
+    dims, gates = ghz_circuit(d, n)
+    st = O3.run(dims, gates)
+    rep = sum(d ** k for k in range(n))
+    assert sorted(st) == [v * rep for v in range(d)]
+    assert max(st) < 2 ** 63
+    assert all(a == 1.0 / np.sqrt(d) for a in st.values())
