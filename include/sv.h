@@ -249,6 +249,32 @@ SV_API sv_status sv_shard_plan(const int32_t *dims, int32_t n, int32_t nranks, i
 
 SV_API const char *sv_version(void);
 
+/* ---- sparse states (the paper's "Our Method (Sparse)") --
+ * The state is the list of basis indices holding a non-zero amplitude (complex128, sorted by
+ * index, on the device).  A gate transforms only the classes that hold a stored index: column v
+ * of U times the amplitude of each stored member with target digit v, summed per index
+ * (PAPER.md:222); entries whose controls do not hold are unchanged; amplitudes
+ * with |a| < eps are dropped afterwards.  D must be <= 2^63 (the paper's 64-bit index limit,
+ * PAPER.md:489), so GHZ reaches 62 qubits, 39 qutrits, 31 ququads, 27 ququints. */
+typedef struct sv_sparse_s *sv_sparse_handle;
+
+/* State = e_0.  eps <= 0 selects 1e-12.  SV_ERR_OVERFLOW if D > 2^63. */
+SV_API sv_status sv_sparse_create(const int32_t *dims, int32_t n, double eps, sv_sparse_handle *out);
+SV_API sv_status sv_sparse_destroy(sv_sparse_handle h);
+SV_API sv_status sv_sparse_reset(sv_sparse_handle h, uint64_t basis_index);
+/* Same argument conventions and validation as sv_apply_gate / sv_apply_circuit (flags:
+ * SV_NO_CHECK only).  Each gate synchronises (the new entry count sizes the next gate). */
+SV_API sv_status sv_sparse_apply_gate(sv_sparse_handle h, int32_t target, const int32_t *ctrl,
+                                      const int32_t *ctrl_vals, int32_t nctrl, const double *U);
+SV_API sv_status sv_sparse_apply_circuit(sv_sparse_handle h, const sv_gate *gates, int64_t ngates,
+                                         uint32_t flags);
+SV_API sv_status sv_sparse_nnz(sv_sparse_handle h, uint64_t *out);
+/* Copy min(cap, nnz) entries (ascending index) into idx[] and amp[] (2 doubles each);
+ * *n receives nnz. */
+SV_API sv_status sv_sparse_entries(sv_sparse_handle h, uint64_t cap, uint64_t *idx, double *amp,
+                                   uint64_t *n);
+SV_API sv_status sv_sparse_launches(sv_sparse_handle h, uint64_t *out);
+
 #ifdef __cplusplus
 }
 #endif

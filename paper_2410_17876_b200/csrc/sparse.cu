@@ -1,0 +1,384 @@
+// sparse.cu — the paper's sparse variant ("Our Method (Sparse)"; SURVEY.md
+// §8 f3) on the GPU.  The state is the list of basis indices with non-zero amplitude, sorted.
+// A gate visits only the classes that hold a stored index ("identify all basis
+// states with non-zero amplitudes in a given class"): every stored amplitude a at index i with
+// target digit v contributes U[k][v] a to the class member base + k b_t, base = i - v b_t
+// (column v of U, skipping exact zeros), entries whose controls do not hold pass through
+// unchanged; the contributions are radix-sorted by index, summed per index
+// (the vector addition of PAPER.md:222) and amplitudes below eps are dropped.
+// Our kernels do the method's arithmetic; CUB provides the sort / reduce-by-key / select
+// primitives (library calls, like cuBLAS for a GEMM).
+#include <cuda_runtime.h>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
+#include <cub/device/device_select.cuh>
+
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "plan.h"
+#include "../../include/sv.h"
+
+namespace svi {
+
+std::string *err_slot();
+sv_status fail_msg(sv_status s, const std::string &msg);
+
+struct SparseGateP {
+    uint64_t bt, mbt;            // target stride (+ magic)
+    uint64_t dt, mdt;            // target dim (+ magic)
+    int32_t nctrl;
+    uint64_t cb[kMaxRem], mcb[kMaxRem], cd[kMaxRem], mcd[kMaxRem], cv[kMaxRem];
+    int32_t fan;                 // output slots per stored amplitude
+    int32_t nrow[kMaxDim];       // per column v: non-zero rows
+    int32_t rows[kMaxDim][kMaxDim];
+    double2 coef[kMaxDim][kMaxDim];   // coef[v][r] = U[rows[v][r]][v]
+    uint64_t invalid;            // key of unused slots (= D, sorts after every index)
+};
+
+namespace {
+
+__global__ void k_sparse_expand(const uint64_t *__restrict__ keys, const double2 *__restrict__ vals, uint64_t nnz,
+                                const __grid_constant__ SparseGateP g, uint64_t *okeys, double2 *ovals) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nnz) return;
+    const uint64_t i = keys[e];
+    const double2 a = vals[e];
+    uint64_t *ok = okeys + e * (uint64_t)g.fan;
+    double2 *ov = ovals + e * (uint64_t)g.fan;
+    bool fire = true;
+    for (int c = 0; c < g.nctrl; ++c) {                       // floor(i/b_c) mod d_c == v_c
+        uint64_t r, r2;
+        const uint64_t q = fastdiv64(i, g.cb[c], g.mcb[c], r);
+        fastdiv64(q, g.cd[c], g.mcd[c], r2);
+        fire = fire && (r2 == g.cv[c]);
+    }
+    if (!fire) {
+        ok[0] = i;
+        ov[0] = a;
+        for (int s = 1; s < g.fan; ++s) { ok[s] = g.invalid; ov[s] = make_double2(0.0, 0.0); }
+        return;
+    }
+    uint64_t r;
+    const uint64_t q = fastdiv64(i, g.bt, g.mbt, r);
+    uint64_t v;
+    fastdiv64(q, g.dt, g.mdt, v);                            // target digit of i
+    const uint64_t base = i - v * g.bt;                       // the class's member with digit 0
+    for (int s = 0; s < g.fan; ++s) {
+        if (s < g.nrow[v]) {
+            ok[s] = base + (uint64_t)g.rows[v][s] * g.bt;
+            ov[s] = cmul(g.coef[v][s], a);
+        } else {
+            ok[s] = g.invalid;
+            ov[s] = make_double2(0.0, 0.0);
+        }
+    }
+}
+
+__global__ void k_sparse_flags(const uint64_t *keys, const double2 *vals, uint64_t n, uint64_t invalid,
+                               double eps2, unsigned char *flags) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    const double2 a = vals[e];
+    flags[e] = (keys[e] != invalid) && (a.x * a.x + a.y * a.y >= eps2);
+}
+
+__global__ void k_sparse_set(uint64_t *keys, double2 *vals, uint64_t idx) {
+    keys[0] = idx;
+    vals[0] = make_double2(1.0, 0.0);
+}
+
+struct CSum {
+    __device__ __forceinline__ double2 operator()(const double2 &a, const double2 &b) const {
+        return make_double2(a.x + b.x, a.y + b.y);
+    }
+};
+
+}  // namespace
+}  // namespace svi
+
+using namespace svi;
+
+struct sv_sparse_s {
+    Register reg;
+    double eps = 1e-12;
+    cudaStream_t stream = nullptr;
+    uint64_t nnz = 0, cap = 0;
+    uint64_t *keys = nullptr, *keys2 = nullptr;       // state (sorted) / scratch
+    double2 *vals = nullptr, *vals2 = nullptr;
+    unsigned char *flags = nullptr;
+    void *tmp = nullptr;
+    size_t tmp_bytes = 0;
+    uint64_t *d_count = nullptr;
+    int nbits = 64;
+    uint64_t launches = 0;
+    bool broken = false;
+};
+
+namespace {
+
+sv_status sp_cuda(sv_sparse_handle h, cudaError_t e, const char *where) {
+    if (h) h->broken = true;
+    return fail_msg(SV_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+template <typename T>
+cudaError_t grow(T *&p, uint64_t n) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    return cudaMalloc(&p, n * sizeof(T) + 16);
+}
+
+// ensure room for n slots in every buffer
+cudaError_t reserve(sv_sparse_handle h, uint64_t n) {
+    if (n <= h->cap) return cudaSuccess;
+    uint64_t c = h->cap ? h->cap : 1024;
+    while (c < n) c *= 2;
+    // keep the live state across the resize
+    uint64_t *nk = nullptr;
+    double2 *nv = nullptr;
+    cudaError_t e = cudaMalloc(&nk, c * sizeof(uint64_t));
+    if (e == cudaSuccess) e = cudaMalloc(&nv, c * sizeof(double2));
+    if (e != cudaSuccess) return e;
+    if (h->nnz) {
+        e = cudaMemcpyAsync(nk, h->keys, h->nnz * sizeof(uint64_t), cudaMemcpyDeviceToDevice, h->stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(nv, h->vals, h->nnz * sizeof(double2), cudaMemcpyDeviceToDevice, h->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+        if (e != cudaSuccess) return e;
+    }
+    if (h->keys) cudaFree(h->keys);
+    if (h->vals) cudaFree(h->vals);
+    h->keys = nk;
+    h->vals = nv;
+    e = grow(h->keys2, c);
+    if (e == cudaSuccess) e = grow(h->vals2, c);
+    if (e == cudaSuccess) e = grow(h->flags, c);
+    h->cap = c;
+    return e;
+}
+
+cudaError_t ensure_tmp(sv_sparse_handle h, size_t bytes) {
+    if (bytes <= h->tmp_bytes) return cudaSuccess;
+    if (h->tmp) cudaFree(h->tmp);
+    h->tmp = nullptr;
+    h->tmp_bytes = 0;
+    cudaError_t e = cudaMalloc(&h->tmp, bytes);
+    if (e == cudaSuccess) h->tmp_bytes = bytes;
+    return e;
+}
+
+sv_status sparse_gate(sv_sparse_handle h, const GateSpec &g) {
+    const Register &reg = h->reg;
+    SparseGateP p;
+    std::memset(&p, 0, sizeof(p));
+    const int d = g.d;
+    p.bt = reg.b[g.target];
+    p.mbt = make_fastdiv64(p.bt).m;
+    p.dt = (uint64_t)d;
+    p.mdt = make_fastdiv64(p.dt).m;
+    p.invalid = reg.D;
+    if ((int)g.ctrl.size() > kMaxRem) return fail_msg(SV_ERR_UNSUPPORTED, "too many controls");
+    p.nctrl = (int32_t)g.ctrl.size();
+    for (size_t c = 0; c < g.ctrl.size(); ++c) {
+        p.cb[c] = reg.b[g.ctrl[c].q];
+        p.mcb[c] = make_fastdiv64(p.cb[c]).m;
+        p.cd[c] = (uint64_t)reg.dims[g.ctrl[c].q];
+        p.mcd[c] = make_fastdiv64(p.cd[c]).m;
+        p.cv[c] = (uint64_t)g.ctrl[c].v;
+    }
+    int fan = 1;
+    for (int v = 0; v < d; ++v) {                  // column v: the image of |v>
+        int nr = 0;
+        for (int r = 0; r < d; ++r) {
+            const double2 u = g.U[r * d + v];
+            if (u.x != 0.0 || u.y != 0.0) {
+                p.rows[v][nr] = r;
+                p.coef[v][nr] = u;
+                ++nr;
+            }
+        }
+        p.nrow[v] = nr;
+        fan = nr > fan ? nr : fan;
+    }
+    p.fan = fan;
+    const uint64_t n = h->nnz, N = n * (uint64_t)fan;
+    if (n == 0) return SV_OK;
+    cudaError_t e = reserve(h, N);
+    if (e != cudaSuccess) return sp_cuda(h, e, "sparse reserve");
+    const unsigned blocks = (unsigned)((n + 255) / 256);
+    k_sparse_expand<<<blocks, 256, 0, h->stream>>>(h->keys, h->vals, n, p, h->keys2, h->vals2);
+    ++h->launches;
+    // sort the contributions by basis index (stable: a fixed, deterministic summation order)
+    size_t need = 0, t = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, need, h->keys2, h->keys, h->vals2, h->vals, (int64_t)N, 0, h->nbits);
+    cub::DeviceReduce::ReduceByKey(nullptr, t, h->keys, h->keys2, h->vals, h->vals2, h->d_count, CSum(), (int64_t)N);
+    need = need > t ? need : t;
+    cub::DeviceSelect::Flagged(nullptr, t, h->keys2, h->flags, h->keys, h->d_count + 1, (int64_t)N);
+    need = need > t ? need : t;
+    cub::DeviceSelect::Flagged(nullptr, t, h->vals2, h->flags, h->vals, h->d_count + 1, (int64_t)N);
+    need = need > t ? need : t;
+    e = ensure_tmp(h, need);
+    if (e != cudaSuccess) return sp_cuda(h, e, "sparse scratch");
+    size_t tb = h->tmp_bytes;
+    e = cub::DeviceRadixSort::SortPairs(h->tmp, tb, h->keys2, h->keys, h->vals2, h->vals, (int64_t)N, 0, h->nbits,
+                                        h->stream);
+    if (e != cudaSuccess) return sp_cuda(h, e, "sparse sort");
+    tb = h->tmp_bytes;
+    // sum the contributions that land on the same index (the vector addition of PAPER.md:222)
+    e = cub::DeviceReduce::ReduceByKey(h->tmp, tb, h->keys, h->keys2, h->vals, h->vals2, h->d_count, CSum(),
+                                       (int64_t)N, h->stream);
+    if (e != cudaSuccess) return sp_cuda(h, e, "sparse reduce");
+    uint64_t runs = 0;
+    e = cudaMemcpyAsync(&runs, h->d_count, sizeof(uint64_t), cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return sp_cuda(h, e, "sparse count");
+    k_sparse_flags<<<(unsigned)((runs + 255) / 256), 256, 0, h->stream>>>(h->keys2, h->vals2, runs, p.invalid,
+                                                                           h->eps * h->eps, h->flags);
+    ++h->launches;
+    tb = h->tmp_bytes;
+    e = cub::DeviceSelect::Flagged(h->tmp, tb, h->keys2, h->flags, h->keys, h->d_count + 1, (int64_t)runs, h->stream);
+    tb = h->tmp_bytes;
+    if (e == cudaSuccess)
+        e = cub::DeviceSelect::Flagged(h->tmp, tb, h->vals2, h->flags, h->vals, h->d_count + 1, (int64_t)runs,
+                                       h->stream);
+    if (e != cudaSuccess) return sp_cuda(h, e, "sparse prune");
+    uint64_t kept = 0;
+    e = cudaMemcpyAsync(&kept, h->d_count + 1, sizeof(uint64_t), cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return sp_cuda(h, e, "sparse count");
+    h->nnz = kept;
+    return SV_OK;
+}
+
+sv_status sp_check(sv_sparse_handle h) {
+    if (!h) return fail_msg(SV_ERR_INVALID_ARG, "null handle");
+    if (h->broken) return fail_msg(SV_ERR_CUDA, "handle is unusable after an earlier CUDA fault");
+    return SV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+sv_status sv_sparse_create(const int32_t *dims, int32_t n, double eps, sv_sparse_handle *out) {
+    if (!out) return fail_msg(SV_ERR_INVALID_ARG, "null out");
+    *out = nullptr;
+    sv_sparse_handle h = new (std::nothrow) sv_sparse_s();
+    if (!h) return fail_msg(SV_ERR_NOMEM, "host allocation");
+    sv_status s = make_register(dims, n, &h->reg, err_slot());
+    if (s != SV_OK) { delete h; return s; }
+    if (h->reg.D > (1ull << 63)) { delete h; return fail_msg(SV_ERR_OVERFLOW, "sparse indices need D <= 2^63 (PAPER.md:489)"); }
+    h->eps = eps > 0 ? eps : 1e-12;
+    int nb = 1;
+    while (nb < 64 && (h->reg.D >> nb) != 0) ++nb;      // bits of D (the invalid key) and below
+    h->nbits = nb;
+    cudaError_t e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMalloc(&h->d_count, 2 * sizeof(uint64_t));
+    if (e == cudaSuccess) e = reserve(h, 1024);
+    if (e != cudaSuccess) { cudaGetLastError(); sv_sparse_destroy(h); return fail_msg(SV_ERR_CUDA, cudaGetErrorString(e)); }
+    s = sv_sparse_reset(h, 0);
+    if (s != SV_OK) { sv_sparse_destroy(h); return s; }
+    *out = h;
+    return SV_OK;
+}
+
+sv_status sv_sparse_destroy(sv_sparse_handle h) {
+    if (!h) return fail_msg(SV_ERR_INVALID_ARG, "null handle");
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    for (void *p : {(void *)h->keys, (void *)h->keys2, (void *)h->vals, (void *)h->vals2, (void *)h->flags,
+                    h->tmp, (void *)h->d_count})
+        if (p) cudaFree(p);
+    if (h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+    return SV_OK;
+}
+
+sv_status sv_sparse_reset(sv_sparse_handle h, uint64_t basis_index) {
+    sv_status s = sp_check(h);
+    if (s != SV_OK) return s;
+    if (basis_index >= h->reg.D) return fail_msg(SV_ERR_INDEX_RANGE, "basis index >= D");
+    k_sparse_set<<<1, 1, 0, h->stream>>>(h->keys, h->vals, basis_index);
+    ++h->launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return sp_cuda(h, e, "sparse reset");
+    h->nnz = 1;
+    return SV_OK;
+}
+
+sv_status sv_sparse_apply_gate(sv_sparse_handle h, int32_t target, const int32_t *ctrl, const int32_t *ctrl_vals,
+                               int32_t nctrl, const double *U) {
+    sv_status s = sp_check(h);
+    if (s != SV_OK) return s;
+    s = validate_gate(h->reg, target, ctrl, ctrl_vals, nctrl, U, err_slot());
+    if (s != SV_OK) return s;
+    GateSpec g;
+    g.target = target;
+    g.d = h->reg.dims[target];
+    for (int i = 0; i < nctrl; ++i) g.ctrl.push_back({ctrl[i], ctrl_vals[i]});
+    g.U.resize((size_t)g.d * g.d);
+    for (int i = 0; i < g.d * g.d; ++i) g.U[i] = make_double2(U[2 * i], U[2 * i + 1]);
+    if (!(unitarity_error(g.U.data(), g.d) <= 1e-12)) return fail_msg(SV_ERR_NOT_UNITARY, "U is not unitary");
+    return sparse_gate(h, g);
+}
+
+sv_status sv_sparse_apply_circuit(sv_sparse_handle h, const sv_gate *gates, int64_t ngates, uint32_t flags) {
+    sv_status s = sp_check(h);
+    if (s != SV_OK) return s;
+    if (ngates < 0 || (ngates && !gates)) return fail_msg(SV_ERR_INVALID_ARG, "bad gate list");
+    std::vector<GateSpec> specs;
+    for (int64_t i = 0; i < ngates; ++i) {            // validate everything first
+        const sv_gate &x = gates[i];
+        s = validate_gate(h->reg, x.target, x.ctrl, x.ctrl_vals, x.nctrl, x.U, err_slot());
+        if (s != SV_OK) return s;
+        GateSpec g;
+        g.target = x.target;
+        g.d = h->reg.dims[x.target];
+        for (int c = 0; c < x.nctrl; ++c) g.ctrl.push_back({x.ctrl[c], x.ctrl_vals[c]});
+        g.U.resize((size_t)g.d * g.d);
+        for (int k = 0; k < g.d * g.d; ++k) g.U[k] = make_double2(x.U[2 * k], x.U[2 * k + 1]);
+        if (!(flags & SV_NO_CHECK) && !(unitarity_error(g.U.data(), g.d) <= 1e-12))
+            return fail_msg(SV_ERR_NOT_UNITARY, "gate " + std::to_string(i) + ": U is not unitary");
+        specs.push_back(g);
+    }
+    for (const GateSpec &g : specs) {
+        s = sparse_gate(h, g);
+        if (s != SV_OK) return s;
+    }
+    return SV_OK;
+}
+
+sv_status sv_sparse_nnz(sv_sparse_handle h, uint64_t *out) {
+    sv_status s = sp_check(h);
+    if (s != SV_OK) return s;
+    if (!out) return fail_msg(SV_ERR_INVALID_ARG, "null out");
+    cudaError_t e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return sp_cuda(h, e, "sparse sync");
+    *out = h->nnz;
+    return SV_OK;
+}
+
+sv_status sv_sparse_entries(sv_sparse_handle h, uint64_t cap, uint64_t *idx, double *amp, uint64_t *n) {
+    sv_status s = sp_check(h);
+    if (s != SV_OK) return s;
+    if (!n || (cap && (!idx || !amp))) return fail_msg(SV_ERR_INVALID_ARG, "null out");
+    const uint64_t k = h->nnz < cap ? h->nnz : cap;
+    cudaError_t e = cudaSuccess;
+    if (k) {
+        e = cudaMemcpyAsync(idx, h->keys, k * sizeof(uint64_t), cudaMemcpyDeviceToHost, h->stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(amp, h->vals, k * sizeof(double2), cudaMemcpyDeviceToHost, h->stream);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return sp_cuda(h, e, "sparse readback");
+    *n = h->nnz;
+    return SV_OK;
+}
+
+sv_status sv_sparse_launches(sv_sparse_handle h, uint64_t *out) {
+    if (!h || !out) return fail_msg(SV_ERR_INVALID_ARG, "null handle/out");
+    *out = h->launches;
+    return SV_OK;
+}
+
+}  // extern "C"

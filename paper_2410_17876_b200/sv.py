@@ -99,13 +99,23 @@ _sig("sv_shard_plan", [_i32p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _i32p,
                        _i32p, _i32p, _i32p])
 _sig("sv_version", [], C.c_char_p)
 _sig("sv_profile_read", [_h, C.c_int32, C.POINTER(sv_profile)])
+_sig("sv_sparse_create", [_i32p, C.c_int32, C.c_double, C.POINTER(_h)])
+_sig("sv_sparse_destroy", [_h])
+_sig("sv_sparse_reset", [_h, C.c_uint64])
+_sig("sv_sparse_apply_gate", [_h, C.c_int32, _i32p, _i32p, C.c_int32, _dp])
+_sig("sv_sparse_apply_circuit", [_h, C.POINTER(sv_gate), C.c_int64, C.c_uint32])
+_sig("sv_sparse_nnz", [_h, C.POINTER(C.c_uint64)])
+_sig("sv_sparse_entries", [_h, C.c_uint64, _u64p, _dp, C.POINTER(C.c_uint64)])
+_sig("sv_sparse_launches", [_h, C.POINTER(C.c_uint64)])
 _sig("sv_block_plan", [_i32p, C.c_int32, C.POINTER(sv_gate), C.c_int64, C.c_int64, C.POINTER(C.c_int64),
                        C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)])
 
 EXPORTS = ["sv_create", "sv_create_ex", "sv_create_sharded", "sv_nccl_unique_id", "sv_destroy",
            "sv_reset", "sv_apply_gate", "sv_apply_circuit", "sv_amplitudes", "sv_set_amplitudes",
            "sv_norm", "sv_sync", "sv_last_error", "sv_get_info", "sv_set_option", "sv_plan_gate",
-           "sv_enumerate_fibres", "sv_fuse_plan", "sv_shard_plan", "sv_version", "sv_profile_read", "sv_block_plan"]
+           "sv_enumerate_fibres", "sv_fuse_plan", "sv_shard_plan", "sv_version", "sv_profile_read", "sv_block_plan",
+           "sv_sparse_create", "sv_sparse_destroy", "sv_sparse_reset", "sv_sparse_apply_gate",
+           "sv_sparse_apply_circuit", "sv_sparse_nnz", "sv_sparse_entries", "sv_sparse_launches"]
 
 
 def _check(rc: int):
@@ -314,6 +324,66 @@ def block_plan(dims, gates, tile_cap: int = 4096):
                               order.ctypes.data_as(p64), pid.ctypes.data_as(p64), tiles.ctypes.data_as(p64),
                               C.byref(npass)))
     return order[:len(gates)], pid[:len(gates)], tiles[:npass.value]
+
+
+class SparseState:
+    """A sparse complex128 state on the GPU (the paper's sparse variant): sorted (index, amplitude)
+    entries; gates touch only the classes holding a stored index."""
+
+    def __init__(self, dims: Sequence[int], eps: float = 1e-12):
+        self.dims = [int(d) for d in dims]
+        d = _i32(self.dims)
+        h = _h()
+        _check(_lib.sv_sparse_create(d.ctypes.data_as(_i32p), d.size, float(eps), C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _check(_lib.sv_sparse_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def reset(self, index: int = 0):
+        _check(_lib.sv_sparse_reset(self._h, int(index)))
+
+    def apply_gate(self, target: int, U, ctrl=(), vals=()):
+        c, v, Uc = _i32(ctrl), _i32(vals), _cplx(U)
+        _check(_lib.sv_sparse_apply_gate(self._h, int(target), _p(c, _i32p), _p(v, _i32p), int(c.size),
+                                         Uc.view(np.float64).ctypes.data_as(_dp)))
+
+    def apply_circuit(self, gates, check: bool = True):
+        ga = gates if isinstance(gates, _GateArray) else _GateArray(gates)
+        _check(_lib.sv_sparse_apply_circuit(self._h, ga.arr, ga.n, 0 if check else SV_NO_CHECK))
+
+    def nnz(self) -> int:
+        out = C.c_uint64()
+        _check(_lib.sv_sparse_nnz(self._h, C.byref(out)))
+        return out.value
+
+    def entries(self):
+        n = self.nnz()
+        idx = np.zeros(max(1, n), dtype=np.uint64)
+        amp = np.zeros(max(1, n), dtype=np.complex128)
+        got = C.c_uint64()
+        _check(_lib.sv_sparse_entries(self._h, n, idx.ctypes.data_as(_u64p), amp.view(np.float64).ctypes.data_as(_dp),
+                                      C.byref(got)))
+        return idx[:n], amp[:n]
+
+    def launches(self) -> int:
+        out = C.c_uint64()
+        _check(_lib.sv_sparse_launches(self._h, C.byref(out)))
+        return out.value
 
 
 def shard_plan(dims, nranks, rank, target, ctrl=(), vals=()):
