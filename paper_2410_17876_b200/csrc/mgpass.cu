@@ -20,7 +20,6 @@
 
 namespace svi {
 
-constexpr int kPassThreads = 512;
 constexpr int kMaxPassGates = 24;
 constexpr int kMaxMembers = 128;
 constexpr int kPoolC = 768;
@@ -84,7 +83,6 @@ __device__ __forceinline__ void bulk_store(void *dst, const void *src, uint32_t 
                  "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read_1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
@@ -288,26 +286,24 @@ __device__ __forceinline__ void apply_gate_tile(const PassParams &p, const PassG
     const uint32_t ncls = nslots / (uint32_t)g.d;
     const double2 *U = Us + g.uoff;       // shared-memory copy: not hoisted into registers
     const bool needml = g.inctl || len < p.LT;
-    if (D == 0) {
+    if constexpr (D == 0) {
         for (uint32_t c = tid; c < ncls; c += NT) {
             uint32_t e0;
             if (class_at(p, g, len, needml, lowoff, c, e0)) apply_class_generic(buf, e0, g.st, g, U);
         }
-        return;
-    }
-    if (D >= 4) {   // the d x d matrix is hoisted into registers: one class per iteration
+    } else if constexpr (D >= 4) {   // one class per iteration (register pressure)
         for (uint32_t c = tid; c < ncls; c += NT) {
             uint32_t e0;
-            if (class_at(p, g, len, needml, lowoff, c, e0)) apply_class<D ? D : 2>(buf, e0, g.st, g, U, g.d);
+            if (class_at(p, g, len, needml, lowoff, c, e0)) apply_class<D>(buf, e0, g.st, g, U, g.d);
         }
-        return;
-    }
-    for (uint32_t c = tid; c < ncls; c += 2 * NT) {
-        uint32_t ea = 0, eb = 0;
-        const bool oka = class_at(p, g, len, needml, lowoff, c, ea);
-        const uint32_t c2 = c + NT;
-        const bool okb = c2 < ncls && class_at(p, g, len, needml, lowoff, c2, eb);
-        apply_class2<D ? D : 2>(buf, ea, oka, eb, okb, g.st, g, U);
+    } else {                         // two classes per iteration (ILP)
+        for (uint32_t c = tid; c < ncls; c += 2 * NT) {
+            uint32_t ea = 0, eb = 0;
+            const bool oka = class_at(p, g, len, needml, lowoff, c, ea);
+            const uint32_t c2 = c + NT;
+            const bool okb = c2 < ncls && class_at(p, g, len, needml, lowoff, c2, eb);
+            apply_class2<D>(buf, ea, oka, eb, okb, g.st, g, U);
+        }
     }
 }
 

@@ -96,6 +96,120 @@ struct CSum {
     }
 };
 
+// ---------------------------------------------------------------------------------------
+// Small-state path: one CTA keeps the whole sparse state in shared memory and applies a run
+// of gates without leaving the kernel (the GHZ circuits of PAPER.md:485-489 hold d entries).
+// Per gate: expand the class contributions into a scratch array, bitonic-sort it by index,
+// sum each run of equal indices, drop |a| < eps, compact with a block scan.  Stops (and
+// reports how many gates it applied) when a gate's contributions would exceed the capacity.
+// ---------------------------------------------------------------------------------------
+constexpr int kSmallThreads = 1024;
+constexpr int kSmallCap = 4096;
+
+__global__ void __launch_bounds__(kSmallThreads) k_sparse_small(const SparseGateP *__restrict__ gates, int ngates,
+                                                                uint64_t *keys_io, double2 *vals_io,
+                                                                unsigned long long *io, double eps2) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double2 *sv = reinterpret_cast<double2 *>(smem);                 // state values
+    double2 *tv = sv + kSmallCap;                                     // contributions
+    uint64_t *sk = reinterpret_cast<uint64_t *>(tv + kSmallCap);      // state keys
+    uint64_t *tk = sk + kSmallCap;                                    // contribution keys
+    int *scan = reinterpret_cast<int *>(tk + kSmallCap);              // kSmallCap + 1
+    __shared__ int s_n;
+    const int tid = threadIdx.x;
+    if (tid == 0) s_n = (int)io[0];
+    __syncthreads();
+    int n = s_n;
+    for (int i = tid; i < n; i += kSmallThreads) { sk[i] = keys_io[i]; sv[i] = vals_io[i]; }
+    __syncthreads();
+    int done = 0;
+    for (; done < ngates; ++done) {
+        const SparseGateP &g = gates[done];
+        const int m = n * g.fan;
+        if (m > kSmallCap) break;
+        int P = 1;
+        while (P < m) P <<= 1;
+        // expand (same rule as k_sparse_expand)
+        for (int s = tid; s < P; s += kSmallThreads) { tk[s] = g.invalid; tv[s] = make_double2(0.0, 0.0); }
+        __syncthreads();
+        for (int e = tid; e < n; e += kSmallThreads) {
+            const uint64_t i = sk[e];
+            const double2 a = sv[e];
+            uint64_t *ok = tk + e * g.fan;
+            double2 *ov = tv + e * g.fan;
+            bool fire = true;
+            for (int c = 0; c < g.nctrl; ++c) {
+                uint64_t r, r2;
+                const uint64_t q = fastdiv64(i, g.cb[c], g.mcb[c], r);
+                fastdiv64(q, g.cd[c], g.mcd[c], r2);
+                fire = fire && (r2 == g.cv[c]);
+            }
+            if (!fire) { ok[0] = i; ov[0] = a; continue; }
+            uint64_t r, v;
+            const uint64_t q = fastdiv64(i, g.bt, g.mbt, r);
+            fastdiv64(q, g.dt, g.mdt, v);
+            const uint64_t base = i - v * g.bt;
+            for (int s = 0; s < g.nrow[v]; ++s) {
+                ok[s] = base + (uint64_t)g.rows[v][s] * g.bt;
+                ov[s] = cmul(g.coef[v][s], a);
+            }
+        }
+        __syncthreads();
+        // bitonic sort of the P slots by index (unused slots carry the largest key)
+        for (int k = 2; k <= P; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = tid; i < P; i += kSmallThreads) {
+                    const int ixj = i ^ j;
+                    if (ixj > i) {
+                        const bool up = (i & k) == 0;
+                        const uint64_t a = tk[i], b = tk[ixj];
+                        if ((a > b) == up) {
+                            tk[i] = b; tk[ixj] = a;
+                            const double2 t = tv[i]; tv[i] = tv[ixj]; tv[ixj] = t;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        // heads of runs of equal indices: sum the run, keep it if |sum| >= eps
+        for (int i = tid; i < P; i += kSmallThreads) {
+            int keep = 0;
+            if (tk[i] != g.invalid && (i == 0 || tk[i - 1] != tk[i])) {
+                double2 s = tv[i];
+                for (int j = i + 1; j < P && tk[j] == tk[i]; ++j) { s.x += tv[j].x; s.y += tv[j].y; }
+                tv[i] = s;
+                keep = (s.x * s.x + s.y * s.y >= eps2);
+            }
+            scan[i] = keep;
+        }
+        __syncthreads();
+        // exclusive scan of the keep flags (Hillis-Steele over P <= kSmallCap entries)
+        for (int off = 1; off < P; off <<= 1) {
+            int add[kSmallCap / kSmallThreads];
+            for (int u = 0, i = tid; i < P; i += kSmallThreads, ++u) add[u] = i >= off ? scan[i - off] : 0;
+            __syncthreads();
+            for (int u = 0, i = tid; i < P; i += kSmallThreads, ++u) scan[i] += add[u];
+            __syncthreads();
+        }
+        // scan now holds inclusive sums; compact the kept heads into the state arrays
+        for (int i = tid; i < P; i += kSmallThreads) {
+            const int incl = scan[i];
+            const int excl = i ? scan[i - 1] : 0;
+            if (incl != excl) { sk[excl] = tk[i]; sv[excl] = tv[i]; }
+        }
+        __syncthreads();
+        n = scan[P - 1];
+        __syncthreads();
+    }
+    for (int i = tid; i < n; i += kSmallThreads) { keys_io[i] = sk[i]; vals_io[i] = sv[i]; }
+    if (tid == 0) { io[0] = (unsigned long long)n; io[1] = (unsigned long long)done; }
+}
+
+size_t small_smem() {
+    return (size_t)kSmallCap * (2 * sizeof(double2) + 2 * sizeof(uint64_t)) + (size_t)(kSmallCap + 1) * sizeof(int);
+}
+
 }  // namespace
 }  // namespace svi
 
@@ -113,6 +227,8 @@ struct sv_sparse_s {
     size_t tmp_bytes = 0;
     uint64_t *d_count = nullptr;
     int nbits = 64;
+    SparseGateP *d_gp = nullptr;                     // gate table of the small-state kernel
+    size_t gp_cap = 0;
     uint64_t launches = 0;
     bool broken = false;
 };
@@ -169,9 +285,7 @@ cudaError_t ensure_tmp(sv_sparse_handle h, size_t bytes) {
     return e;
 }
 
-sv_status sparse_gate(sv_sparse_handle h, const GateSpec &g) {
-    const Register &reg = h->reg;
-    SparseGateP p;
+sv_status make_sparse_params(const Register &reg, const GateSpec &g, SparseGateP &p) {
     std::memset(&p, 0, sizeof(p));
     const int d = g.d;
     p.bt = reg.b[g.target];
@@ -203,7 +317,14 @@ sv_status sparse_gate(sv_sparse_handle h, const GateSpec &g) {
         fan = nr > fan ? nr : fan;
     }
     p.fan = fan;
-    const uint64_t n = h->nnz, N = n * (uint64_t)fan;
+    return SV_OK;
+}
+
+sv_status sparse_gate(sv_sparse_handle h, const GateSpec &g) {
+    SparseGateP p;
+    sv_status s0 = make_sparse_params(h->reg, g, p);
+    if (s0 != SV_OK) return s0;
+    const uint64_t n = h->nnz, N = n * (uint64_t)p.fan;
     if (n == 0) return SV_OK;
     cudaError_t e = reserve(h, N);
     if (e != cudaSuccess) return sp_cuda(h, e, "sparse reserve");
@@ -252,6 +373,58 @@ sv_status sparse_gate(sv_sparse_handle h, const GateSpec &g) {
     return SV_OK;
 }
 
+// Apply a gate list: runs of gates go through the one-CTA small-state kernel while the
+// state's contributions fit its shared-memory capacity; a gate that does not fit goes
+// through the general (expand / radix sort / reduce-by-key / select) path.
+sv_status sparse_run(sv_sparse_handle h, const std::vector<GateSpec> &specs) {
+    std::vector<SparseGateP> ps(specs.size());
+    for (size_t i = 0; i < specs.size(); ++i) {
+        sv_status s = make_sparse_params(h->reg, specs[i], ps[i]);
+        if (s != SV_OK) return s;
+    }
+    if (ps.size() > h->gp_cap) {
+        if (h->d_gp) cudaFree(h->d_gp);
+        h->d_gp = nullptr;
+        h->gp_cap = 0;
+        cudaError_t e = cudaMalloc(&h->d_gp, ps.size() * sizeof(SparseGateP));
+        if (e != cudaSuccess) return sp_cuda(h, e, "sparse gate table");
+        h->gp_cap = ps.size();
+    }
+    if (!ps.empty()) {
+        cudaError_t e = cudaMemcpyAsync(h->d_gp, ps.data(), ps.size() * sizeof(SparseGateP), cudaMemcpyHostToDevice,
+                                        h->stream);
+        if (e != cudaSuccess) return sp_cuda(h, e, "sparse gate table");
+    }
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(k_sparse_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)small_smem());
+        if (e != cudaSuccess) return sp_cuda(h, e, "sparse small attribute");
+        configured = true;
+    }
+    size_t i = 0;
+    while (i < ps.size()) {
+        if (h->nnz > 0 && h->nnz * (uint64_t)ps[i].fan <= (uint64_t)kSmallCap) {
+            unsigned long long io[2] = {(unsigned long long)h->nnz, 0ull};
+            cudaError_t e = cudaMemcpyAsync(h->d_count, io, sizeof(io), cudaMemcpyHostToDevice, h->stream);
+            if (e != cudaSuccess) return sp_cuda(h, e, "sparse small setup");
+            k_sparse_small<<<1, kSmallThreads, small_smem(), h->stream>>>(h->d_gp + i, (int)(ps.size() - i), h->keys,
+                                                                          h->vals, (unsigned long long *)h->d_count,
+                                                                          h->eps * h->eps);
+            ++h->launches;
+            e = cudaMemcpyAsync(io, h->d_count, sizeof(io), cudaMemcpyDeviceToHost, h->stream);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+            if (e != cudaSuccess) return sp_cuda(h, e, "sparse small path");
+            h->nnz = io[0];
+            i += (size_t)io[1];
+            if (i >= ps.size()) break;
+        }
+        sv_status s = sparse_gate(h, specs[i]);         // the general path for this gate
+        if (s != SV_OK) return s;
+        ++i;
+    }
+    return SV_OK;
+}
+
 sv_status sp_check(sv_sparse_handle h) {
     if (!h) return fail_msg(SV_ERR_INVALID_ARG, "null handle");
     if (h->broken) return fail_msg(SV_ERR_CUDA, "handle is unusable after an earlier CUDA fault");
@@ -276,7 +449,7 @@ sv_status sv_sparse_create(const int32_t *dims, int32_t n, double eps, sv_sparse
     h->nbits = nb;
     cudaError_t e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMalloc(&h->d_count, 2 * sizeof(uint64_t));
-    if (e == cudaSuccess) e = reserve(h, 1024);
+    if (e == cudaSuccess) e = reserve(h, kSmallCap);      // the small-state kernel writes back up to kSmallCap
     if (e != cudaSuccess) { cudaGetLastError(); sv_sparse_destroy(h); return fail_msg(SV_ERR_CUDA, cudaGetErrorString(e)); }
     s = sv_sparse_reset(h, 0);
     if (s != SV_OK) { sv_sparse_destroy(h); return s; }
@@ -288,7 +461,7 @@ sv_status sv_sparse_destroy(sv_sparse_handle h) {
     if (!h) return fail_msg(SV_ERR_INVALID_ARG, "null handle");
     if (h->stream) cudaStreamSynchronize(h->stream);
     for (void *p : {(void *)h->keys, (void *)h->keys2, (void *)h->vals, (void *)h->vals2, (void *)h->flags,
-                    h->tmp, (void *)h->d_count})
+                    h->tmp, (void *)h->d_count, (void *)h->d_gp})
         if (p) cudaFree(p);
     if (h->stream) cudaStreamDestroy(h->stream);
     delete h;
@@ -320,7 +493,7 @@ sv_status sv_sparse_apply_gate(sv_sparse_handle h, int32_t target, const int32_t
     g.U.resize((size_t)g.d * g.d);
     for (int i = 0; i < g.d * g.d; ++i) g.U[i] = make_double2(U[2 * i], U[2 * i + 1]);
     if (!(unitarity_error(g.U.data(), g.d) <= 1e-12)) return fail_msg(SV_ERR_NOT_UNITARY, "U is not unitary");
-    return sparse_gate(h, g);
+    return sparse_run(h, std::vector<GateSpec>{g});
 }
 
 sv_status sv_sparse_apply_circuit(sv_sparse_handle h, const sv_gate *gates, int64_t ngates, uint32_t flags) {
@@ -342,11 +515,7 @@ sv_status sv_sparse_apply_circuit(sv_sparse_handle h, const sv_gate *gates, int6
             return fail_msg(SV_ERR_NOT_UNITARY, "gate " + std::to_string(i) + ": U is not unitary");
         specs.push_back(g);
     }
-    for (const GateSpec &g : specs) {
-        s = sparse_gate(h, g);
-        if (s != SV_OK) return s;
-    }
-    return SV_OK;
+    return sparse_run(h, specs);
 }
 
 sv_status sv_sparse_nnz(sv_sparse_handle h, uint64_t *out) {
