@@ -103,36 +103,37 @@ struct CSum {
 // sum each run of equal indices, drop |a| < eps, compact with a block scan.  Stops (and
 // reports how many gates it applied) when a gate's contributions would exceed the capacity.
 // ---------------------------------------------------------------------------------------
-constexpr int kSmallThreads = 1024;
-constexpr int kSmallCap = 4096;
+constexpr int kSmallCap = 4096;   // entries of the 1024-thread variant
+constexpr int kTinyCap = 256;     // entries of the one-warp variant (GHZ-sized states)
 
-__global__ void __launch_bounds__(kSmallThreads) k_sparse_small(const SparseGateP *__restrict__ gates, int ngates,
+template <int NT, int CAP>
+__global__ void __launch_bounds__(NT) k_sparse_small(const SparseGateP *__restrict__ gates, int ngates,
                                                                 uint64_t *keys_io, double2 *vals_io,
                                                                 unsigned long long *io, double eps2) {
     extern __shared__ __align__(16) unsigned char smem[];
     double2 *sv = reinterpret_cast<double2 *>(smem);                 // state values
-    double2 *tv = sv + kSmallCap;                                     // contributions
-    uint64_t *sk = reinterpret_cast<uint64_t *>(tv + kSmallCap);      // state keys
-    uint64_t *tk = sk + kSmallCap;                                    // contribution keys
-    int *scan = reinterpret_cast<int *>(tk + kSmallCap);              // kSmallCap + 1
+    double2 *tv = sv + CAP;                                     // contributions
+    uint64_t *sk = reinterpret_cast<uint64_t *>(tv + CAP);      // state keys
+    uint64_t *tk = sk + CAP;                                    // contribution keys
+    int *scan = reinterpret_cast<int *>(tk + CAP);              // CAP + 1
     __shared__ int s_n;
     const int tid = threadIdx.x;
     if (tid == 0) s_n = (int)io[0];
     __syncthreads();
     int n = s_n;
-    for (int i = tid; i < n; i += kSmallThreads) { sk[i] = keys_io[i]; sv[i] = vals_io[i]; }
+    for (int i = tid; i < n; i += NT) { sk[i] = keys_io[i]; sv[i] = vals_io[i]; }
     __syncthreads();
     int done = 0;
     for (; done < ngates; ++done) {
         const SparseGateP &g = gates[done];
         const int m = n * g.fan;
-        if (m > kSmallCap) break;
+        if (m > CAP) break;
         int P = 1;
         while (P < m) P <<= 1;
         // expand (same rule as k_sparse_expand)
-        for (int s = tid; s < P; s += kSmallThreads) { tk[s] = g.invalid; tv[s] = make_double2(0.0, 0.0); }
+        for (int s = tid; s < P; s += NT) { tk[s] = g.invalid; tv[s] = make_double2(0.0, 0.0); }
         __syncthreads();
-        for (int e = tid; e < n; e += kSmallThreads) {
+        for (int e = tid; e < n; e += NT) {
             const uint64_t i = sk[e];
             const double2 a = sv[e];
             uint64_t *ok = tk + e * g.fan;
@@ -158,7 +159,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_sparse_small(const SparseGate
         // bitonic sort of the P slots by index (unused slots carry the largest key)
         for (int k = 2; k <= P; k <<= 1) {
             for (int j = k >> 1; j > 0; j >>= 1) {
-                for (int i = tid; i < P; i += kSmallThreads) {
+                for (int i = tid; i < P; i += NT) {
                     const int ixj = i ^ j;
                     if (ixj > i) {
                         const bool up = (i & k) == 0;
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_sparse_small(const SparseGate
             }
         }
         // heads of runs of equal indices: sum the run, keep it if |sum| >= eps
-        for (int i = tid; i < P; i += kSmallThreads) {
+        for (int i = tid; i < P; i += NT) {
             int keep = 0;
             if (tk[i] != g.invalid && (i == 0 || tk[i - 1] != tk[i])) {
                 double2 s = tv[i];
@@ -184,16 +185,16 @@ __global__ void __launch_bounds__(kSmallThreads) k_sparse_small(const SparseGate
             scan[i] = keep;
         }
         __syncthreads();
-        // exclusive scan of the keep flags (Hillis-Steele over P <= kSmallCap entries)
+        // exclusive scan of the keep flags (Hillis-Steele over P <= CAP entries)
         for (int off = 1; off < P; off <<= 1) {
-            int add[kSmallCap / kSmallThreads];
-            for (int u = 0, i = tid; i < P; i += kSmallThreads, ++u) add[u] = i >= off ? scan[i - off] : 0;
+            int add[CAP / NT];
+            for (int u = 0, i = tid; i < P; i += NT, ++u) add[u] = i >= off ? scan[i - off] : 0;
             __syncthreads();
-            for (int u = 0, i = tid; i < P; i += kSmallThreads, ++u) scan[i] += add[u];
+            for (int u = 0, i = tid; i < P; i += NT, ++u) scan[i] += add[u];
             __syncthreads();
         }
         // scan now holds inclusive sums; compact the kept heads into the state arrays
-        for (int i = tid; i < P; i += kSmallThreads) {
+        for (int i = tid; i < P; i += NT) {
             const int incl = scan[i];
             const int excl = i ? scan[i - 1] : 0;
             if (incl != excl) { sk[excl] = tk[i]; sv[excl] = tv[i]; }
@@ -202,12 +203,13 @@ __global__ void __launch_bounds__(kSmallThreads) k_sparse_small(const SparseGate
         n = scan[P - 1];
         __syncthreads();
     }
-    for (int i = tid; i < n; i += kSmallThreads) { keys_io[i] = sk[i]; vals_io[i] = sv[i]; }
+    for (int i = tid; i < n; i += NT) { keys_io[i] = sk[i]; vals_io[i] = sv[i]; }
     if (tid == 0) { io[0] = (unsigned long long)n; io[1] = (unsigned long long)done; }
 }
 
+template <int CAP>
 size_t small_smem() {
-    return (size_t)kSmallCap * (2 * sizeof(double2) + 2 * sizeof(uint64_t)) + (size_t)(kSmallCap + 1) * sizeof(int);
+    return (size_t)CAP * (2 * sizeof(double2) + 2 * sizeof(uint64_t)) + (size_t)(CAP + 1) * sizeof(int);
 }
 
 }  // namespace
@@ -229,6 +231,8 @@ struct sv_sparse_s {
     int nbits = 64;
     SparseGateP *d_gp = nullptr;                     // gate table of the small-state kernel
     size_t gp_cap = 0;
+    std::vector<SparseGateP> gp_host;                // what d_gp holds
+    unsigned long long *io_host = nullptr;           // pinned: small-kernel in/out counters
     uint64_t launches = 0;
     bool broken = false;
 };
@@ -390,37 +394,54 @@ sv_status sparse_run(sv_sparse_handle h, const std::vector<GateSpec> &specs) {
         if (e != cudaSuccess) return sp_cuda(h, e, "sparse gate table");
         h->gp_cap = ps.size();
     }
-    if (!ps.empty()) {
+    // upload the gate table unless the same circuit was submitted last time
+    const bool same = ps.size() == h->gp_host.size() &&
+                      (ps.empty() || std::memcmp(ps.data(), h->gp_host.data(), ps.size() * sizeof(SparseGateP)) == 0);
+    if (!ps.empty() && !same) {
         cudaError_t e = cudaMemcpyAsync(h->d_gp, ps.data(), ps.size() * sizeof(SparseGateP), cudaMemcpyHostToDevice,
                                         h->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
         if (e != cudaSuccess) return sp_cuda(h, e, "sparse gate table");
+        h->gp_host = ps;
     }
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(k_sparse_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)small_smem());
+        cudaError_t e = cudaFuncSetAttribute(k_sparse_small<1024, kSmallCap>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)small_smem<kSmallCap>());
         if (e != cudaSuccess) return sp_cuda(h, e, "sparse small attribute");
         configured = true;
     }
     size_t i = 0;
     while (i < ps.size()) {
-        if (h->nnz > 0 && h->nnz * (uint64_t)ps[i].fan <= (uint64_t)kSmallCap) {
-            unsigned long long io[2] = {(unsigned long long)h->nnz, 0ull};
-            cudaError_t e = cudaMemcpyAsync(h->d_count, io, sizeof(io), cudaMemcpyHostToDevice, h->stream);
+        const uint64_t m = h->nnz * (uint64_t)ps[i].fan;
+        size_t done = 0;
+        if (h->nnz > 0 && m <= (uint64_t)kSmallCap) {
+            h->io_host[0] = (unsigned long long)h->nnz;
+            h->io_host[1] = 0ull;
+            cudaError_t e = cudaMemcpyAsync(h->d_count, h->io_host, 2 * sizeof(unsigned long long),
+                                            cudaMemcpyHostToDevice, h->stream);
             if (e != cudaSuccess) return sp_cuda(h, e, "sparse small setup");
-            k_sparse_small<<<1, kSmallThreads, small_smem(), h->stream>>>(h->d_gp + i, (int)(ps.size() - i), h->keys,
-                                                                          h->vals, (unsigned long long *)h->d_count,
-                                                                          h->eps * h->eps);
+            const int left = (int)(ps.size() - i);
+            unsigned long long *io = (unsigned long long *)h->d_count;
+            if (m <= (uint64_t)kTinyCap)   // one warp: GHZ-sized states
+                k_sparse_small<32, kTinyCap><<<1, 32, small_smem<kTinyCap>(), h->stream>>>(
+                    h->d_gp + i, left, h->keys, h->vals, io, h->eps * h->eps);
+            else
+                k_sparse_small<1024, kSmallCap><<<1, 1024, small_smem<kSmallCap>(), h->stream>>>(
+                    h->d_gp + i, left, h->keys, h->vals, io, h->eps * h->eps);
             ++h->launches;
-            e = cudaMemcpyAsync(io, h->d_count, sizeof(io), cudaMemcpyDeviceToHost, h->stream);
+            e = cudaMemcpyAsync(h->io_host, h->d_count, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->stream);
             if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
             if (e != cudaSuccess) return sp_cuda(h, e, "sparse small path");
-            h->nnz = io[0];
-            i += (size_t)io[1];
-            if (i >= ps.size()) break;
+            h->nnz = h->io_host[0];
+            done = (size_t)h->io_host[1];
+            i += done;
         }
-        sv_status s = sparse_gate(h, specs[i]);         // the general path for this gate
-        if (s != SV_OK) return s;
-        ++i;
+        if (done == 0 && i < ps.size()) {                  // the general path for this gate
+            sv_status s = sparse_gate(h, specs[i]);
+            if (s != SV_OK) return s;
+            ++i;
+        }
     }
     return SV_OK;
 }
@@ -449,6 +470,7 @@ sv_status sv_sparse_create(const int32_t *dims, int32_t n, double eps, sv_sparse
     h->nbits = nb;
     cudaError_t e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMalloc(&h->d_count, 2 * sizeof(uint64_t));
+    if (e == cudaSuccess) e = cudaMallocHost(&h->io_host, 2 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = reserve(h, kSmallCap);      // the small-state kernel writes back up to kSmallCap
     if (e != cudaSuccess) { cudaGetLastError(); sv_sparse_destroy(h); return fail_msg(SV_ERR_CUDA, cudaGetErrorString(e)); }
     s = sv_sparse_reset(h, 0);
@@ -463,6 +485,7 @@ sv_status sv_sparse_destroy(sv_sparse_handle h) {
     for (void *p : {(void *)h->keys, (void *)h->keys2, (void *)h->vals, (void *)h->vals2, (void *)h->flags,
                     h->tmp, (void *)h->d_count, (void *)h->d_gp})
         if (p) cudaFree(p);
+    if (h->io_host) cudaFreeHost(h->io_host);
     if (h->stream) cudaStreamDestroy(h->stream);
     delete h;
     return SV_OK;
