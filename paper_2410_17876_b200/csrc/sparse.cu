@@ -26,7 +26,7 @@ namespace svi {
 std::string *err_slot();
 sv_status fail_msg(sv_status s, const std::string &msg);
 
-struct SparseGateP {
+struct alignas(16) SparseGateP {   // 16-B multiple: copied with 16-B cp.async chunks
     uint64_t bt, mbt;            // target stride (+ magic)
     uint64_t dt, mdt;            // target dim (+ magic)
     int32_t nctrl;
@@ -111,21 +111,35 @@ __global__ void __launch_bounds__(NT) k_sparse_small(const SparseGateP *__restri
                                                                 uint64_t *keys_io, double2 *vals_io,
                                                                 unsigned long long *io, double eps2) {
     extern __shared__ __align__(16) unsigned char smem[];
-    double2 *sv = reinterpret_cast<double2 *>(smem);                 // state values
+    SparseGateP *gbuf = reinterpret_cast<SparseGateP *>(smem);      // double-buffered gate records
+    double2 *sv = reinterpret_cast<double2 *>(gbuf + 2);             // state values
     double2 *tv = sv + CAP;                                     // contributions
     uint64_t *sk = reinterpret_cast<uint64_t *>(tv + CAP);      // state keys
     uint64_t *tk = sk + CAP;                                    // contribution keys
     int *scan = reinterpret_cast<int *>(tk + CAP);              // CAP + 1
     __shared__ int s_n;
     const int tid = threadIdx.x;
+    // asynchronous copy of a gate record (cp.async, 16 B per thread-instruction) into gbuf[slot]
+    auto prefetch = [&](int k, int slot) {
+        if (k >= ngates) return;
+        const char *src = reinterpret_cast<const char *>(gates + k);
+        char *dst = reinterpret_cast<char *>(gbuf + slot);
+        for (int o = tid * 16; o < (int)sizeof(SparseGateP); o += NT * 16)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst + o)),
+                         "l"(src + o) : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    prefetch(0, 0);
     if (tid == 0) s_n = (int)io[0];
     __syncthreads();
     int n = s_n;
     for (int i = tid; i < n; i += NT) { sk[i] = keys_io[i]; sv[i] = vals_io[i]; }
-    __syncthreads();
     int done = 0;
     for (; done < ngates; ++done) {
-        const SparseGateP &g = gates[done];
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();                                       // gate record `done` is in smem
+        prefetch(done + 1, (done + 1) & 1);                    // overlaps with this gate
+        const SparseGateP &g = gbuf[done & 1];
         const int m = n * g.fan;
         if (m > CAP) break;
         int P = 1;
@@ -203,13 +217,15 @@ __global__ void __launch_bounds__(NT) k_sparse_small(const SparseGateP *__restri
         n = scan[P - 1];
         __syncthreads();
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");       // no copy outlives the CTA
     for (int i = tid; i < n; i += NT) { keys_io[i] = sk[i]; vals_io[i] = sv[i]; }
     if (tid == 0) { io[0] = (unsigned long long)n; io[1] = (unsigned long long)done; }
 }
 
 template <int CAP>
 size_t small_smem() {
-    return (size_t)CAP * (2 * sizeof(double2) + 2 * sizeof(uint64_t)) + (size_t)(CAP + 1) * sizeof(int);
+    return 2 * sizeof(SparseGateP) + (size_t)CAP * (2 * sizeof(double2) + 2 * sizeof(uint64_t)) +
+           (size_t)(CAP + 1) * sizeof(int);
 }
 
 }  // namespace
