@@ -105,41 +105,57 @@ struct CSum {
 // ---------------------------------------------------------------------------------------
 constexpr int kSmallCap = 4096;   // entries of the 1024-thread variant
 constexpr int kTinyCap = 256;     // entries of the one-warp variant (GHZ-sized states)
+constexpr int kSmallD = 8;        // small-path gate records: d <= 8, at most 8 controls
+
+// compact gate record of the small-state kernel (1.7 KB instead of 6.5 KB)
+struct alignas(16) SmallGateP {
+    uint64_t bt, mbt, dt, mdt;
+    uint64_t cb[kSmallD], mcb[kSmallD], cd[kSmallD], mcd[kSmallD], cv[kSmallD];
+    uint64_t invalid;
+    int32_t nctrl, fan, ok, pad;
+    int32_t nrow[kSmallD];
+    int32_t rows[kSmallD][kSmallD];
+    double2 coef[kSmallD][kSmallD];
+};
 
 template <int NT, int CAP>
-__global__ void __launch_bounds__(NT) k_sparse_small(const SparseGateP *__restrict__ gates, int ngates,
+__global__ void __launch_bounds__(NT) k_sparse_small(const SmallGateP *__restrict__ gates, int ngates,
                                                                 uint64_t *keys_io, double2 *vals_io,
                                                                 unsigned long long *io, double eps2) {
     extern __shared__ __align__(16) unsigned char smem[];
-    SparseGateP *gbuf = reinterpret_cast<SparseGateP *>(smem);      // double-buffered gate records
-    double2 *sv = reinterpret_cast<double2 *>(gbuf + 2);             // state values
+    SmallGateP *gbuf = reinterpret_cast<SmallGateP *>(smem);        // 3-slot ring of gate records
+    double2 *sv = reinterpret_cast<double2 *>(gbuf + 3);             // state values
     double2 *tv = sv + CAP;                                     // contributions
     uint64_t *sk = reinterpret_cast<uint64_t *>(tv + CAP);      // state keys
     uint64_t *tk = sk + CAP;                                    // contribution keys
     int *scan = reinterpret_cast<int *>(tk + CAP);              // CAP + 1
     __shared__ int s_n;
     const int tid = threadIdx.x;
-    // asynchronous copy of a gate record (cp.async, 16 B per thread-instruction) into gbuf[slot]
+    // asynchronous copy of gate record k (cp.async, 16 B per thread-instruction) into gbuf[slot];
+    // always commits a group (possibly empty) so the wait counts stay aligned
     auto prefetch = [&](int k, int slot) {
-        if (k >= ngates) return;
-        const char *src = reinterpret_cast<const char *>(gates + k);
-        char *dst = reinterpret_cast<char *>(gbuf + slot);
-        for (int o = tid * 16; o < (int)sizeof(SparseGateP); o += NT * 16)
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst + o)),
-                         "l"(src + o) : "memory");
+        if (k < ngates) {
+            const char *src = reinterpret_cast<const char *>(gates + k);
+            char *dst = reinterpret_cast<char *>(gbuf + slot);
+            for (int o = tid * 16; o < (int)sizeof(SmallGateP); o += NT * 16)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(
+                                 (uint32_t)__cvta_generic_to_shared(dst + o)), "l"(src + o) : "memory");
+        }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     prefetch(0, 0);
+    prefetch(1, 1);
     if (tid == 0) s_n = (int)io[0];
     __syncthreads();
     int n = s_n;
     for (int i = tid; i < n; i += NT) { sk[i] = keys_io[i]; sv[i] = vals_io[i]; }
     int done = 0;
     for (; done < ngates; ++done) {
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-        __syncthreads();                                       // gate record `done` is in smem
-        prefetch(done + 1, (done + 1) & 1);                    // overlaps with this gate
-        const SparseGateP &g = gbuf[done & 1];
+        asm volatile("cp.async.wait_group 1;" ::: "memory");  // record `done` landed (done+1 may be in flight)
+        __syncthreads();
+        prefetch(done + 2, (done + 2) % 3);                    // two gates ahead
+        const SmallGateP &g = gbuf[done % 3];
+        if (!g.ok) break;                                      // needs the general path
         const int m = n * g.fan;
         if (m > CAP) break;
         int P = 1;
@@ -224,8 +240,24 @@ __global__ void __launch_bounds__(NT) k_sparse_small(const SparseGateP *__restri
 
 template <int CAP>
 size_t small_smem() {
-    return 2 * sizeof(SparseGateP) + (size_t)CAP * (2 * sizeof(double2) + 2 * sizeof(uint64_t)) +
+    return 3 * sizeof(SmallGateP) + (size_t)CAP * (2 * sizeof(double2) + 2 * sizeof(uint64_t)) +
            (size_t)(CAP + 1) * sizeof(int);
+}
+
+// the compact record of a gate, ok = 0 when it does not fit (d > 8 or more than 8 controls)
+void to_small(const SparseGateP &p, SmallGateP &s) {
+    std::memset(&s, 0, sizeof(s));
+    s.ok = (p.dt <= (uint64_t)kSmallD && p.nctrl <= kSmallD) ? 1 : 0;
+    if (!s.ok) return;
+    s.bt = p.bt; s.mbt = p.mbt; s.dt = p.dt; s.mdt = p.mdt;
+    s.invalid = p.invalid; s.nctrl = p.nctrl; s.fan = p.fan;
+    for (int c = 0; c < p.nctrl; ++c) {
+        s.cb[c] = p.cb[c]; s.mcb[c] = p.mcb[c]; s.cd[c] = p.cd[c]; s.mcd[c] = p.mcd[c]; s.cv[c] = p.cv[c];
+    }
+    for (int v = 0; v < (int)p.dt; ++v) {
+        s.nrow[v] = p.nrow[v];
+        for (int r = 0; r < p.nrow[v]; ++r) { s.rows[v][r] = p.rows[v][r]; s.coef[v][r] = p.coef[v][r]; }
+    }
 }
 
 }  // namespace
@@ -245,9 +277,9 @@ struct sv_sparse_s {
     size_t tmp_bytes = 0;
     uint64_t *d_count = nullptr;
     int nbits = 64;
-    SparseGateP *d_gp = nullptr;                     // gate table of the small-state kernel
+    SmallGateP *d_gp = nullptr;                      // gate table of the small-state kernel
     size_t gp_cap = 0;
-    std::vector<SparseGateP> gp_host;                // what d_gp holds
+    std::vector<SmallGateP> gp_host;                 // what d_gp holds
     unsigned long long *io_host = nullptr;           // pinned: small-kernel in/out counters
     uint64_t launches = 0;
     bool broken = false;
@@ -402,23 +434,26 @@ sv_status sparse_run(sv_sparse_handle h, const std::vector<GateSpec> &specs) {
         sv_status s = make_sparse_params(h->reg, specs[i], ps[i]);
         if (s != SV_OK) return s;
     }
-    if (ps.size() > h->gp_cap) {
+    std::vector<SmallGateP> sm(ps.size());
+    for (size_t i = 0; i < ps.size(); ++i) to_small(ps[i], sm[i]);
+    if (sm.size() > h->gp_cap) {
         if (h->d_gp) cudaFree(h->d_gp);
         h->d_gp = nullptr;
         h->gp_cap = 0;
-        cudaError_t e = cudaMalloc(&h->d_gp, ps.size() * sizeof(SparseGateP));
+        h->gp_host.clear();
+        cudaError_t e = cudaMalloc(&h->d_gp, sm.size() * sizeof(SmallGateP));
         if (e != cudaSuccess) return sp_cuda(h, e, "sparse gate table");
-        h->gp_cap = ps.size();
+        h->gp_cap = sm.size();
     }
     // upload the gate table unless the same circuit was submitted last time
-    const bool same = ps.size() == h->gp_host.size() &&
-                      (ps.empty() || std::memcmp(ps.data(), h->gp_host.data(), ps.size() * sizeof(SparseGateP)) == 0);
-    if (!ps.empty() && !same) {
-        cudaError_t e = cudaMemcpyAsync(h->d_gp, ps.data(), ps.size() * sizeof(SparseGateP), cudaMemcpyHostToDevice,
+    const bool same = sm.size() == h->gp_host.size() &&
+                      (sm.empty() || std::memcmp(sm.data(), h->gp_host.data(), sm.size() * sizeof(SmallGateP)) == 0);
+    if (!sm.empty() && !same) {
+        cudaError_t e = cudaMemcpyAsync(h->d_gp, sm.data(), sm.size() * sizeof(SmallGateP), cudaMemcpyHostToDevice,
                                         h->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
         if (e != cudaSuccess) return sp_cuda(h, e, "sparse gate table");
-        h->gp_host = ps;
+        h->gp_host = sm;
     }
     static bool configured = false;
     if (!configured) {
@@ -431,7 +466,7 @@ sv_status sparse_run(sv_sparse_handle h, const std::vector<GateSpec> &specs) {
     while (i < ps.size()) {
         const uint64_t m = h->nnz * (uint64_t)ps[i].fan;
         size_t done = 0;
-        if (h->nnz > 0 && m <= (uint64_t)kSmallCap) {
+        if (h->nnz > 0 && m <= (uint64_t)kSmallCap && sm[i].ok) {
             h->io_host[0] = (unsigned long long)h->nnz;
             h->io_host[1] = 0ull;
             cudaError_t e = cudaMemcpyAsync(h->d_count, h->io_host, 2 * sizeof(unsigned long long),
