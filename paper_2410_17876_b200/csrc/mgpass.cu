@@ -5,11 +5,14 @@
 // shared memory as [member][run] where a "member" is one combination of the H digits (global
 // offset sum_h j_h b_h) and the run is a contiguous stretch of the low space (stride < b_{min H}).
 // Loading / storing a tile = one cp.async.bulk per member (TMA bulk copies onto an mbarrier,
-// 3-stage ring, persistent grid, as in tiled_impl.cuh).  Between load and store the CTA applies
-// the pass's gates one after another in shared memory: each gate visits its equivalence classes
-// inside the tile — a target in H has smem stride W_h * LT, a low target has
-// stride b_t — and its controls are decided per class (in-tile digits) or once per tile
-// (digits outside the tile, constant across it).
+// persistent grid, a producer warp and NT compute threads).  Between load and store the CTA
+// applies the pass's gates one after another in shared memory: each gate visits its
+// equivalence classes inside the tile — a target in H has smem stride
+// W_h * LT, a low target has stride b_t — and its controls are decided
+//   * per class from static bit masks: controls on H digits (a mask over the M members) and on
+//     low-prefix digits (a mask over the position modulo L = b_{m0}, identical in every tile);
+//   * per class from the tile's run offset: controls on run digits above the low prefix;
+//   * once per tile: controls on digits outside the tile (the producer's fire bits).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -24,22 +27,30 @@ constexpr int kMaxPassGates = 24;
 constexpr int kMaxMembers = 128;
 constexpr int kPoolC = 768;
 constexpr int kMaxPassCtrl = 4;
+constexpr int kMaskWords = 4 + 16;   // member mask (128 bits) + low-position mask (L < 512 bits)
 
+// in-pass gate kinds: general y = U x (§2.3), monomial y_{sigma(j)} = c_j x_j (§2.1-2.2),
+// and the pure permutation (every moving coefficient exactly 1: no arithmetic at all)
+enum PassKind : int32_t { kPGeneral = 0, kPMonomial = 1, kPPerm = 2 };
+
+// a control decided at run time (static in-tile controls live in the masks)
 struct PassCtrl {
-    int32_t cls;          // 0 = H digit (from member index), 1 = low digit (from run position), 2 = per tile
+    int32_t cls;          // 1 = run digit above the low prefix (needs the tile's run offset), 2 = outside the tile
     uint32_t v;
     uint32_t d, md;       // control dimension (+ magic)
-    uint32_t w, mw;       // cls 0: member radix weight; cls 1: stride b_c (+ magic)
+    uint32_t w, mw;       // cls 1: stride b_c (+ magic)
     uint32_t M, mM;       // cls 1: b_c * d_c (+ magic)
-    uint64_t b64, mb64;   // cls 2: global stride (+ magic); cls 1: M and its 64-bit magic
+    uint64_t b64, mb64;   // cls 2: global stride (+ magic); cls 1: 64-bit magic of M
     uint64_t md64;        // cls 2: magic for d
 };
 
+enum PassFlags : uint32_t { kFMemberMask = 1, kFLowMask = 2, kFRunCtrl = 4 };
+
 struct PassGateP {
     int32_t d, kind, nctrl, uoff;
-    int32_t inctl;        // has controls decided inside the tile (cls 0 / 1)
+    uint32_t flags;       // PassFlags: which in-tile control checks the gate needs
     uint32_t st, mst;     // smem stride of the target (+ magic)
-    uint32_t active;
+    uint32_t active;      // monomial / permutation: members that move or scale
     int8_t sigma[kMaxDim];
     PassCtrl c[kMaxPassCtrl];
 };
@@ -50,11 +61,13 @@ struct PassParams {
     RemovedRun rem[kMaxRem];
     uint64_t ntiles, R, tpr, tpr_m;
     uint32_t LT, mLT;     // run elements per member in a tile (+ magic)
+    uint32_t L, mL;       // low-prefix block b_{m0} (+ magic)
     int32_t M;            // members per tile
     int32_t ngates;
     int32_t upool;        // used entries of U (copied to shared memory at kernel start)
     uint64_t moff[kMaxMembers];
     PassGateP g[kMaxPassGates];
+    uint32_t mask[kMaxPassGates][kMaskWords];   // per gate: member mask, low-position mask
     double2 U[kPoolC];    // general: row-major d x d; monomial: coefficient per member
 };
 
@@ -87,16 +100,6 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
-__device__ __forceinline__ void cfma(double2 &acc, const double2 u, const double2 x) {
-    acc.x = fma(u.x, x.x, acc.x);
-    acc.x = fma(-u.y, x.y, acc.x);
-    acc.y = fma(u.x, x.y, acc.y);
-    acc.y = fma(u.y, x.x, acc.y);
-}
-__device__ __forceinline__ double2 cmul(const double2 u, const double2 x) {
-    return make_double2(fma(u.x, x.x, -u.y * x.y), fma(u.x, x.y, u.y * x.x));
-}
-
 struct TileInfo {
     uint64_t gbase;   // global index of member 0, run position 0
     uint64_t s0;      // offset of the tile inside its run
@@ -114,13 +117,13 @@ __device__ __forceinline__ TileInfo tile_info(const PassParams &p, uint64_t t) {
     return ti;
 }
 
-// Per-stage record written by warp 0 when it issues a tile's loads (before the mbarrier
+// Per-stage record written by the producer when it issues a tile's loads (before the mbarrier
 // arrive, so the consumers' acquire-wait sees it): the tile geometry, which gates fire on this
-// tile (controls outside the tile), and the run offsets of the low controls.
+// tile (controls outside the tile), and the run offsets of the run-digit controls.
 struct StageInfo {
     TileInfo ti;
     uint32_t fire;                                   // bit g: gate g's out-of-tile controls hold
-    uint32_t lowoff[kMaxPassGates][kMaxPassCtrl];    // (s0 mod b_c d_c) for low controls
+    uint32_t lowoff[kMaxPassGates][kMaxPassCtrl];    // (s0 mod b_c d_c) for run-digit controls
 };
 
 __device__ __forceinline__ void issue_loads(const PassParams &p, uint64_t t, double2 *buf, uint64_t *bar,
@@ -156,80 +159,46 @@ __device__ __forceinline__ void issue_loads(const PassParams &p, uint64_t t, dou
         bulk_load(buf + (size_t)m * p.LT, p.psi + ti.gbase + p.moff[m], ti.len * (uint32_t)sizeof(double2), bar);
 }
 
-// y = U x (general) or y_{sigma(j)} = c_j x_j (monomial) on one class at smem e0, stride st
-template <int D>
-__device__ __forceinline__ void apply_class(double2 *buf, uint32_t e0, uint32_t st, const PassGateP &g,
-                                            const double2 *U, int dd) {
-    constexpr int MD = D ? D : kMaxDim;
-    const int d = D ? D : dd;
-    double2 x[MD];
-    if (g.kind == kGeneral) {
-#pragma unroll
-        for (int j = 0; j < MD; ++j)
-            if (D || j < d) x[j] = buf[e0 + j * st];
-#pragma unroll
-        for (int i = 0; i < MD; ++i) {
-            if (D || i < d) {
-                double2 acc = make_double2(0.0, 0.0);
-#pragma unroll
-                for (int j = 0; j < MD; ++j)
-                    if (D || j < d) cfma(acc, U[i * d + j], x[j]);
-                buf[e0 + i * st] = acc;
-            }
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < MD; ++j)
-            if ((D || j < d) && ((g.active >> j) & 1)) x[j] = buf[e0 + j * st];
-#pragma unroll
-        for (int j = 0; j < MD; ++j)
-            if ((D || j < d) && ((g.active >> j) & 1)) buf[e0 + g.sigma[j] * st] = cmul(U[j], x[j]);
-    }
+// In-tile division (x < 2^16, d < 2^16): with m = floor(2^32/d) + 1, umulhi(x, m) is exact
+// because x * (m d - 2^32) <= x d < 2^32, so no fix-up step is needed (d == 1 <=> m == 0).
+__device__ __forceinline__ uint32_t tdiv(uint32_t x, uint32_t d, uint32_t m, uint32_t &r) {
+    const uint32_t q = m ? __umulhi(x, m) : x;
+    r = x - q * d;
+    return q;
 }
 
-// generic dimension: out of line so its 16-wide register arrays do not inflate the kernel
-__device__ __noinline__ void apply_class_generic(double2 *buf, uint32_t e0, uint32_t st, const PassGateP &g,
-                                                 const double2 *U) {
-    const int d = g.d;
-    if (g.kind == kGeneral) {
-        double2 x[kMaxDim];
-        for (int j = 0; j < d; ++j) x[j] = buf[e0 + j * st];
-        for (int i = 0; i < d; ++i) {
-            double2 acc = make_double2(0.0, 0.0);
-            for (int j = 0; j < d; ++j) cfma(acc, U[i * d + j], x[j]);
-            buf[e0 + i * st] = acc;
-        }
-    } else {
-        double2 x[kMaxDim];
-        for (int j = 0; j < d; ++j)
-            if ((g.active >> j) & 1) x[j] = buf[e0 + j * st];
-        for (int j = 0; j < d; ++j)
-            if ((g.active >> j) & 1) buf[e0 + g.sigma[j] * st] = cmul(U[j], x[j]);
-    }
-}
-
-// member-0 smem index of class c, and whether the class exists (ragged) and fires (controls)
-__device__ __forceinline__ bool class_at(const PassParams &p, const PassGateP &g, uint32_t len, bool needml,
-                                         const uint32_t *lowoff, uint32_t c, uint32_t &e0) {
+// member-0 smem index of class c (c < ncls): classes of stride st are grouped d*st apart
+__device__ __forceinline__ uint32_t class_e0(uint32_t c, uint32_t st, uint32_t mst, uint32_t d) {
     uint32_t off;
-    const uint32_t grp = fastdiv32(c, g.st, g.mst, off);
-    e0 = grp * g.st * (uint32_t)g.d + off;
-    if (!needml) return true;                            // full tile, no in-tile controls
+    const uint32_t grp = tdiv(c, st, mst, off);
+    return grp * st * d + off;
+}
+
+// What one gate needs to decide its classes inside the current tile.
+struct TileGate {
+    uint32_t LT, mLT, L, mL, len, flags;
+    const uint32_t *mask;       // shared memory: member mask words 0..3, low-position mask 4..19
+    const uint32_t *lowoff;     // shared memory: run offsets of the run-digit controls
+};
+
+// whether class e0 exists (ragged last tile of a run) and its in-tile controls hold
+__device__ __forceinline__ bool class_ok(const TileGate &tg, const PassGateP &g, uint32_t e0) {
     uint32_t l;
-    const uint32_t m = fastdiv32(e0, p.LT, p.mLT, l);
-    if (l >= len) return false;                          // ragged last tile of a run
-    bool ok = true;
-#pragma unroll
-    for (int k = 0; k < kMaxPassCtrl; ++k) {
-        if (k >= g.nctrl) break;
-        const PassCtrl &cc = g.c[k];
-        uint32_t r, r2;
-        if (cc.cls == 0) {
-            const uint32_t q = fastdiv32(m, cc.w, cc.mw, r);
-            fastdiv32(q, cc.d, cc.md, r2);
-            ok = ok && (r2 == cc.v);
-        } else if (cc.cls == 1) {
-            fastdiv32(lowoff[k] + l, cc.M, cc.mM, r);
+    const uint32_t m = tdiv(e0, tg.LT, tg.mLT, l);
+    bool ok = l < tg.len;
+    if (tg.flags & kFMemberMask) ok = ok && ((tg.mask[m >> 5] >> (m & 31)) & 1u);
+    if (tg.flags & kFLowMask) {
+        uint32_t lq;
+        tdiv(l, tg.L, tg.mL, lq);
+        ok = ok && ((tg.mask[4 + (lq >> 5)] >> (lq & 31)) & 1u);
+    }
+    if (tg.flags & kFRunCtrl) {
+#pragma unroll 1
+        for (int k = 0; k < g.nctrl; ++k) {
+            const PassCtrl &cc = g.c[k];
+            if (cc.cls != 1) continue;
+            uint32_t r, r2;
+            fastdiv32(tg.lowoff[k] + l, cc.M, cc.mM, r);
             const uint32_t q = fastdiv32(r, cc.w, cc.mw, r2);
             fastdiv32(q, cc.d, cc.md, r2);
             ok = ok && (r2 == cc.v);
@@ -238,79 +207,156 @@ __device__ __forceinline__ bool class_at(const PassParams &p, const PassGateP &g
     return ok;
 }
 
-// two classes per iteration: both gathers are issued before either matvec (ILP)
-template <int D>
-__device__ __forceinline__ void apply_class2(double2 *buf, uint32_t ea, bool oka, uint32_t eb, bool okb,
-                                             uint32_t st, const PassGateP &g, const double2 *U) {
-    double2 xa[D], xb[D];
-    if (g.kind == kGeneral) {
+// The K classes c0, c0+NT, ..., c0+(K-1)NT of one thread iteration (a warp's accesses stay
+// contiguous for strides >= 32): member-0 smem index and whether the class exists and fires.
+// Classes past ncls read index 0 and do not store.
+template <int K, int NT>
+__device__ __forceinline__ void class_batch(const TileGate &tg, const PassGateP &g, uint32_t c0, uint32_t ncls,
+                                            uint32_t D, bool needck, uint32_t (&e)[K], bool (&ok)[K]) {
+    const uint32_t st = g.st, mst = g.mst;
 #pragma unroll
-        for (int j = 0; j < D; ++j) {
-            if (oka) xa[j] = buf[ea + j * st];
-            if (okb) xb[j] = buf[eb + j * st];
-        }
+    for (int k = 0; k < K; ++k) {
+        const uint32_t c = c0 + (uint32_t)(k * NT);
+        ok[k] = c < ncls;
+        e[k] = ok[k] ? class_e0(c, st, mst, D) : 0u;
+        if (needck && ok[k]) ok[k] = class_ok(tg, g, e[k]);
+    }
+}
+
+// an offset the compiler cannot prove zero: keeps the matrix reads inside the class loop
+// (hoisting all d*d entries out of it would cost 4 d^2 registers per thread)
+__device__ __forceinline__ uint32_t opaque_zero(uint32_t v) {
+    uint32_t z;
+    asm("and.b32 %0, %1, 0;" : "=r"(z) : "r"(v));
+    return z;
+}
+
+// One general gate (y = U x per class) on one tile, K classes per thread
+// iteration.  All K*D gathers are issued before the matvecs; buf and U are restrict-qualified
+// so the matrix reads may be scheduled across the stores of earlier rows.
+template <int D, int K, int NT>
+__device__ __forceinline__ void gate_tile_general(const TileGate &tg, const PassGateP &g, double2 *__restrict__ buf,
+                                                  const double2 *__restrict__ U, uint32_t ncls, bool needck,
+                                                  int tid) {
+    const uint32_t st = g.st;
+#pragma unroll 1
+    for (uint32_t c0 = (uint32_t)tid; c0 < ncls; c0 += (uint32_t)(NT * K)) {
+        uint32_t e[K];
+        bool ok[K];
+        class_batch<K, NT>(tg, g, c0, ncls, (uint32_t)D, needck, e, ok);
+        const double2 *__restrict__ Ui = U + opaque_zero(c0);
+        double2 x[K][D];
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+#pragma unroll
+            for (int j = 0; j < D; ++j) x[k][j] = buf[e[k] + j * st];
 #pragma unroll
         for (int i = 0; i < D; ++i) {
-            double2 aa = make_double2(0.0, 0.0), ab = make_double2(0.0, 0.0);
+            double2 acc[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) acc[k] = make_double2(0.0, 0.0);
 #pragma unroll
             for (int j = 0; j < D; ++j) {
-                const double2 u = U[i * D + j];
-                cfma(aa, u, xa[j]);
-                cfma(ab, u, xb[j]);
+                const double2 u = Ui[i * D + j];
+#pragma unroll
+                for (int k = 0; k < K; ++k) cfma(acc[k], u, x[k][j]);
             }
-            if (oka) buf[ea + i * st] = aa;
-            if (okb) buf[eb + i * st] = ab;
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+                if (ok[k]) buf[e[k] + i * st] = acc[k];
         }
-    } else {
+    }
+}
+
+// One monomial gate (phase / permutation, y_{sigma(j)} = c_j x_j) on one
+// tile; PERM: every moving coefficient is exactly 1, so the gate only moves data.  Only the
+// members that move or scale are read and written (select-form predicated gathers: a branch
+// per member makes ptxas spill the array).
+template <int D, int K, int NT, bool PERM>
+__device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const PassGateP &g, double2 *__restrict__ buf,
+                                                   const double2 *__restrict__ U, uint32_t ncls, bool needck,
+                                                   int tid) {
+    const uint32_t st = g.st;
+    const uint32_t act = g.active;
+#pragma unroll 1
+    for (uint32_t c0 = (uint32_t)tid; c0 < ncls; c0 += (uint32_t)(NT * K)) {
+        uint32_t e[K];
+        bool ok[K];
+        class_batch<K, NT>(tg, g, c0, ncls, (uint32_t)D, needck, e, ok);
+        double2 x[K][D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            const bool aj = (act >> j) & 1;
+#pragma unroll
+            for (int k = 0; k < K; ++k) x[k][j] = aj ? buf[e[k] + j * st] : make_double2(0.0, 0.0);
+        }
 #pragma unroll
         for (int j = 0; j < D; ++j)
-            if ((g.active >> j) & 1) {
-                if (oka) xa[j] = buf[ea + j * st];
-                if (okb) xb[j] = buf[eb + j * st];
-            }
+            if ((act >> j) & 1) {
+                const uint32_t so = (uint32_t)g.sigma[j] * st;
+                if (PERM) {
 #pragma unroll
-        for (int j = 0; j < D; ++j)
-            if ((g.active >> j) & 1) {
-                const double2 u = U[j];
-                if (oka) buf[ea + g.sigma[j] * st] = cmul(u, xa[j]);
-                if (okb) buf[eb + g.sigma[j] * st] = cmul(u, xb[j]);
+                    for (int k = 0; k < K; ++k)
+                        if (ok[k]) buf[e[k] + so] = x[k][j];
+                } else {
+                    const double2 u = U[j];
+#pragma unroll
+                    for (int k = 0; k < K; ++k)
+                        if (ok[k]) buf[e[k] + so] = cmul(u, x[k][j]);
+                }
             }
     }
 }
 
-template <int D, int NT>
-__device__ __forceinline__ void apply_gate_tile(const PassParams &p, const PassGateP &g, double2 *buf,
-                                                const double2 *Us, uint32_t len, const uint32_t *lowoff,
-                                                int tid) {
-    const uint32_t nslots = (uint32_t)p.M * p.LT;
-    const uint32_t ncls = nslots / (uint32_t)g.d;
-    const double2 *U = Us + g.uoff;       // shared-memory copy: not hoisted into registers
-    const bool needml = g.inctl || len < p.LT;
-    if constexpr (D == 0) {
-        for (uint32_t c = tid; c < ncls; c += NT) {
-            uint32_t e0;
-            if (class_at(p, g, len, needml, lowoff, c, e0)) apply_class_generic(buf, e0, g.st, g, U);
-        }
-    } else if constexpr (D >= 4) {   // one class per iteration (register pressure)
-        for (uint32_t c = tid; c < ncls; c += NT) {
-            uint32_t e0;
-            if (class_at(p, g, len, needml, lowoff, c, e0)) apply_class<D>(buf, e0, g.st, g, U, g.d);
-        }
-    } else {                         // two classes per iteration (ILP)
-        for (uint32_t c = tid; c < ncls; c += 2 * NT) {
-            uint32_t ea = 0, eb = 0;
-            const bool oka = class_at(p, g, len, needml, lowoff, c, ea);
-            const uint32_t c2 = c + NT;
-            const bool okb = c2 < ncls && class_at(p, g, len, needml, lowoff, c2, eb);
-            apply_class2<D>(buf, ea, oka, eb, okb, g.st, g, U);
+// generic dimension (fused or d > 5): out of line so its 16-wide register arrays do not
+// inflate the kernel
+__device__ __noinline__ void gate_tile_generic(const TileGate &tg, const PassGateP &g, double2 *buf,
+                                               const double2 *U, uint32_t ncls, bool needck, int tid, int nt) {
+    const int d = g.d;
+    for (uint32_t c = tid; c < ncls; c += nt) {
+        const uint32_t e0 = class_e0(c, g.st, g.mst, (uint32_t)d);
+        if (needck && !class_ok(tg, g, e0)) continue;
+        double2 x[kMaxDim];
+        if (g.kind == kPGeneral) {
+            for (int j = 0; j < d; ++j) x[j] = buf[e0 + j * g.st];
+            for (int i = 0; i < d; ++i) {
+                double2 acc = make_double2(0.0, 0.0);
+                for (int j = 0; j < d; ++j) cfma(acc, U[i * d + j], x[j]);
+                buf[e0 + i * g.st] = acc;
+            }
+        } else {
+            for (int j = 0; j < d; ++j)
+                if ((g.active >> j) & 1) x[j] = buf[e0 + j * g.st];
+            for (int j = 0; j < d; ++j)
+                if ((g.active >> j) & 1) buf[e0 + g.sigma[j] * g.st] = cmul(U[j], x[j]);
         }
     }
+}
+
+// classes per thread iteration (registers: 4*K*D for the gathered classes), by thread count:
+// 256 threads may use up to ~200 registers, 384 up to 152, 512 up to 120
+template <int D, int NT> struct PassK { static constexpr int value = 1; };
+template <int NT> struct PassK<2, NT> { static constexpr int value = 4; };
+template <int NT> struct PassK<3, NT> { static constexpr int value = NT >= 512 ? 3 : 4; };
+template <int NT> struct PassK<4, NT> { static constexpr int value = NT >= 512 ? 2 : 3; };
+template <int NT> struct PassK<5, NT> { static constexpr int value = NT >= 384 ? 2 : 3; };
+
+// NT = compute threads of the CTA (sets the register budget), NTG = threads of one consumer
+// group (the class stride)
+template <int D, int NT, int NTG>
+__device__ __forceinline__ void apply_gate_tile(const TileGate &tg, const PassGateP &g, double2 *buf,
+                                                const double2 *U, uint32_t ncls, bool needck, int tid) {
+    constexpr int K = PassK<D, NT>::value;
+    if (g.kind == kPGeneral) gate_tile_general<D, K, NTG>(tg, g, buf, U, ncls, needck, tid);
+    else if (g.kind == kPPerm) gate_tile_monomial<D, K, NTG, true>(tg, g, buf, U, ncls, needck, tid);
+    else gate_tile_monomial<D, K, NTG, false>(tg, g, buf, U, ncls, needck, tid);
 }
 
 }  // namespace
 
-__device__ __forceinline__ void compute_barrier(int nthreads) {   // named barrier 1: compute warps only
-    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+// named barrier 1 + group: the compute warps of one consumer group only
+__device__ __forceinline__ void compute_barrier(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -319,12 +365,16 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 // Warp-specialised: warps 0..NT/32-1 compute, warp NT/32 is the producer (TMA loads, stage
 // records, TMA stores).  full[s] completes when a tile's bytes have landed; done[s] when the
 // compute warps have finished it (after fence.proxy.async, so the bulk store sees their writes).
-template <int NT>
+// The compute warps form G consumer groups of NT/G threads; group g takes the CTA's tiles
+// g, g+G, ... (ping-pong), so one group's barrier waits overlap the other groups' work.
+template <int NT, int G>
 __global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant__ PassParams p, int S, int TE) {
+    constexpr int NTG = NT / G;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double2 *bufs = reinterpret_cast<double2 *>(smem_raw);
     double2 *Us = bufs + (size_t)S * TE;                       // the pass's matrices
-    StageInfo *sinfo = reinterpret_cast<StageInfo *>(Us + p.upool);
+    uint32_t *masks = reinterpret_cast<uint32_t *>(Us + p.upool);
+    StageInfo *sinfo = reinterpret_cast<StageInfo *>(masks + kMaxPassGates * kMaskWords);
     uint64_t *full = reinterpret_cast<uint64_t *>(sinfo + S);
     uint64_t *done = full + S;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -333,6 +383,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant_
         fence_mbar_init();
     }
     for (int k = tid; k < p.upool; k += NT + 32) Us[k] = p.U[k];
+    for (int k = tid; k < p.ngates * kMaskWords; k += NT + 32) masks[k] = (&p.mask[0][0])[k];
     __syncthreads();
     const uint64_t first = blockIdx.x, step = gridDim.x;
     if (first >= p.ntiles) return;
@@ -362,7 +413,9 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant_
     }
 
     // ---------------- compute warps
-    for (uint64_t i = 0; i < my; ++i) {
+    const uint32_t slots = (uint32_t)p.M * p.LT;
+    const int grp = tid / NTG, gtid = tid % NTG;
+    for (uint64_t i = (uint64_t)grp; i < my; i += (uint64_t)G) {
         const int s = (int)(i % (uint64_t)S);
         double2 *buf = bufs + (size_t)s * TE;
         mbar_wait(&full[s], (uint32_t)((i / (uint64_t)S) & 1));
@@ -372,19 +425,29 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant_
         for (int gi = 0; gi < p.ngates; ++gi) {
             if (!((fire >> gi) & 1)) continue;          // out-of-tile control unmet: uniform skip
             const PassGateP &g = p.g[gi];
-            const uint32_t *lo = si.lowoff[gi];
+            TileGate tg;
+            tg.LT = p.LT;
+            tg.mLT = p.mLT;
+            tg.L = p.L;
+            tg.mL = p.mL;
+            tg.len = len;
+            tg.flags = g.flags;
+            tg.mask = masks + gi * kMaskWords;
+            tg.lowoff = si.lowoff[gi];
+            const bool needck = g.flags != 0 || len < p.LT;
+            const double2 *U = Us + g.uoff;
             switch (g.d) {
-                case 2: apply_gate_tile<2, NT>(p, g, buf, Us, len, lo, tid); break;
-                case 3: apply_gate_tile<3, NT>(p, g, buf, Us, len, lo, tid); break;
-                case 4: apply_gate_tile<4, NT>(p, g, buf, Us, len, lo, tid); break;
-                case 5: apply_gate_tile<5, NT>(p, g, buf, Us, len, lo, tid); break;
-                default: apply_gate_tile<0, NT>(p, g, buf, Us, len, lo, tid); break;
+                case 2: apply_gate_tile<2, NT, NTG>(tg, g, buf, U, slots / 2, needck, gtid); break;
+                case 3: apply_gate_tile<3, NT, NTG>(tg, g, buf, U, slots / 3, needck, gtid); break;
+                case 4: apply_gate_tile<4, NT, NTG>(tg, g, buf, U, slots / 4, needck, gtid); break;
+                case 5: apply_gate_tile<5, NT, NTG>(tg, g, buf, U, slots / 5, needck, gtid); break;
+                default: gate_tile_generic(tg, g, buf, U, slots / (uint32_t)g.d, needck, gtid, NTG); break;
             }
-            compute_barrier(NT);
+            compute_barrier(1 + grp, NTG);
         }
         fence_proxy_async();
-        compute_barrier(NT);
-        if (tid == 0) mbar_arrive(&done[s]);
+        compute_barrier(1 + grp, NTG);
+        if (gtid == 0) mbar_arrive(&done[s]);
     }
 }
 
@@ -397,6 +460,9 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
     p.psi = psi;
     const int m0 = pp.m0;
     const uint64_t L = (m0 < reg.n) ? reg.b[m0] : reg.D;
+    if (L > 32u * (kMaskWords - 4)) return false;          // low-position mask capacity
+    p.L = (uint32_t)L;
+    p.mL = make_fastdiv32(p.L).m;
     uint64_t M = 1;
     for (int h : pp.H) M *= (uint64_t)reg.dims[h];
     if (M > (uint64_t)kMaxMembers) return false;
@@ -429,8 +495,9 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
     }
     p.nrem = nr;
     // schedule: runs of the low space below min H, split into tiles of LT elements
-    // The run per member is widened to fill the tile (a multiple of b_{m0}, so low-prefix
-    // classes stay whole, and at most the run R below min H).
+    // The run per member is widened to fill the tile (a multiple of L = b_{m0}, so low-prefix
+    // classes stay whole and every tile starts at a multiple of L, and at most the run R below
+    // min H).
     const uint64_t R = pp.H.empty() ? reg.D : reg.b[pp.H[0]];
     uint64_t LT = ((uint64_t)TE / M / L) * L;
     if (LT < L) LT = L;
@@ -454,7 +521,13 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
         *touched += (double)gp.touched;
         PassGateP &q = p.g[gi];
         q.d = gp.d;
-        q.kind = gp.kind;
+        q.kind = gp.kind == kGeneral ? kPGeneral : kPMonomial;
+        if (q.kind == kPMonomial) {            // every moving coefficient exactly 1: pure data movement
+            bool perm = true;
+            for (int j = 0; j < gp.d; ++j)
+                if (((gp.active >> j) & 1) && !(gp.U[j].x == 1.0 && gp.U[j].y == 0.0)) perm = false;
+            if (perm) q.kind = kPPerm;
+        }
         q.active = gp.active;
         for (int j = 0; j < kMaxDim; ++j) q.sigma[j] = (int8_t)(j < gp.d ? gp.sigma[j] : j);
         const int need = gp.kind == kGeneral ? gp.d * gp.d : gp.d;
@@ -469,70 +542,96 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
         q.st = (uint32_t)st;
         q.mst = make_fastdiv32(q.st).m;
         if ((int)g.ctrl.size() > kMaxPassCtrl) return false;
-        q.nctrl = (int32_t)g.ctrl.size();
+        // static in-tile controls become bit masks; the rest are decided at run time
+        uint32_t *mm = p.mask[gi];
+        for (uint64_t m = 0; m < M; ++m) mm[m >> 5] |= 1u << (m & 31);
+        for (uint64_t l = 0; l < L; ++l) mm[4 + (l >> 5)] |= 1u << (l & 31);
+        int nc = 0;
         for (size_t k = 0; k < g.ctrl.size(); ++k) {
-            PassCtrl &cc = q.c[k];
             const int c = g.ctrl[k].q;
-            cc.v = (uint32_t)g.ctrl[k].v;
-            cc.d = (uint32_t)reg.dims[c];
+            const uint32_t v = (uint32_t)g.ctrl[k].v;
+            const uint64_t dc = (uint64_t)reg.dims[c];
+            if (std::find(pp.H.begin(), pp.H.end(), c) != pp.H.end()) {         // H digit: member mask
+                for (uint64_t m = 0; m < M; ++m)
+                    if ((m / W[c]) % dc != v) mm[m >> 5] &= ~(1u << (m & 31));
+                q.flags |= kFMemberMask;
+                continue;
+            }
+            if (c < m0) {                      // low-prefix digit: position mask modulo L
+                for (uint64_t l = 0; l < L; ++l)
+                    if ((l / reg.b[c]) % dc != v) mm[4 + (l >> 5)] &= ~(1u << (l & 31));
+                q.flags |= kFLowMask;
+                continue;
+            }
+            PassCtrl &cc = q.c[nc++];
+            cc.v = v;
+            cc.d = (uint32_t)dc;
             cc.md = make_fastdiv32(cc.d).m;
-            const bool inH = std::find(pp.H.begin(), pp.H.end(), c) != pp.H.end();
-            if (inH) {
-                cc.cls = 0;
-                q.inctl = 1;
-                cc.w = (uint32_t)W[c];
-                cc.mw = make_fastdiv32(cc.w).m;
-            } else if (reg.b[c] < R) {        // below min H: decided by the run position
+            if (reg.b[c] < R) {                // run digit above the low prefix: tile's run offset
                 cc.cls = 1;
-                q.inctl = 1;
+                q.flags |= kFRunCtrl;
                 cc.w = (uint32_t)reg.b[c];
                 cc.mw = make_fastdiv32(cc.w).m;
                 cc.M = cc.w * cc.d;
                 cc.mM = make_fastdiv32(cc.M).m;
                 cc.mb64 = make_fastdiv64(cc.M).m;
-            } else {                          // outside the tile: constant per tile
+            } else {                           // outside the tile: constant per tile
                 cc.cls = 2;
                 cc.b64 = reg.b[c];
                 cc.mb64 = make_fastdiv64(cc.b64).m;
                 cc.md64 = make_fastdiv64(cc.d).m;
             }
         }
+        q.nctrl = nc;
     }
     return p.ntiles > 0;
 }
 
-template <int NT>
+template <int NT, int G>
 cudaError_t launch_pass_t(const PassParams &p, cudaStream_t st, const LaunchCfg &cfg) {
     const int S = cfg.pass_stages, TE = cfg.pass_tile;
     // size for the largest matrix pool so the attribute and the occupancy are set once per config
     const size_t smem = (size_t)S * TE * sizeof(double2) + (size_t)kPoolC * sizeof(double2) +
+                        (size_t)kMaxPassGates * kMaskWords * sizeof(uint32_t) +
                         (size_t)S * sizeof(StageInfo) + (size_t)2 * S * sizeof(uint64_t);
     static size_t configured = 0, occ_for = 0;
     static int occ = 1;
     if (configured < smem) {
-        cudaError_t e = cudaFuncSetAttribute(k_gate_pass<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(k_gate_pass<NT, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         configured = smem;
     }
     if (occ_for != smem) {   // resident CTAs per SM at this smem size (persistent grid)
         int o = 1;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_gate_pass<NT>, NT + 32, smem) != cudaSuccess || o < 1) o = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_gate_pass<NT, G>, NT + 32, smem) != cudaSuccess || o < 1) o = 1;
         occ = o;
         occ_for = smem;
     }
     const uint64_t cap = (uint64_t)cfg.num_sms * (uint64_t)occ;
     const unsigned grid = (unsigned)(p.ntiles < cap ? p.ntiles : cap);
-    k_gate_pass<NT><<<grid, NT + 32, smem, st>>>(p, S, TE);
+    k_gate_pass<NT, G><<<grid, NT + 32, smem, st>>>(p, S, TE);
     return cudaGetLastError();
 }
 
 cudaError_t launch_pass(const PassParams &p, cudaStream_t st, const LaunchCfg &cfg) {
-    return cfg.pass_threads >= 512 ? launch_pass_t<512>(p, st, cfg) : launch_pass_t<256>(p, st, cfg);
+    int G = cfg.pass_groups;                      // one stage per group at least
+    while (G > 1 && cfg.pass_stages < G) G /= 2;
+    if (cfg.pass_threads >= 512) {
+        if (G >= 4) return launch_pass_t<512, 4>(p, st, cfg);
+        if (G == 2) return launch_pass_t<512, 2>(p, st, cfg);
+        return launch_pass_t<512, 1>(p, st, cfg);
+    }
+    if (cfg.pass_threads >= 384) {
+        if (G >= 2) return launch_pass_t<384, 2>(p, st, cfg);
+        return launch_pass_t<384, 1>(p, st, cfg);
+    }
+    if (G >= 2) return launch_pass_t<256, 2>(p, st, cfg);
+    return launch_pass_t<256, 1>(p, st, cfg);
 }
 
 cudaError_t run_pass(const Register &reg, const std::vector<GateSpec> &gates, const PassPlan &pp, double2 *psi,
                      cudaStream_t st, const LaunchCfg &cfg, bool *handled, double *touched) {
-    static thread_local PassParams p;   // ~21 KB; parameters are copied at launch
+    static thread_local PassParams p;   // ~23 KB; parameters are copied at launch
     *handled = build_pass(reg, gates, pp, psi, cfg.pass_tile, p, touched);
     if (!*handled) return cudaSuccess;
     return launch_pass(p, st, cfg);

@@ -59,10 +59,11 @@ void default_cfg(LaunchCfg &c, int device) {
     c.tile_stages = 3;
     c.ctas_per_sm = 2;
     c.num_sms = sms;
-    c.pass_tile = 6144;        // measured best on c3/c4 (profiles/r01/passbench_*)
-    c.pass_stages = 2;
-    c.pass_threads = 256;
+    c.pass_tile = 4096;        // measured best on c2-c4 (profiles/r01/passbench_*_groups.jsonl)
+    c.pass_stages = 3;
+    c.pass_threads = 384;
     c.pass_gates = 24;
+    c.pass_groups = 2;         // two consumer groups ping-pong over tiles
 }
 
 }  // namespace
@@ -488,12 +489,16 @@ sv_status sv_set_option(sv_handle h, int32_t option, int64_t value) {
             h->cfg.pass_tile = (int)value;
             return SV_OK;
         case SV_OPT_PASS_STAGES:
-            if (value < 2 || value > 4) return fail(SV_ERR_INVALID_ARG, "pass stages 2..4");
+            if (value < 2 || value > 6) return fail(SV_ERR_INVALID_ARG, "pass stages 2..6");
             h->cfg.pass_stages = (int)value;
             return SV_OK;
         case SV_OPT_PASS_THREADS:
-            if (value != 256 && value != 512) return fail(SV_ERR_INVALID_ARG, "pass threads 256 or 512");
+            if (value != 256 && value != 384 && value != 512) return fail(SV_ERR_INVALID_ARG, "pass threads 256, 384 or 512");
             h->cfg.pass_threads = (int)value;
+            return SV_OK;
+        case SV_OPT_PASS_GROUPS:
+            if (value != 1 && value != 2 && value != 4) return fail(SV_ERR_INVALID_ARG, "pass groups 1, 2 or 4");
+            h->cfg.pass_groups = (int)value;
             return SV_OK;
         case SV_OPT_PASS_GATES:
             if (value < 1 || value > 24) return fail(SV_ERR_INVALID_ARG, "pass gates 1..24");

@@ -28,11 +28,16 @@ def P():
 
 
 def run_gpu(P, dims, gates, psi0=None, kernel=0, fuse=False, graph=False, per_gate=False, block=False,
-            pass_tile=None):
+            pass_tile=None, pass_cfg=None):
     with P.State(dims) as st:
         st.set_option(P.sv.SV_OPT_KERNEL, kernel)
         if pass_tile:
             st.set_option(P.sv.SV_OPT_PASS_TILE, pass_tile)
+        if pass_cfg:
+            threads, groups, stages = pass_cfg
+            st.set_option(P.sv.SV_OPT_PASS_THREADS, threads)
+            st.set_option(P.sv.SV_OPT_PASS_GROUPS, groups)
+            st.set_option(P.sv.SV_OPT_PASS_STAGES, stages)
         if psi0 is not None:
             st.set_amplitudes(0, psi0)
         n0 = st.info().kernel_launches
@@ -353,8 +358,13 @@ def test_loopback_sharded_matches_single_state(P, nranks):
         del os.environ["SV_EXCHANGE_CHUNK"]
 
 
-@pytest.mark.parametrize("pass_tile", [4096, 1024, 256])
-def test_block_passes_random_sweep(P, pass_tile):
+# (compute threads, consumer groups, stages) of the pass kernel
+PASS_CFGS = [(256, 1, 2), (384, 1, 2), (512, 1, 2), (384, 2, 2), (256, 2, 3), (384, 2, 3), (512, 2, 3), (512, 4, 4)]
+
+
+@pytest.mark.parametrize("pass_cfg", PASS_CFGS)
+@pytest.mark.parametrize("pass_tile", [6144, 4096, 1024, 256])
+def test_block_passes_random_sweep(P, pass_tile, pass_cfg):
     """SV_BLOCK multi-gate passes on random registers and circuits with controls inside the
     tile (in-tile high digits, low digits) and outside it (per-tile predicate), ragged tiles,
     tiny registers; against O-2."""
@@ -367,11 +377,14 @@ def test_block_passes_random_sweep(P, pass_tile):
         _, gates = random_circuit(70_000 + s, dims, 80, max_ctrl=3)
         psi0 = random_state(int(np.prod(dims)), s)
         ref = O2.run(dims, gates, psi0)
-        got, nrm, _ = run_gpu(P, dims, gates, psi0, block=True, pass_tile=pass_tile)
+        if pass_tile * 16 * pass_cfg[2] > 200 * 1024:
+            pytest.skip("tile ring does not fit shared memory")
+        got, nrm, _ = run_gpu(P, dims, gates, psi0, block=True, pass_tile=pass_tile, pass_cfg=pass_cfg)
         assert np.max(np.abs(got - ref)) <= 1e-12, (dims, s)
 
 
-def test_block_passes_labelled_bit_exact(P):
+@pytest.mark.parametrize("pass_cfg", PASS_CFGS)
+def test_block_passes_labelled_bit_exact(P, pass_cfg):
     """Permutation-only circuits through multi-gate passes: bit-exact against O-2."""
     rng = np.random.default_rng(3)
     dims = config_circuit(4, ngates=0, nqubits=4)[0]
@@ -386,7 +399,8 @@ def test_block_passes_labelled_bit_exact(P):
         gates.append(Gate(t, ctrl, vals, permutation_matrix(rng.permutation(dims[t]))))
     psi0 = labelled_state(0, D)
     ref = O2.run(dims, gates, psi0)
-    got, _, launched = run_gpu(P, dims, gates, psi0, block=True)
+    tile = {2: 6144, 3: 4096}.get(pass_cfg[2], 2048)
+    got, _, launched = run_gpu(P, dims, gates, psi0, block=True, pass_tile=tile, pass_cfg=pass_cfg)
     assert launched < len(gates)
     assert np.array_equal(got, ref)
 
