@@ -179,19 +179,18 @@ struct TileGate {
     uint32_t LT, mLT, L, mL, len, flags;
     const uint32_t *mask;       // shared memory: member mask words 0..3, low-position mask 4..19
     const uint32_t *lowoff;     // shared memory: run offsets of the run-digit controls
+    const uint32_t *soff;       // shared memory: sigma(j) * st of a monomial gate
 };
 
 // whether class e0 exists (ragged last tile of a run) and its in-tile controls hold
 __device__ __forceinline__ bool class_ok(const TileGate &tg, const PassGateP &g, uint32_t e0) {
     uint32_t l;
     const uint32_t m = tdiv(e0, tg.LT, tg.mLT, l);
-    bool ok = l < tg.len;
-    if (tg.flags & kFMemberMask) ok = ok && ((tg.mask[m >> 5] >> (m & 31)) & 1u);
-    if (tg.flags & kFLowMask) {
-        uint32_t lq;
-        tdiv(l, tg.L, tg.mL, lq);
-        ok = ok && ((tg.mask[4 + (lq >> 5)] >> (lq & 31)) & 1u);
-    }
+    // static masks are all ones where a gate has no such control: evaluated without branches
+    uint32_t lq;
+    tdiv(l, tg.L, tg.mL, lq);
+    const uint32_t bits = (tg.mask[m >> 5] >> (m & 31)) & (tg.mask[4 + (lq >> 5)] >> (lq & 31));
+    bool ok = (l < tg.len) & (bits & 1u);
     if (tg.flags & kFRunCtrl) {
 #pragma unroll 1
         for (int k = 0; k < g.nctrl; ++k) {
@@ -236,11 +235,11 @@ __device__ __forceinline__ uint32_t opaque_zero(uint32_t v) {
 // so the matrix reads may be scheduled across the stores of earlier rows.
 template <int D, int K, int NT>
 __device__ __forceinline__ void gate_tile_general(const TileGate &tg, const PassGateP &g, double2 *__restrict__ buf,
-                                                  const double2 *__restrict__ U, uint32_t ncls, bool needck,
-                                                  int tid) {
+                                                  const double2 *__restrict__ U, uint32_t cbeg, uint32_t cend,
+                                                  uint32_t ncls, bool needck, int tid) {
     const uint32_t st = g.st;
 #pragma unroll 1
-    for (uint32_t c0 = (uint32_t)tid; c0 < ncls; c0 += (uint32_t)(NT * K)) {
+    for (uint32_t c0 = cbeg + (uint32_t)tid; c0 < cend; c0 += (uint32_t)(NT * K)) {
         uint32_t e[K];
         bool ok[K];
         class_batch<K, NT>(tg, g, c0, ncls, (uint32_t)D, needck, e, ok);
@@ -274,12 +273,18 @@ __device__ __forceinline__ void gate_tile_general(const TileGate &tg, const Pass
 // per member makes ptxas spill the array).
 template <int D, int K, int NT, bool PERM>
 __device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const PassGateP &g, double2 *__restrict__ buf,
-                                                   const double2 *__restrict__ U, uint32_t ncls, bool needck,
-                                                   int tid) {
+                                                   const double2 *__restrict__ U, uint32_t cbeg, uint32_t cend,
+                                                   uint32_t ncls, bool needck, int tid) {
     const uint32_t st = g.st;
     const uint32_t act = g.active;
+    // destination offsets sigma(j) * st, read once from shared memory: the stores below may
+    // alias that table as far as the compiler knows, so it keeps them in registers instead of
+    // re-reading the parameter bank inside the loop
+    uint32_t so[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) so[j] = tg.soff[j];
 #pragma unroll 1
-    for (uint32_t c0 = (uint32_t)tid; c0 < ncls; c0 += (uint32_t)(NT * K)) {
+    for (uint32_t c0 = cbeg + (uint32_t)tid; c0 < cend; c0 += (uint32_t)(NT * K)) {
         uint32_t e[K];
         bool ok[K];
         class_batch<K, NT>(tg, g, c0, ncls, (uint32_t)D, needck, e, ok);
@@ -293,16 +298,15 @@ __device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const Pas
 #pragma unroll
         for (int j = 0; j < D; ++j)
             if ((act >> j) & 1) {
-                const uint32_t so = (uint32_t)g.sigma[j] * st;
                 if (PERM) {
 #pragma unroll
                     for (int k = 0; k < K; ++k)
-                        if (ok[k]) buf[e[k] + so] = x[k][j];
+                        if (ok[k]) buf[e[k] + so[j]] = x[k][j];
                 } else {
                     const double2 u = U[j];
 #pragma unroll
                     for (int k = 0; k < K; ++k)
-                        if (ok[k]) buf[e[k] + so] = cmul(u, x[k][j]);
+                        if (ok[k]) buf[e[k] + so[j]] = cmul(u, x[k][j]);
                 }
             }
     }
@@ -310,7 +314,7 @@ __device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const Pas
 
 // generic dimension (fused or d > 5): out of line so its 16-wide register arrays do not
 // inflate the kernel
-__device__ __noinline__ void gate_tile_generic(const TileGate &tg, const PassGateP &g, double2 *buf,
+__device__ __noinline__ void gate_tile_generic(const TileGate tg, const PassGateP &g, double2 *buf,
                                                const double2 *U, uint32_t ncls, bool needck, int tid, int nt) {
     const int d = g.d;
     for (uint32_t c = tid; c < ncls; c += nt) {
@@ -347,9 +351,19 @@ template <int D, int NT, int NTG>
 __device__ __forceinline__ void apply_gate_tile(const TileGate &tg, const PassGateP &g, double2 *buf,
                                                 const double2 *U, uint32_t ncls, bool needck, int tid) {
     constexpr int K = PassK<D, NT>::value;
-    if (g.kind == kPGeneral) gate_tile_general<D, K, NTG>(tg, g, buf, U, ncls, needck, tid);
-    else if (g.kind == kPPerm) gate_tile_monomial<D, K, NTG, true>(tg, g, buf, U, ncls, needck, tid);
-    else gate_tile_monomial<D, K, NTG, false>(tg, g, buf, U, ncls, needck, tid);
+    // full batches of K classes per thread, then the remainder one class per thread (no idle
+    // batch slots in the tail)
+    const uint32_t full = ncls / (uint32_t)(NTG * K) * (uint32_t)(NTG * K);
+    if (g.kind == kPGeneral) {
+        gate_tile_general<D, K, NTG>(tg, g, buf, U, 0, full, ncls, needck, tid);
+        gate_tile_general<D, 1, NTG>(tg, g, buf, U, full, ncls, ncls, needck, tid);
+    } else if (g.kind == kPPerm) {
+        gate_tile_monomial<D, K, NTG, true>(tg, g, buf, U, 0, full, ncls, needck, tid);
+        gate_tile_monomial<D, 1, NTG, true>(tg, g, buf, U, full, ncls, ncls, needck, tid);
+    } else {
+        gate_tile_monomial<D, K, NTG, false>(tg, g, buf, U, 0, full, ncls, needck, tid);
+        gate_tile_monomial<D, 1, NTG, false>(tg, g, buf, U, full, ncls, ncls, needck, tid);
+    }
 }
 
 }  // namespace
@@ -374,7 +388,8 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant_
     double2 *bufs = reinterpret_cast<double2 *>(smem_raw);
     double2 *Us = bufs + (size_t)S * TE;                       // the pass's matrices
     uint32_t *masks = reinterpret_cast<uint32_t *>(Us + p.upool);
-    StageInfo *sinfo = reinterpret_cast<StageInfo *>(masks + kMaxPassGates * kMaskWords);
+    uint32_t *soffs = masks + kMaxPassGates * kMaskWords;     // per gate: sigma(j) * st
+    StageInfo *sinfo = reinterpret_cast<StageInfo *>(soffs + kMaxPassGates * kMaxDim);
     uint64_t *full = reinterpret_cast<uint64_t *>(sinfo + S);
     uint64_t *done = full + S;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -384,6 +399,8 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant_
     }
     for (int k = tid; k < p.upool; k += NT + 32) Us[k] = p.U[k];
     for (int k = tid; k < p.ngates * kMaskWords; k += NT + 32) masks[k] = (&p.mask[0][0])[k];
+    for (int k = tid; k < p.ngates * kMaxDim; k += NT + 32)
+        soffs[k] = (uint32_t)p.g[k / kMaxDim].sigma[k % kMaxDim] * p.g[k / kMaxDim].st;
     __syncthreads();
     const uint64_t first = blockIdx.x, step = gridDim.x;
     if (first >= p.ntiles) return;
@@ -434,6 +451,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant_
             tg.flags = g.flags;
             tg.mask = masks + gi * kMaskWords;
             tg.lowoff = si.lowoff[gi];
+            tg.soff = soffs + gi * kMaxDim;
             const bool needck = g.flags != 0 || len < p.LT;
             const double2 *U = Us + g.uoff;
             switch (g.d) {
@@ -592,7 +610,7 @@ cudaError_t launch_pass_t(const PassParams &p, cudaStream_t st, const LaunchCfg 
     const int S = cfg.pass_stages, TE = cfg.pass_tile;
     // size for the largest matrix pool so the attribute and the occupancy are set once per config
     const size_t smem = (size_t)S * TE * sizeof(double2) + (size_t)kPoolC * sizeof(double2) +
-                        (size_t)kMaxPassGates * kMaskWords * sizeof(uint32_t) +
+                        (size_t)kMaxPassGates * (kMaskWords + kMaxDim) * sizeof(uint32_t) +
                         (size_t)S * sizeof(StageInfo) + (size_t)2 * S * sizeof(uint64_t);
     static size_t configured = 0, occ_for = 0;
     static int occ = 1;
