@@ -1,15 +1,473 @@
-// mgpass.cu — host side of the multi-gate pass kernel: pass parameters,
-// register-stage planning, launch dispatch.  The kernel is in mgpass_impl.cuh; its
-// instantiations live in mgpass_k256.cu / mgpass_k384.cu.
-#include "mgpass_impl.cuh"
+// mgpass.cu — multi-gate cache-blocked pass kernel for sm_100a.
+//
+// One HBM pass applies a whole list of gates.  A tile holds every digit value of the in-tile
+// qudits Q = {q_0..q_{m0-1}} ∪ H (plan_passes) and one value of every other digit, laid out in
+// shared memory as [member][run] where a "member" is one combination of the H digits (global
+// offset sum_h j_h b_h) and the run is a contiguous stretch of the low space (stride < b_{min H}).
+// Loading / storing a tile = one cp.async.bulk per member (TMA bulk copies onto an mbarrier,
+// persistent grid, a producer warp and NT compute threads).  Between load and store the CTA
+// applies the pass's gates one after another in shared memory: each gate visits its
+// equivalence classes inside the tile — a target in H has smem stride
+// W_h * LT, a low target has stride b_t — and its controls are decided
+//   * per class from static bit masks: controls on H digits (a mask over the M members) and on
+//     low-prefix digits (a mask over the position modulo L = b_{m0}, identical in every tile);
+//   * per class from the tile's run offset: controls on run digits above the low prefix;
+//   * once per tile: controls on digits outside the tile (the producer's fire bits).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "sv_internal.h"
+#include "plan.h"
 
 namespace svi {
 
-// explicit instantiations in mgpass_k256.cu / mgpass_k384.cu
-extern template cudaError_t launch_pass_t<256, 1>(const PassParams &, cudaStream_t, const LaunchCfg &);
-extern template cudaError_t launch_pass_t<256, 2>(const PassParams &, cudaStream_t, const LaunchCfg &);
-extern template cudaError_t launch_pass_t<384, 1>(const PassParams &, cudaStream_t, const LaunchCfg &);
-extern template cudaError_t launch_pass_t<384, 2>(const PassParams &, cudaStream_t, const LaunchCfg &);
+constexpr int kMaxPassGates = 24;
+constexpr int kMaxMembers = 128;
+constexpr int kPoolC = 768;
+constexpr int kMaxPassCtrl = 4;
+constexpr int kMaskWords = 4 + 16;   // member mask (128 bits) + low-position mask (L < 512 bits)
+
+// in-pass gate kinds: general y = U x (§2.3), monomial y_{sigma(j)} = c_j x_j (§2.1-2.2),
+// and the pure permutation (every moving coefficient exactly 1: no arithmetic at all)
+enum PassKind : int32_t { kPGeneral = 0, kPMonomial = 1, kPPerm = 2 };
+
+// a control decided at run time (static in-tile controls live in the masks)
+struct PassCtrl {
+    int32_t cls;          // 1 = run digit above the low prefix (needs the tile's run offset), 2 = outside the tile
+    uint32_t v;
+    uint32_t d, md;       // control dimension (+ magic)
+    uint32_t w, mw;       // cls 1: stride b_c (+ magic)
+    uint32_t M, mM;       // cls 1: b_c * d_c (+ magic)
+    uint64_t b64, mb64;   // cls 2: global stride (+ magic); cls 1: 64-bit magic of M
+    uint64_t md64;        // cls 2: magic for d
+};
+
+enum PassFlags : uint32_t { kFMemberMask = 1, kFLowMask = 2, kFRunCtrl = 4 };
+
+struct PassGateP {
+    int32_t d, kind, nctrl, uoff;
+    uint32_t flags;       // PassFlags: which in-tile control checks the gate needs
+    uint32_t st, mst;     // smem stride of the target (+ magic)
+    uint32_t active;      // monomial / permutation: members that move or scale
+    int8_t sigma[kMaxDim];
+    PassCtrl c[kMaxPassCtrl];
+};
+
+struct PassParams {
+    double2 *psi;
+    int32_t nrem;
+    RemovedRun rem[kMaxRem];
+    uint64_t ntiles, R, tpr, tpr_m;
+    uint32_t LT, mLT;     // run elements per member in a tile (+ magic)
+    uint32_t L, mL;       // low-prefix block b_{m0} (+ magic)
+    int32_t M;            // members per tile
+    int32_t ngates;
+    int32_t upool;        // used entries of U (copied to shared memory at kernel start)
+    uint64_t moff[kMaxMembers];
+    PassGateP g[kMaxPassGates];
+    uint32_t mask[kMaxPassGates][kMaskWords];   // per gate: member mask, low-position mask
+    double2 U[kPoolC];    // general: row-major d x d; monomial: coefficient per member
+};
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_store(void *dst, const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+struct TileInfo {
+    uint64_t gbase;   // global index of member 0, run position 0
+    uint64_t s0;      // offset of the tile inside its run
+    uint32_t len;     // valid run elements per member
+};
+
+__device__ __forceinline__ TileInfo tile_info(const PassParams &p, uint64_t t) {
+    TileInfo ti;
+    uint64_t sub;
+    const uint64_t run = fastdiv64(t, p.tpr, p.tpr_m, sub);
+    ti.s0 = sub * p.LT;
+    const uint64_t rem = p.R - ti.s0;
+    ti.len = (uint32_t)(rem < p.LT ? rem : p.LT);
+    ti.gbase = insert_digits(run * p.R + ti.s0, p.nrem, p.rem);
+    return ti;
+}
+
+// Per-stage record written by the producer when it issues a tile's loads (before the mbarrier
+// arrive, so the consumers' acquire-wait sees it): the tile geometry, which gates fire on this
+// tile (controls outside the tile), and the run offsets of the run-digit controls.
+struct StageInfo {
+    TileInfo ti;
+    uint32_t fire;                                   // bit g: gate g's out-of-tile controls hold
+    uint32_t lowoff[kMaxPassGates][kMaxPassCtrl];    // (s0 mod b_c d_c) for run-digit controls
+};
+
+__device__ __forceinline__ void issue_loads(const PassParams &p, uint64_t t, double2 *buf, uint64_t *bar,
+                                            StageInfo *si, int lane) {
+    const TileInfo ti = tile_info(p, t);
+    // lane g decides gate g for this tile
+    bool fire = true;
+    if (lane < p.ngates) {
+        const PassGateP &g = p.g[lane];
+        for (int k = 0; k < g.nctrl; ++k) {
+            const PassCtrl &cc = g.c[k];
+            if (cc.cls == 2) {
+                uint64_t r;
+                const uint64_t q = fastdiv64(ti.gbase, cc.b64, cc.mb64, r);
+                fastdiv64(q, cc.d, cc.md64, r);
+                fire = fire && (r == cc.v);
+            } else if (cc.cls == 1) {
+                uint64_t r;
+                fastdiv64(ti.s0, cc.M, cc.mb64, r);
+                si->lowoff[lane][k] = (uint32_t)r;
+            }
+        }
+    }
+    const uint32_t bits = __ballot_sync(0xffffffffu, fire && lane < p.ngates);
+    if (lane == 0) {
+        si->ti = ti;
+        si->fire = bits;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_expect_tx(bar, (uint32_t)p.M * ti.len * (uint32_t)sizeof(double2));
+    __syncwarp();
+    for (int m = lane; m < p.M; m += 32)
+        bulk_load(buf + (size_t)m * p.LT, p.psi + ti.gbase + p.moff[m], ti.len * (uint32_t)sizeof(double2), bar);
+}
+
+// In-tile division (x < 2^16, d < 2^16): with m = floor(2^32/d) + 1, umulhi(x, m) is exact
+// because x * (m d - 2^32) <= x d < 2^32, so no fix-up step is needed (d == 1 <=> m == 0).
+__device__ __forceinline__ uint32_t tdiv(uint32_t x, uint32_t d, uint32_t m, uint32_t &r) {
+    const uint32_t q = m ? __umulhi(x, m) : x;
+    r = x - q * d;
+    return q;
+}
+
+// member-0 smem index of class c (c < ncls): classes of stride st are grouped d*st apart
+__device__ __forceinline__ uint32_t class_e0(uint32_t c, uint32_t st, uint32_t mst, uint32_t d) {
+    uint32_t off;
+    const uint32_t grp = tdiv(c, st, mst, off);
+    return grp * st * d + off;
+}
+
+// What one gate needs to decide its classes inside the current tile.
+struct TileGate {
+    uint32_t LT, mLT, L, mL, len, flags;
+    const uint32_t *mask;       // shared memory: member mask words 0..3, low-position mask 4..19
+    const uint32_t *lowoff;     // shared memory: run offsets of the run-digit controls
+    const uint32_t *soff;       // shared memory: sigma(j) * st of a monomial gate
+};
+
+// whether class e0 exists (ragged last tile of a run) and its in-tile controls hold
+__device__ __forceinline__ bool class_ok(const TileGate &tg, const PassGateP &g, uint32_t e0) {
+    uint32_t l;
+    const uint32_t m = tdiv(e0, tg.LT, tg.mLT, l);
+    // static masks are all ones where a gate has no such control: evaluated without branches
+    uint32_t lq;
+    tdiv(l, tg.L, tg.mL, lq);
+    const uint32_t bits = (tg.mask[m >> 5] >> (m & 31)) & (tg.mask[4 + (lq >> 5)] >> (lq & 31));
+    bool ok = (l < tg.len) & (bits & 1u);
+    if (tg.flags & kFRunCtrl) {
+#pragma unroll 1
+        for (int k = 0; k < g.nctrl; ++k) {
+            const PassCtrl &cc = g.c[k];
+            if (cc.cls != 1) continue;
+            uint32_t r, r2;
+            fastdiv32(tg.lowoff[k] + l, cc.M, cc.mM, r);
+            const uint32_t q = fastdiv32(r, cc.w, cc.mw, r2);
+            fastdiv32(q, cc.d, cc.md, r2);
+            ok = ok && (r2 == cc.v);
+        }
+    }
+    return ok;
+}
+
+// The K classes c0, c0+NT, ..., c0+(K-1)NT of one thread iteration (a warp's accesses stay
+// contiguous for strides >= 32): member-0 smem index and whether the class exists and fires.
+// Classes past ncls read index 0 and do not store.
+template <int K, int NT>
+__device__ __forceinline__ void class_batch(const TileGate &tg, const PassGateP &g, uint32_t c0, uint32_t ncls,
+                                            uint32_t D, bool needck, uint32_t (&e)[K], bool (&ok)[K]) {
+    const uint32_t st = g.st, mst = g.mst;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const uint32_t c = c0 + (uint32_t)(k * NT);
+        ok[k] = c < ncls;
+        e[k] = ok[k] ? class_e0(c, st, mst, D) : 0u;
+        if (needck && ok[k]) ok[k] = class_ok(tg, g, e[k]);
+    }
+}
+
+// an offset the compiler cannot prove zero: keeps the matrix reads inside the class loop
+// (hoisting all d*d entries out of it would cost 4 d^2 registers per thread)
+__device__ __forceinline__ uint32_t opaque_zero(uint32_t v) {
+    uint32_t z;
+    asm("and.b32 %0, %1, 0;" : "=r"(z) : "r"(v));
+    return z;
+}
+
+// One general gate (y = U x per class) on one tile, K classes per thread
+// iteration.  All K*D gathers are issued before the matvecs; buf and U are restrict-qualified
+// so the matrix reads may be scheduled across the stores of earlier rows.
+template <int D, int K, int NT>
+__device__ __forceinline__ void gate_tile_general(const TileGate &tg, const PassGateP &g, double2 *__restrict__ buf,
+                                                  const double2 *__restrict__ U, uint32_t cbeg, uint32_t cend,
+                                                  uint32_t ncls, bool needck, int tid) {
+    const uint32_t st = g.st;
+#pragma unroll 1
+    for (uint32_t c0 = cbeg + (uint32_t)tid; c0 < cend; c0 += (uint32_t)(NT * K)) {
+        uint32_t e[K];
+        bool ok[K];
+        class_batch<K, NT>(tg, g, c0, ncls, (uint32_t)D, needck, e, ok);
+        const double2 *__restrict__ Ui = U + opaque_zero(c0);
+        double2 x[K][D];
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+#pragma unroll
+            for (int j = 0; j < D; ++j) x[k][j] = buf[e[k] + j * st];
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            double2 acc[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) acc[k] = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                const double2 u = Ui[i * D + j];
+#pragma unroll
+                for (int k = 0; k < K; ++k) cfma(acc[k], u, x[k][j]);
+            }
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+                if (ok[k]) buf[e[k] + i * st] = acc[k];
+        }
+    }
+}
+
+// One monomial gate (phase / permutation, y_{sigma(j)} = c_j x_j) on one
+// tile; PERM: every moving coefficient is exactly 1, so the gate only moves data.  Only the
+// members that move or scale are read and written (select-form predicated gathers: a branch
+// per member makes ptxas spill the array).
+template <int D, int K, int NT, bool PERM>
+__device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const PassGateP &g, double2 *__restrict__ buf,
+                                                   const double2 *__restrict__ U, uint32_t cbeg, uint32_t cend,
+                                                   uint32_t ncls, bool needck, int tid) {
+    const uint32_t st = g.st;
+    const uint32_t act = g.active;
+    // destination offsets sigma(j) * st, read once from shared memory: the stores below may
+    // alias that table as far as the compiler knows, so it keeps them in registers instead of
+    // re-reading the parameter bank inside the loop
+    uint32_t so[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) so[j] = tg.soff[j];
+#pragma unroll 1
+    for (uint32_t c0 = cbeg + (uint32_t)tid; c0 < cend; c0 += (uint32_t)(NT * K)) {
+        uint32_t e[K];
+        bool ok[K];
+        class_batch<K, NT>(tg, g, c0, ncls, (uint32_t)D, needck, e, ok);
+        double2 x[K][D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            const bool aj = (act >> j) & 1;
+#pragma unroll
+            for (int k = 0; k < K; ++k) x[k][j] = aj ? buf[e[k] + j * st] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int j = 0; j < D; ++j)
+            if ((act >> j) & 1) {
+                if (PERM) {
+#pragma unroll
+                    for (int k = 0; k < K; ++k)
+                        if (ok[k]) buf[e[k] + so[j]] = x[k][j];
+                } else {
+                    const double2 u = U[j];
+#pragma unroll
+                    for (int k = 0; k < K; ++k)
+                        if (ok[k]) buf[e[k] + so[j]] = cmul(u, x[k][j]);
+                }
+            }
+    }
+}
+
+// generic dimension (fused or d > 5): out of line so its 16-wide register arrays do not
+// inflate the kernel
+__device__ __noinline__ void gate_tile_generic(const TileGate tg, const PassGateP &g, double2 *buf,
+                                               const double2 *U, uint32_t ncls, bool needck, int tid, int nt) {
+    const int d = g.d;
+    for (uint32_t c = tid; c < ncls; c += nt) {
+        const uint32_t e0 = class_e0(c, g.st, g.mst, (uint32_t)d);
+        if (needck && !class_ok(tg, g, e0)) continue;
+        double2 x[kMaxDim];
+        if (g.kind == kPGeneral) {
+            for (int j = 0; j < d; ++j) x[j] = buf[e0 + j * g.st];
+            for (int i = 0; i < d; ++i) {
+                double2 acc = make_double2(0.0, 0.0);
+                for (int j = 0; j < d; ++j) cfma(acc, U[i * d + j], x[j]);
+                buf[e0 + i * g.st] = acc;
+            }
+        } else {
+            for (int j = 0; j < d; ++j)
+                if ((g.active >> j) & 1) x[j] = buf[e0 + j * g.st];
+            for (int j = 0; j < d; ++j)
+                if ((g.active >> j) & 1) buf[e0 + g.sigma[j] * g.st] = cmul(U[j], x[j]);
+        }
+    }
+}
+
+// classes per thread iteration (registers: 4*K*D for the gathered classes), by thread count:
+// 256 threads may use up to ~200 registers, 384 up to 152, 512 up to 120
+template <int D, int NT> struct PassK { static constexpr int value = 1; };
+template <int NT> struct PassK<2, NT> { static constexpr int value = 4; };
+template <int NT> struct PassK<3, NT> { static constexpr int value = NT >= 512 ? 3 : 4; };
+template <int NT> struct PassK<4, NT> { static constexpr int value = NT >= 512 ? 2 : 3; };
+template <int NT> struct PassK<5, NT> { static constexpr int value = NT >= 384 ? 2 : 3; };
+
+// NT = compute threads of the CTA (sets the register budget), NTG = threads of one consumer
+// group (the class stride)
+template <int D, int NT, int NTG>
+__device__ __forceinline__ void apply_gate_tile(const TileGate &tg, const PassGateP &g, double2 *buf,
+                                                const double2 *U, uint32_t ncls, bool needck, int tid) {
+    constexpr int K = PassK<D, NT>::value;
+    // full batches of K classes per thread, then the remainder one class per thread (no idle
+    // batch slots in the tail)
+    const uint32_t full = ncls / (uint32_t)(NTG * K) * (uint32_t)(NTG * K);
+    if (g.kind == kPGeneral) {
+        gate_tile_general<D, K, NTG>(tg, g, buf, U, 0, full, ncls, needck, tid);
+        gate_tile_general<D, 1, NTG>(tg, g, buf, U, full, ncls, ncls, needck, tid);
+    } else if (g.kind == kPPerm) {
+        gate_tile_monomial<D, K, NTG, true>(tg, g, buf, U, 0, full, ncls, needck, tid);
+        gate_tile_monomial<D, 1, NTG, true>(tg, g, buf, U, full, ncls, ncls, needck, tid);
+    } else {
+        gate_tile_monomial<D, K, NTG, false>(tg, g, buf, U, 0, full, ncls, needck, tid);
+        gate_tile_monomial<D, 1, NTG, false>(tg, g, buf, U, full, ncls, ncls, needck, tid);
+    }
+}
+
+}  // namespace
+
+// named barrier 1 + group: the compute warps of one consumer group only
+__device__ __forceinline__ void compute_barrier(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Warp-specialised: warps 0..NT/32-1 compute, warp NT/32 is the producer (TMA loads, stage
+// records, TMA stores).  full[s] completes when a tile's bytes have landed; done[s] when the
+// compute warps have finished it (after fence.proxy.async, so the bulk store sees their writes).
+// The compute warps form G consumer groups of NT/G threads; group g takes the CTA's tiles
+// g, g+G, ... (ping-pong), so one group's barrier waits overlap the other groups' work.
+template <int NT, int G>
+__global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant__ PassParams p, int S, int TE) {
+    constexpr int NTG = NT / G;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double2 *bufs = reinterpret_cast<double2 *>(smem_raw);
+    double2 *Us = bufs + (size_t)S * TE;                       // the pass's matrices
+    uint32_t *masks = reinterpret_cast<uint32_t *>(Us + p.upool);
+    uint32_t *soffs = masks + kMaxPassGates * kMaskWords;     // per gate: sigma(j) * st
+    StageInfo *sinfo = reinterpret_cast<StageInfo *>(soffs + kMaxPassGates * kMaxDim);
+    uint64_t *full = reinterpret_cast<uint64_t *>(sinfo + S);
+    uint64_t *done = full + S;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&done[s], 1); }
+        fence_mbar_init();
+    }
+    for (int k = tid; k < p.upool; k += NT + 32) Us[k] = p.U[k];
+    for (int k = tid; k < p.ngates * kMaskWords; k += NT + 32) masks[k] = (&p.mask[0][0])[k];
+    for (int k = tid; k < p.ngates * kMaxDim; k += NT + 32)
+        soffs[k] = (uint32_t)p.g[k / kMaxDim].sigma[k % kMaxDim] * p.g[k / kMaxDim].st;
+    __syncthreads();
+    const uint64_t first = blockIdx.x, step = gridDim.x;
+    if (first >= p.ntiles) return;
+    const uint64_t my = (p.ntiles - first + step - 1) / step;
+
+    if (warp == NT / 32) {
+        // ---------------- producer warp
+        for (uint64_t i = 0; i < my + (uint64_t)S; ++i) {
+            const int s = (int)(i % (uint64_t)S);
+            if (i >= (uint64_t)S) {                   // drain tile i-S from stage s
+                const uint64_t j = i - (uint64_t)S;
+                if (j >= my) continue;
+                mbar_wait(&done[s], (uint32_t)((j / (uint64_t)S) & 1));
+                const StageInfo &si = sinfo[s];
+                for (int m = lane; m < p.M; m += 32)
+                    bulk_store(p.psi + si.ti.gbase + p.moff[m], bufs + (size_t)s * TE + (size_t)m * p.LT,
+                               si.ti.len * (uint32_t)sizeof(double2));
+                bulk_commit();
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                __syncwarp();
+            }
+            if (i < my)
+                issue_loads(p, first + i * step, bufs + (size_t)s * TE, &full[s], &sinfo[s], lane);
+        }
+        bulk_wait_all();
+        return;
+    }
+
+    // ---------------- compute warps
+    const uint32_t slots = (uint32_t)p.M * p.LT;
+    const int grp = tid / NTG, gtid = tid % NTG;
+    for (uint64_t i = (uint64_t)grp; i < my; i += (uint64_t)G) {
+        const int s = (int)(i % (uint64_t)S);
+        double2 *buf = bufs + (size_t)s * TE;
+        mbar_wait(&full[s], (uint32_t)((i / (uint64_t)S) & 1));
+        const StageInfo &si = sinfo[s];
+        const uint32_t len = si.ti.len;
+        const uint32_t fire = si.fire;
+        for (int gi = 0; gi < p.ngates; ++gi) {
+            if (!((fire >> gi) & 1)) continue;          // out-of-tile control unmet: uniform skip
+            const PassGateP &g = p.g[gi];
+            TileGate tg;
+            tg.LT = p.LT;
+            tg.mLT = p.mLT;
+            tg.L = p.L;
+            tg.mL = p.mL;
+            tg.len = len;
+            tg.flags = g.flags;
+            tg.mask = masks + gi * kMaskWords;
+            tg.lowoff = si.lowoff[gi];
+            tg.soff = soffs + gi * kMaxDim;
+            const bool needck = g.flags != 0 || len < p.LT;
+            const double2 *U = Us + g.uoff;
+            switch (g.d) {
+                case 2: apply_gate_tile<2, NT, NTG>(tg, g, buf, U, slots / 2, needck, gtid); break;
+                case 3: apply_gate_tile<3, NT, NTG>(tg, g, buf, U, slots / 3, needck, gtid); break;
+                case 4: apply_gate_tile<4, NT, NTG>(tg, g, buf, U, slots / 4, needck, gtid); break;
+                case 5: apply_gate_tile<5, NT, NTG>(tg, g, buf, U, slots / 5, needck, gtid); break;
+                default: gate_tile_generic(tg, g, buf, U, slots / (uint32_t)g.d, needck, gtid, NTG); break;
+            }
+            compute_barrier(1 + grp, NTG);
+        }
+        fence_proxy_async();
+        compute_barrier(1 + grp, NTG);
+        if (gtid == 0) mbar_arrive(&done[s]);
+    }
+}
 
 // ------------------------------------------------------------------------------ host
 // Build the pass parameters; returns false if the pass does not fit this kernel.
@@ -69,121 +527,40 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
     p.tpr_m = make_fastdiv64(p.tpr).m;
     const uint64_t nruns = reg.D / (M * R);
     p.ntiles = nruns * p.tpr;
-    // Register stages: regroup the pass's gates, only across gates they
-    // commute with, into runs whose targets are one or two in-tile qudits ("axes", product of
-    // dimensions <= kMaxPair); gates of dimension > 5 get a generic stage of their own.
-    auto generic = [](const GateSpec &g) { return g.span != 1 || g.d < 2 || g.d > 5; };
-    auto tile_stride = [&](int t) -> uint64_t { return t < m0 ? reg.b[t] : W[t] * LT; };
-    for (int i : pp.gates) {
-        const int t = gates[i].target;
-        if (gates[i].span != 1 || (t >= m0 && std::find(pp.H.begin(), pp.H.end(), t) == pp.H.end())) return false;
-    }
-    constexpr int kMaxPair = 16;
-    std::vector<int> order, rest(pp.gates.begin(), pp.gates.end());
-    std::vector<int> axis_a, axis_b;        // per stage: axis digits (b = -1: one axis)
-    p.nstages = 0;
-    while (!rest.empty()) {
-        std::vector<int> take, skip;
-        int a = gates[rest[0]].target, b = -1;
-        if (generic(gates[rest[0]])) {
-            take.push_back(rest[0]);
-            skip.assign(rest.begin() + 1, rest.end());
-        } else {
-            for (int i : rest) {
-                const GateSpec &x = gates[i];
-                bool ok = !generic(x);
-                for (int j : skip)
-                    if (ok && !commute(gates[j], x)) ok = false;
-                if (ok && b < 0 && x.target != a && reg.dims[a] * reg.dims[x.target] <= kMaxPair) b = x.target;
-                (ok && (x.target == a || x.target == b) ? take : skip).push_back(i);
-            }
-        }
-        PassStage &S = p.st[p.nstages++];
-        S.g0 = (int32_t)order.size();
-        S.g1 = S.g0 + (int32_t)take.size();
-        if (generic(gates[take[0]])) {
-            S.da = 0;
-            S.db = 0;
-            axis_a.push_back(-1);
-            axis_b.push_back(-1);
-        } else {
-            if (b >= 0 && reg.dims[b] < reg.dims[a]) std::swap(a, b);      // axis 0 = smaller dimension
-            S.da = reg.dims[a];
-            S.db = b >= 0 ? reg.dims[b] : 1;
-            S.sta = (uint32_t)tile_stride(a);
-            S.stb = b >= 0 ? (uint32_t)tile_stride(b) : 0u;
-            // class enumeration: insert the axis digits in ascending stride order
-            uint32_t s1 = S.sta, d1 = (uint32_t)S.da, s2 = S.stb, d2 = (uint32_t)S.db;
-            if (b < 0) { s2 = 1; d2 = 1; }
-            else if (s2 < s1) { std::swap(s1, s2); std::swap(d1, d2); }
-            S.s1 = s1; S.m1 = make_fastdiv32(s1).m; S.d1 = d1;
-            S.s2 = s2; S.m2 = make_fastdiv32(s2).m; S.d2 = d2;
-            axis_a.push_back(a);
-            axis_b.push_back(b);
-        }
-        order.insert(order.end(), take.begin(), take.end());
-        rest.swap(skip);
-    }
     // gates
     int uoff = 0;
     *touched = 0.0;
-    p.ngates = (int32_t)order.size();
-    int stage_of[kMaxPassGates];
-    for (int k = 0; k < p.nstages; ++k)
-        for (int gi = p.st[k].g0; gi < p.st[k].g1; ++gi) stage_of[gi] = k;
-    for (size_t gi = 0; gi < order.size(); ++gi) {
-        const GateSpec &g = gates[order[gi]];
+    p.ngates = (int32_t)pp.gates.size();
+    for (size_t gi = 0; gi < pp.gates.size(); ++gi) {
+        const GateSpec &g = gates[pp.gates[gi]];
         GatePlan gp;
         std::string err;
         if (plan_gate(reg, g, false, &gp, &err) != SV_OK) return false;
         *touched += (double)gp.touched;
         PassGateP &q = p.g[gi];
-        const int sg = stage_of[gi];
-        const int ax_a = axis_a[sg], ax_b = axis_b[sg];
-        const bool gen = p.st[sg].da == 0;
-        const int t = g.target;
         q.d = gp.d;
-        q.kind = gp.kind;
+        q.kind = gp.kind == kGeneral ? kPGeneral : kPMonomial;
+        if (q.kind == kPMonomial) {            // every moving coefficient exactly 1: pure data movement
+            bool perm = true;
+            for (int j = 0; j < gp.d; ++j)
+                if (((gp.active >> j) & 1) && !(gp.U[j].x == 1.0 && gp.U[j].y == 0.0)) perm = false;
+            if (perm) q.kind = kPPerm;
+        }
         q.active = gp.active;
         for (int j = 0; j < kMaxDim; ++j) q.sigma[j] = (int8_t)(j < gp.d ? gp.sigma[j] : j);
-        q.st = (uint32_t)tile_stride(t);
-        q.mst = make_fastdiv32(q.st).m;
-        q.axis = (!gen && t == ax_b) ? 1 : 0;
-        q.axctl = -1;
-        // form: a cyclic shift with coefficients (X_{+s}, CINC, diagonal gates) or dense U
-        int shift = -1;
-        if (gp.kind == kMonomial) {
-            shift = (gp.sigma[0]) % gp.d;
-            for (int j = 0; j < gp.d; ++j)
-                if (gp.sigma[j] != (j + shift) % gp.d) shift = -1;
-        }
-        int need;
-        if (gen) {
-            need = gp.kind == kGeneral ? gp.d * gp.d : gp.d;
-            if (uoff + need > kPoolC) return false;
-            for (int k = 0; k < need; ++k) p.U[uoff + k] = gp.U[k];
-        } else if (shift >= 0) {
-            q.form = kFormShift;
-            q.shift = shift;
-            q.pure = 1;
-            need = gp.d;
-            if (uoff + need > kPoolC) return false;
-            for (int j = 0; j < gp.d; ++j) {
-                p.U[uoff + j] = gp.U[j];              // coefficient of member j
-                if (!(gp.U[j].x == 1.0 && gp.U[j].y == 0.0)) q.pure = 0;
-            }
-        } else {
-            q.form = kFormDense;
-            need = gp.d * gp.d;
-            if (uoff + need > kPoolC) return false;
-            for (int k = 0; k < need; ++k) p.U[uoff + k] = g.U[k];
-        }
+        const int need = gp.kind == kGeneral ? gp.d * gp.d : gp.d;
+        if (uoff + need > kPoolC) return false;
         q.uoff = uoff;
+        for (int k = 0; k < need; ++k) p.U[uoff + k] = gp.U[k];
         uoff += need;
         p.upool = uoff;
+        const int t = g.target;
+        if (g.span != 1 || (t >= m0 && std::find(pp.H.begin(), pp.H.end(), t) == pp.H.end())) return false;
+        const uint64_t st = (t < m0) ? reg.b[t] : W[t] * LT;
+        q.st = (uint32_t)st;
+        q.mst = make_fastdiv32(q.st).m;
         if ((int)g.ctrl.size() > kMaxPassCtrl) return false;
-        // a control on the stage's other axis selects lines; static in-tile controls become
-        // bit masks; the rest are decided at run time
+        // static in-tile controls become bit masks; the rest are decided at run time
         uint32_t *mm = p.mask[gi];
         for (uint64_t m = 0; m < M; ++m) mm[m >> 5] |= 1u << (m & 31);
         for (uint64_t l = 0; l < L; ++l) mm[4 + (l >> 5)] |= 1u << (l & 31);
@@ -192,10 +569,6 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
             const int c = g.ctrl[k].q;
             const uint32_t v = (uint32_t)g.ctrl[k].v;
             const uint64_t dc = (uint64_t)reg.dims[c];
-            if (!gen && (c == ax_a || c == ax_b)) {
-                q.axctl = (int32_t)v;
-                continue;
-            }
             if (std::find(pp.H.begin(), pp.H.end(), c) != pp.H.end()) {         // H digit: member mask
                 for (uint64_t m = 0; m < M; ++m)
                     if ((m / W[c]) % dc != v) mm[m >> 5] &= ~(1u << (m & 31));
@@ -232,10 +605,46 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
     return p.ntiles > 0;
 }
 
+template <int NT, int G>
+cudaError_t launch_pass_t(const PassParams &p, cudaStream_t st, const LaunchCfg &cfg) {
+    const int S = cfg.pass_stages, TE = cfg.pass_tile;
+    // size for the largest matrix pool so the attribute and the occupancy are set once per config
+    const size_t smem = (size_t)S * TE * sizeof(double2) + (size_t)kPoolC * sizeof(double2) +
+                        (size_t)kMaxPassGates * (kMaskWords + kMaxDim) * sizeof(uint32_t) +
+                        (size_t)S * sizeof(StageInfo) + (size_t)2 * S * sizeof(uint64_t);
+    static size_t configured = 0, occ_for = 0;
+    static int occ = 1;
+    if (configured < smem) {
+        cudaError_t e = cudaFuncSetAttribute(k_gate_pass<NT, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = smem;
+    }
+    if (occ_for != smem) {   // resident CTAs per SM at this smem size (persistent grid)
+        int o = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_gate_pass<NT, G>, NT + 32, smem) != cudaSuccess || o < 1) o = 1;
+        occ = o;
+        occ_for = smem;
+    }
+    const uint64_t cap = (uint64_t)cfg.num_sms * (uint64_t)occ;
+    const unsigned grid = (unsigned)(p.ntiles < cap ? p.ntiles : cap);
+    k_gate_pass<NT, G><<<grid, NT + 32, smem, st>>>(p, S, TE);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_pass(const PassParams &p, cudaStream_t st, const LaunchCfg &cfg) {
-    const int G = cfg.pass_groups >= 2 && cfg.pass_stages >= 2 ? 2 : 1;   // one stage per group at least
-    if (cfg.pass_threads >= 384) return G == 2 ? launch_pass_t<384, 2>(p, st, cfg) : launch_pass_t<384, 1>(p, st, cfg);
-    return G == 2 ? launch_pass_t<256, 2>(p, st, cfg) : launch_pass_t<256, 1>(p, st, cfg);
+    int G = cfg.pass_groups;                      // one stage per group at least
+    while (G > 1 && cfg.pass_stages < G) G /= 2;
+    if (cfg.pass_threads >= 512) {
+        if (G >= 4) return launch_pass_t<512, 4>(p, st, cfg);
+        if (G == 2) return launch_pass_t<512, 2>(p, st, cfg);
+        return launch_pass_t<512, 1>(p, st, cfg);
+    }
+    if (cfg.pass_threads >= 384) {
+        if (G >= 2) return launch_pass_t<384, 2>(p, st, cfg);
+        return launch_pass_t<384, 1>(p, st, cfg);
+    }
+    if (G >= 2) return launch_pass_t<256, 2>(p, st, cfg);
+    return launch_pass_t<256, 1>(p, st, cfg);
 }
 
 cudaError_t run_pass(const Register &reg, const std::vector<GateSpec> &gates, const PassPlan &pp, double2 *psi,

@@ -250,7 +250,7 @@ std::vector<GateSpec> merge_same_qudit(const std::vector<GateSpec> &in) {
 }
 
 // ------------------------------------------------------------------- multi-gate passes
-bool commute(const GateSpec &a, const GateSpec &b) {
+static bool commute(const GateSpec &a, const GateSpec &b) {
     if (a.target == b.target) return false;
     for (const auto &c : b.ctrl)
         if (c.q == a.target) return false;

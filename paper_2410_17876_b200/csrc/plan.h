@@ -49,10 +49,6 @@ sv_status plan_gate(const Register &reg, const GateSpec &g, bool check_unitary, 
 // into one gate of dimension <= 16.
 std::vector<GateSpec> fuse_gates(const Register &reg, const std::vector<GateSpec> &in);
 
-// Whether two single-qudit gates commute as operators: different targets and neither target
-// is a control of the other (sufficient, not necessary).
-bool commute(const GateSpec &a, const GateSpec &b);
-
 // Consecutive gates on the same target with identical controls -> one matrix product.
 std::vector<GateSpec> merge_same_qudit(const std::vector<GateSpec> &in);
 

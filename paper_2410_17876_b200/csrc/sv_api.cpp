@@ -493,11 +493,11 @@ sv_status sv_set_option(sv_handle h, int32_t option, int64_t value) {
             h->cfg.pass_stages = (int)value;
             return SV_OK;
         case SV_OPT_PASS_THREADS:
-            if (value != 256 && value != 384) return fail(SV_ERR_INVALID_ARG, "pass threads 256 or 384");
+            if (value != 256 && value != 384 && value != 512) return fail(SV_ERR_INVALID_ARG, "pass threads 256, 384 or 512");
             h->cfg.pass_threads = (int)value;
             return SV_OK;
         case SV_OPT_PASS_GROUPS:
-            if (value != 1 && value != 2) return fail(SV_ERR_INVALID_ARG, "pass groups 1 or 2");
+            if (value != 1 && value != 2 && value != 4) return fail(SV_ERR_INVALID_ARG, "pass groups 1, 2 or 4");
             h->cfg.pass_groups = (int)value;
             return SV_OK;
         case SV_OPT_PASS_GATES:

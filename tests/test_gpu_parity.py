@@ -359,7 +359,7 @@ def test_loopback_sharded_matches_single_state(P, nranks):
 
 
 # (compute threads, consumer groups, stages) of the pass kernel
-PASS_CFGS = [(256, 1, 2), (384, 1, 2), (384, 2, 2), (256, 2, 3), (384, 2, 3), (384, 2, 4)]
+PASS_CFGS = [(256, 1, 2), (384, 1, 2), (512, 1, 2), (384, 2, 2), (256, 2, 3), (384, 2, 3), (512, 2, 3), (512, 4, 4)]
 
 
 @pytest.mark.parametrize("pass_cfg", PASS_CFGS)
