@@ -97,11 +97,29 @@ class Clocks:
 
 def touched_total(dims, gates):
     """sum_g T_g from the library's host planner (no device work)."""
+    return circuit_work(dims, gates)[0]
+
+
+def circuit_work(dims, gates):
+    """Per circuit, from the library's host planner: sum_g T_g (touched amplitudes) and the
+    FP64 flops of the general gates (8 d flop per touched amplitude: a d x d complex matvec per
+    class); monomial gates (phase / permutation, §2.1-2.2) do at most 6 flop per
+    moved amplitude and are counted as data movement only."""
     import paper_2410_17876_b200 as P
-    tot = 0
+    T = 0
+    flops = 0
     for g in gates:
-        tot += int(P.plan_gate(dims, g.target, g.U, g.ctrl, g.vals).touched)
-    return tot
+        pl = P.plan_gate(dims, g.target, g.U, g.ctrl, g.vals)
+        T += int(pl.touched)
+        if int(pl.kind) == 0:
+            flops += 8 * int(pl.d) * int(pl.touched)
+    return T, flops
+
+
+# FP64 peak measured on this pool's B200 (tools/probes/fp64_probe.cu, profiles/r01/fp64_probe.jsonl:
+# DFMA 35.7 TFLOP/s, DMMA 37.1); shared memory: 128 B/clk/SM x 148 SMs at the SM clock
+FP64_TFLOPS = 35.7
+SMEM_B_PER_CLK_SM = 128
 
 
 def cpu_baseline(cfg: int, budget_s: float = 20.0):
@@ -109,7 +127,7 @@ def cpu_baseline(cfg: int, budget_s: float = 20.0):
     applied in order until ~budget_s of CPU time."""
     from oracle import blocksim as O2
     from sv_inputs import config_circuit
-    nq = {3: 7, 4: 5, 5: 4}.get(cfg, None)
+    nq = {3: 11, 4: 5, 5: 4}.get(cfg, None)        # ~10-20 s of O-2 work on 16 cores
     dims, gates = config_circuit(cfg, nqubits=nq)
     D = int(np.prod(dims))
     psi = np.zeros(D, dtype=np.complex128)
@@ -210,7 +228,7 @@ def main():
     fuse = not args.no_fuse
     block = args.block or (args.config in (1, 2, 3, 4) and not args.no_block)
     graph = args.graph or (args.config in (1, 2) and not args.no_graph)
-    T_step = touched_total(dims, gates)                       # global amplitude updates / step
+    T_step, F_step = circuit_work(dims, gates)               # global amplitude updates, flops / step
     D_total = int(np.prod(dims, dtype=object))
     nread = min(4096, D_total)
 
@@ -303,6 +321,20 @@ def main():
             traffic = None
 
     bpu = 32.0 if args.dtype == "c128" else 16.0      # bytes per amplitude update (read + write)
+    # The pass kernel's own roofline: per launch it must stream the state through HBM once,
+    # move 32 B per touched amplitude of each gate through shared memory and do the general
+    # gates' FP64 flops; the binding resource sets its lower-bound time.
+    pass_roofline = None
+    if block and prof.launches and world == 1 and args.dtype == "c128":
+        sm_hz = (clk.summary().get("sm_mhz") or 1965.0) * 1e6
+        per_launch = {"hbm": state_bytes_per_launch / (hbm * 1e9),
+                      "smem": bpu * T_step * args.steps / prof.launches / (SMEM_B_PER_CLK_SM * 148 * sm_hz),
+                      "fp64": F_step * args.steps / prof.launches / (FP64_TFLOPS * 1e12)}
+        b = max(per_launch, key=per_launch.get)
+        pass_roofline = {"bound": b, "lower_bound_ms_per_launch": {k: 1e3 * v for k, v in per_launch.items()},
+                         "ms_per_launch": ms_per_launch, "frac": 1e3 * per_launch[b] / ms_per_launch,
+                         "peaks": {"hbm_gbs": hbm, "fp64_tflops": FP64_TFLOPS,
+                                   "smem_bytes_per_clk_per_sm": SMEM_B_PER_CLK_SM, "sm_mhz": sm_hz / 1e6}}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -329,6 +361,7 @@ def main():
                          "state_bytes_per_launch": state_bytes_per_launch,
                          "state_gbs": state_gbs,
                          "launches_timed": int(prof.launches)},
+            "pass_roofline": pass_roofline,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
