@@ -8,8 +8,8 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libsv.so")
+CSRC = os.environ.get("SV_BUILD_CSRC") or os.path.join(HERE, "csrc")    # override: variant builds
+LIB = os.environ.get("SV_BUILD_OUT") or os.path.join(HERE, "libsv.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -40,7 +40,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     inc, nccl_lib = _nccl_paths()
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(os.path.dirname(LIB), "build") if os.environ.get("SV_BUILD_OUT") else os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
     common = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-Xcompiler", "-fvisibility=hidden", "-I", os.path.join(ROOT, "include"), "-I", inc,

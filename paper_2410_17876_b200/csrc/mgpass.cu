@@ -8,9 +8,10 @@
 // persistent grid, a producer warp and NT compute threads).  Between load and store the CTA
 // applies the pass's gates one after another in shared memory: each gate visits its
 // equivalence classes inside the tile — a target in H has smem stride
-// W_h * LT, a low target has stride b_t — and its controls are decided
-//   * per class from static bit masks: controls on H digits (a mask over the M members) and on
-//     low-prefix digits (a mask over the position modulo L = b_{m0}, identical in every tile);
+// W_h * LT, a low target has stride b_t — and its controls are handled
+//   * by enumeration for controls on H digits and low-prefix digits: their pinned values are
+//     inserted into the class index next to the target digit (the §2.4 satisfying set is a
+//     Cartesian product), so only firing classes are visited;
 //   * per class from the tile's run offset: controls on run digits above the low prefix;
 //   * once per tile: controls on digits outside the tile (the producer's fire bits).
 #include <cuda_runtime.h>
@@ -27,13 +28,13 @@ constexpr int kMaxPassGates = 24;
 constexpr int kMaxMembers = 128;
 constexpr int kPoolC = 768;
 constexpr int kMaxPassCtrl = 4;
-constexpr int kMaskWords = 4 + 16;   // member mask (128 bits) + low-position mask (L < 512 bits)
+constexpr int kMaxIns = 1 + kMaxPassCtrl;   // inserted in-tile digits: the target + pinned controls
 
 // in-pass gate kinds: general y = U x (§2.3), monomial y_{sigma(j)} = c_j x_j (§2.1-2.2),
 // and the pure permutation (every moving coefficient exactly 1: no arithmetic at all)
 enum PassKind : int32_t { kPGeneral = 0, kPMonomial = 1, kPPerm = 2 };
 
-// a control decided at run time (static in-tile controls live in the masks)
+// a control decided at run time (in-tile controls on H / low-prefix digits are enumerated)
 struct PassCtrl {
     int32_t cls;          // 1 = run digit above the low prefix (needs the tile's run offset), 2 = outside the tile
     uint32_t v;
@@ -44,12 +45,16 @@ struct PassCtrl {
     uint64_t md64;        // cls 2: magic for d
 };
 
-enum PassFlags : uint32_t { kFMemberMask = 1, kFLowMask = 2, kFRunCtrl = 4 };
+enum PassFlags : uint32_t { kFRunCtrl = 4 };
 
 struct PassGateP {
     int32_t d, kind, nctrl, uoff;
     uint32_t flags;       // PassFlags: which in-tile control checks the gate needs
     uint32_t st, mst;     // smem stride of the target (+ magic)
+    uint32_t ncls;        // classes per full tile: M LT / (d prod of the inserted control dims)
+    int32_t nins;         // digits inserted into the class index, ascending tile stride:
+    uint32_t ins_s[kMaxIns], ins_m[kMaxIns];    //   stride (+ magic)
+    uint32_t ins_sd[kMaxIns], ins_ps[kMaxIns];  //   stride * dim, pinned value * stride
     uint32_t active;      // monomial / permutation: members that move or scale
     int8_t sigma[kMaxDim];
     PassCtrl c[kMaxPassCtrl];
@@ -67,7 +72,6 @@ struct PassParams {
     int32_t upool;        // used entries of U (copied to shared memory at kernel start)
     uint64_t moff[kMaxMembers];
     PassGateP g[kMaxPassGates];
-    uint32_t mask[kMaxPassGates][kMaskWords];   // per gate: member mask, low-position mask
     double2 U[kPoolC];    // general: row-major d x d; monomial: coefficient per member
 };
 
@@ -167,17 +171,34 @@ __device__ __forceinline__ uint32_t tdiv(uint32_t x, uint32_t d, uint32_t m, uin
     return q;
 }
 
-// member-0 smem index of class c (c < ncls): classes of stride st are grouped d*st apart
-__device__ __forceinline__ uint32_t class_e0(uint32_t c, uint32_t st, uint32_t mst, uint32_t d) {
-    uint32_t off;
-    const uint32_t grp = tdiv(c, st, mst, off);
-    return grp * st * d + off;
+// member-0 tile index of class c (c < ncls): the target digit (value 0) and the pinned in-tile
+// control digits inserted into c in ascending stride order, e <- (e / s) s d + pin s + e mod s
+// (SURVEY.md §8 a3 inside the tile)
+struct Ins1 {            // one insertion, held in registers across a class loop
+    uint32_t s, m, sd, ps;
+};
+__device__ __forceinline__ Ins1 ins_at(const PassGateP &g, int i) {
+    return Ins1{g.ins_s[i], g.ins_m[i], g.ins_sd[i], g.ins_ps[i]};
+}
+__device__ __forceinline__ uint32_t insert1(uint32_t e, const Ins1 &a) {
+    uint32_t r;
+    const uint32_t q = tdiv(e, a.s, a.m, r);
+    return q * a.sd + a.ps + r;
+}
+// first insertion from registers (the common uncontrolled case has only it), further ones
+// (in-tile controls) from the parameter bank
+__device__ __forceinline__ uint32_t class_e0(uint32_t c, const PassGateP &g, const Ins1 &first, bool more) {
+    uint32_t e = insert1(c, first);
+    if (more) {
+#pragma unroll 1
+        for (int i = 1; i < g.nins; ++i) e = insert1(e, ins_at(g, i));
+    }
+    return e;
 }
 
 // What one gate needs to decide its classes inside the current tile.
 struct TileGate {
-    uint32_t LT, mLT, L, mL, len, flags;
-    const uint32_t *mask;       // shared memory: member mask words 0..3, low-position mask 4..19
+    uint32_t LT, mLT, len, flags;
     const uint32_t *lowoff;     // shared memory: run offsets of the run-digit controls
     const uint32_t *soff;       // shared memory: sigma(j) * st of a monomial gate
 };
@@ -185,12 +206,8 @@ struct TileGate {
 // whether class e0 exists (ragged last tile of a run) and its in-tile controls hold
 __device__ __forceinline__ bool class_ok(const TileGate &tg, const PassGateP &g, uint32_t e0) {
     uint32_t l;
-    const uint32_t m = tdiv(e0, tg.LT, tg.mLT, l);
-    // static masks are all ones where a gate has no such control: evaluated without branches
-    uint32_t lq;
-    tdiv(l, tg.L, tg.mL, lq);
-    const uint32_t bits = (tg.mask[m >> 5] >> (m & 31)) & (tg.mask[4 + (lq >> 5)] >> (lq & 31));
-    bool ok = (l < tg.len) & (bits & 1u);
+    tdiv(e0, tg.LT, tg.mLT, l);
+    bool ok = l < tg.len;
     if (tg.flags & kFRunCtrl) {
 #pragma unroll 1
         for (int k = 0; k < g.nctrl; ++k) {
@@ -210,14 +227,14 @@ __device__ __forceinline__ bool class_ok(const TileGate &tg, const PassGateP &g,
 // contiguous for strides >= 32): member-0 smem index and whether the class exists and fires.
 // Classes past ncls read index 0 and do not store.
 template <int K, int NT>
-__device__ __forceinline__ void class_batch(const TileGate &tg, const PassGateP &g, uint32_t c0, uint32_t ncls,
-                                            uint32_t D, bool needck, uint32_t (&e)[K], bool (&ok)[K]) {
-    const uint32_t st = g.st, mst = g.mst;
+__device__ __forceinline__ void class_batch(const TileGate &tg, const PassGateP &g, const Ins1 &first, bool more,
+                                            uint32_t c0, uint32_t ncls, bool needck, uint32_t (&e)[K],
+                                            bool (&ok)[K]) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const uint32_t c = c0 + (uint32_t)(k * NT);
         ok[k] = c < ncls;
-        e[k] = ok[k] ? class_e0(c, st, mst, D) : 0u;
+        e[k] = ok[k] ? class_e0(c, g, first, more) : 0u;
         if (needck && ok[k]) ok[k] = class_ok(tg, g, e[k]);
     }
 }
@@ -238,11 +255,13 @@ __device__ __forceinline__ void gate_tile_general(const TileGate &tg, const Pass
                                                   const double2 *__restrict__ U, uint32_t cbeg, uint32_t cend,
                                                   uint32_t ncls, bool needck, int tid) {
     const uint32_t st = g.st;
+    const Ins1 first = ins_at(g, 0);
+    const bool more = g.nins > 1;
 #pragma unroll 1
     for (uint32_t c0 = cbeg + (uint32_t)tid; c0 < cend; c0 += (uint32_t)(NT * K)) {
         uint32_t e[K];
         bool ok[K];
-        class_batch<K, NT>(tg, g, c0, ncls, (uint32_t)D, needck, e, ok);
+        class_batch<K, NT>(tg, g, first, more, c0, ncls, needck, e, ok);
         const double2 *__restrict__ Ui = U + opaque_zero(c0);
         double2 x[K][D];
 #pragma unroll
@@ -277,6 +296,8 @@ __device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const Pas
                                                    uint32_t ncls, bool needck, int tid) {
     const uint32_t st = g.st;
     const uint32_t act = g.active;
+    const Ins1 first = ins_at(g, 0);
+    const bool more = g.nins > 1;
     // destination offsets sigma(j) * st, read once from shared memory: the stores below may
     // alias that table as far as the compiler knows, so it keeps them in registers instead of
     // re-reading the parameter bank inside the loop
@@ -287,7 +308,7 @@ __device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const Pas
     for (uint32_t c0 = cbeg + (uint32_t)tid; c0 < cend; c0 += (uint32_t)(NT * K)) {
         uint32_t e[K];
         bool ok[K];
-        class_batch<K, NT>(tg, g, c0, ncls, (uint32_t)D, needck, e, ok);
+        class_batch<K, NT>(tg, g, first, more, c0, ncls, needck, e, ok);
         double2 x[K][D];
 #pragma unroll
         for (int j = 0; j < D; ++j) {
@@ -318,7 +339,7 @@ __device__ __noinline__ void gate_tile_generic(const TileGate tg, const PassGate
                                                const double2 *U, uint32_t ncls, bool needck, int tid, int nt) {
     const int d = g.d;
     for (uint32_t c = tid; c < ncls; c += nt) {
-        const uint32_t e0 = class_e0(c, g.st, g.mst, (uint32_t)d);
+        const uint32_t e0 = class_e0(c, g, ins_at(g, 0), true);
         if (needck && !class_ok(tg, g, e0)) continue;
         double2 x[kMaxDim];
         if (g.kind == kPGeneral) {
@@ -387,8 +408,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant_
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double2 *bufs = reinterpret_cast<double2 *>(smem_raw);
     double2 *Us = bufs + (size_t)S * TE;                       // the pass's matrices
-    uint32_t *masks = reinterpret_cast<uint32_t *>(Us + p.upool);
-    uint32_t *soffs = masks + kMaxPassGates * kMaskWords;     // per gate: sigma(j) * st
+    uint32_t *soffs = reinterpret_cast<uint32_t *>(Us + p.upool);   // per gate: sigma(j) * st
     StageInfo *sinfo = reinterpret_cast<StageInfo *>(soffs + kMaxPassGates * kMaxDim);
     uint64_t *full = reinterpret_cast<uint64_t *>(sinfo + S);
     uint64_t *done = full + S;
@@ -398,7 +418,6 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant_
         fence_mbar_init();
     }
     for (int k = tid; k < p.upool; k += NT + 32) Us[k] = p.U[k];
-    for (int k = tid; k < p.ngates * kMaskWords; k += NT + 32) masks[k] = (&p.mask[0][0])[k];
     for (int k = tid; k < p.ngates * kMaxDim; k += NT + 32)
         soffs[k] = (uint32_t)p.g[k / kMaxDim].sigma[k % kMaxDim] * p.g[k / kMaxDim].st;
     __syncthreads();
@@ -430,7 +449,6 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant_
     }
 
     // ---------------- compute warps
-    const uint32_t slots = (uint32_t)p.M * p.LT;
     const int grp = tid / NTG, gtid = tid % NTG;
     for (uint64_t i = (uint64_t)grp; i < my; i += (uint64_t)G) {
         const int s = (int)(i % (uint64_t)S);
@@ -445,21 +463,18 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant_
             TileGate tg;
             tg.LT = p.LT;
             tg.mLT = p.mLT;
-            tg.L = p.L;
-            tg.mL = p.mL;
             tg.len = len;
             tg.flags = g.flags;
-            tg.mask = masks + gi * kMaskWords;
             tg.lowoff = si.lowoff[gi];
             tg.soff = soffs + gi * kMaxDim;
             const bool needck = g.flags != 0 || len < p.LT;
             const double2 *U = Us + g.uoff;
             switch (g.d) {
-                case 2: apply_gate_tile<2, NT, NTG>(tg, g, buf, U, slots / 2, needck, gtid); break;
-                case 3: apply_gate_tile<3, NT, NTG>(tg, g, buf, U, slots / 3, needck, gtid); break;
-                case 4: apply_gate_tile<4, NT, NTG>(tg, g, buf, U, slots / 4, needck, gtid); break;
-                case 5: apply_gate_tile<5, NT, NTG>(tg, g, buf, U, slots / 5, needck, gtid); break;
-                default: gate_tile_generic(tg, g, buf, U, slots / (uint32_t)g.d, needck, gtid, NTG); break;
+                case 2: apply_gate_tile<2, NT, NTG>(tg, g, buf, U, g.ncls, needck, gtid); break;
+                case 3: apply_gate_tile<3, NT, NTG>(tg, g, buf, U, g.ncls, needck, gtid); break;
+                case 4: apply_gate_tile<4, NT, NTG>(tg, g, buf, U, g.ncls, needck, gtid); break;
+                case 5: apply_gate_tile<5, NT, NTG>(tg, g, buf, U, g.ncls, needck, gtid); break;
+                default: gate_tile_generic(tg, g, buf, U, g.ncls, needck, gtid, NTG); break;
             }
             compute_barrier(1 + grp, NTG);
         }
@@ -478,7 +493,6 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
     p.psi = psi;
     const int m0 = pp.m0;
     const uint64_t L = (m0 < reg.n) ? reg.b[m0] : reg.D;
-    if (L > 32u * (kMaskWords - 4)) return false;          // low-position mask capacity
     p.L = (uint32_t)L;
     p.mL = make_fastdiv32(p.L).m;
     uint64_t M = 1;
@@ -560,25 +574,20 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
         q.st = (uint32_t)st;
         q.mst = make_fastdiv32(q.st).m;
         if ((int)g.ctrl.size() > kMaxPassCtrl) return false;
-        // static in-tile controls become bit masks; the rest are decided at run time
-        uint32_t *mm = p.mask[gi];
-        for (uint64_t m = 0; m < M; ++m) mm[m >> 5] |= 1u << (m & 31);
-        for (uint64_t l = 0; l < L; ++l) mm[4 + (l >> 5)] |= 1u << (l & 31);
+        // in-tile controls on H / low-prefix digits are inserted into the class index with
+        // their pinned values (only firing classes are visited); the rest are decided at run time
+        struct Ins { uint64_t s; uint32_t d, pin; };
+        std::vector<Ins> ins{{st, (uint32_t)gp.d, 0u}};
+        uint64_t cls_div = (uint64_t)gp.d;
         int nc = 0;
         for (size_t k = 0; k < g.ctrl.size(); ++k) {
             const int c = g.ctrl[k].q;
             const uint32_t v = (uint32_t)g.ctrl[k].v;
             const uint64_t dc = (uint64_t)reg.dims[c];
-            if (std::find(pp.H.begin(), pp.H.end(), c) != pp.H.end()) {         // H digit: member mask
-                for (uint64_t m = 0; m < M; ++m)
-                    if ((m / W[c]) % dc != v) mm[m >> 5] &= ~(1u << (m & 31));
-                q.flags |= kFMemberMask;
-                continue;
-            }
-            if (c < m0) {                      // low-prefix digit: position mask modulo L
-                for (uint64_t l = 0; l < L; ++l)
-                    if ((l / reg.b[c]) % dc != v) mm[4 + (l >> 5)] &= ~(1u << (l & 31));
-                q.flags |= kFLowMask;
+            const bool inH = std::find(pp.H.begin(), pp.H.end(), c) != pp.H.end();
+            if (inH || c < m0) {
+                ins.push_back({inH ? W[c] * LT : reg.b[c], (uint32_t)dc, v});
+                cls_div *= dc;
                 continue;
             }
             PassCtrl &cc = q.c[nc++];
@@ -601,6 +610,15 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
             }
         }
         q.nctrl = nc;
+        std::sort(ins.begin(), ins.end(), [](const Ins &a, const Ins &b) { return a.s < b.s; });
+        q.nins = (int32_t)ins.size();
+        for (size_t i = 0; i < ins.size(); ++i) {
+            q.ins_s[i] = (uint32_t)ins[i].s;
+            q.ins_m[i] = make_fastdiv32(q.ins_s[i]).m;
+            q.ins_sd[i] = (uint32_t)(ins[i].s * ins[i].d);
+            q.ins_ps[i] = (uint32_t)(ins[i].s * ins[i].pin);
+        }
+        q.ncls = (uint32_t)((uint64_t)M * LT / cls_div);
     }
     return p.ntiles > 0;
 }
@@ -610,7 +628,7 @@ cudaError_t launch_pass_t(const PassParams &p, cudaStream_t st, const LaunchCfg 
     const int S = cfg.pass_stages, TE = cfg.pass_tile;
     // size for the largest matrix pool so the attribute and the occupancy are set once per config
     const size_t smem = (size_t)S * TE * sizeof(double2) + (size_t)kPoolC * sizeof(double2) +
-                        (size_t)kMaxPassGates * (kMaskWords + kMaxDim) * sizeof(uint32_t) +
+                        (size_t)kMaxPassGates * kMaxDim * sizeof(uint32_t) +
                         (size_t)S * sizeof(StageInfo) + (size_t)2 * S * sizeof(uint64_t);
     static size_t configured = 0, occ_for = 0;
     static int occ = 1;

@@ -61,7 +61,7 @@ void default_cfg(LaunchCfg &c, int device) {
     c.num_sms = sms;
     c.pass_tile = 4096;        // measured best on c2-c4 (profiles/r01/passbench_*_groups.jsonl)
     c.pass_stages = 3;
-    c.pass_threads = 384;
+    c.pass_threads = 512;
     c.pass_gates = 24;
     c.pass_groups = 2;         // two consumer groups ping-pong over tiles
 }

@@ -12,7 +12,8 @@ from typing import Iterable, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsv.so")
+# SV_LIB_PATH: an alternative in-tree build (A/B kernel experiments, tools/build_variant.py)
+LIB_PATH = os.environ.get("SV_LIB_PATH") or os.path.join(_HERE, "libsv.so")
 
 SV_C128, SV_C64 = 0, 1
 SV_FUSE, SV_NO_CHECK, SV_GRAPH, SV_BLOCK = 1, 2, 4, 8
