@@ -453,6 +453,13 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant_
     for (uint64_t i = (uint64_t)grp; i < my; i += (uint64_t)G) {
         const int s = (int)(i % (uint64_t)S);
         double2 *buf = bufs + (size_t)s * TE;
+        // With several groups, consecutive tiles of a stage belong to different groups, so this
+        // group may reach tile i while the stage's previous tile (i - S, another group) is not
+        // even loaded: full[s] would still be in the phase before the one awaited, and a parity
+        // wait cannot tell a phase two steps back from a completed one.  Waiting first for
+        // tile i - S to be consumed (done[s], whose previous phase this group completed itself)
+        // puts full[s] exactly one phase before tile i.
+        if (G > 1 && i >= (uint64_t)S) mbar_wait(&done[s], (uint32_t)(((i - (uint64_t)S) / (uint64_t)S) & 1));
         mbar_wait(&full[s], (uint32_t)((i / (uint64_t)S) & 1));
         const StageInfo &si = sinfo[s];
         const uint32_t len = si.ti.len;

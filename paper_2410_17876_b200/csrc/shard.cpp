@@ -239,24 +239,44 @@ sv_status shard_apply(sv_handle h, const GateSpec &g, bool check_unitary) {
 }
 
 sv_status shard_apply_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_t flags) {
-    // Runs of purely local gates (no sharded target or control) go through the local circuit
-    // driver on every slice this handle owns (fusion / multi-gate passes included).
-    std::vector<GateSpec> run;
+    // Runs of gates with a local target go through the local circuit driver on every slice
+    // this handle owns (fusion / multi-gate passes included).  Controls on sharded digits are
+    // a rank predicate (rule ii): per slice, the gate is dropped when its rank fails them and
+    // kept without them otherwise, so they do not break the run.
+    const std::vector<int> ranks = ranks_of(h->shard);
+    const int first_sh = h->local.n;
+    std::vector<std::vector<GateSpec>> runs(ranks.size());
+    bool any = false;
     auto flush = [&]() -> sv_status {
-        if (run.empty()) return SV_OK;
+        if (!any) return SV_OK;
         const uint32_t local_flags = flags & (SV_FUSE | SV_BLOCK);
-        for (int r : ranks_of(h->shard)) {
-            std::vector<GateSpec> copy = run;
-            sv_status s = run_local_circuit(h, copy, local_flags, slice_of(h->shard, r));
+        for (size_t i = 0; i < ranks.size(); ++i) {
+            if (runs[i].empty()) continue;
+            sv_status s = run_local_circuit(h, runs[i], local_flags, slice_of(h->shard, ranks[i]));
             if (s != SV_OK) return s;
+            runs[i].clear();
         }
-        run.clear();
+        any = false;
         return SV_OK;
     };
     for (const GateSpec &g : specs) {
-        bool local = g.target < h->local.n;
-        for (const auto &c : g.ctrl) local = local && c.q < h->local.n;
-        if (local) { run.push_back(g); continue; }
+        if (g.target < first_sh) {
+            for (size_t i = 0; i < ranks.size(); ++i) {
+                GateSpec lg = g;
+                lg.ctrl.clear();
+                bool fires = true;
+                for (const auto &c : g.ctrl) {
+                    if (c.q < first_sh) { lg.ctrl.push_back(c); continue; }
+                    const int bit = (ranks[i] >> (c.q - first_sh)) & 1;   // rank bit j = digit of q_{n-s+j}
+                    if (bit != c.v) fires = false;
+                }
+                if (fires) {
+                    runs[i].push_back(std::move(lg));
+                    any = true;
+                }
+            }
+            continue;
+        }
         sv_status s = flush();
         if (s != SV_OK) return s;
         s = shard_apply(h, g, false);

@@ -423,3 +423,35 @@ def test_graph_cache_replays_same_circuit_and_recaptures_changes(P):
         st.reset(0)
         st.apply_circuit(changed, graph=True)
         assert np.max(np.abs(st.amplitudes() - O2.run(dims, changed))) <= 1e-10
+
+
+def test_pass_groups_stage_reuse_regression(P):
+    """Two consumer groups share the pass kernel's stage ring; a group that finishes a cheap tile
+    must not start on a stage whose previous tile (the other group's) has not been loaded yet.
+    Found as a hang (or silently wrong tiles) on a c4-shaped register with a pass whose tiles are
+    cheap: gates with an in-tile low control and with an out-of-tile control on the same qutrit.
+    Both consumer-group settings must give bit-identical states (the per-class arithmetic is the
+    same); the single-group path is pinned by the rest of this file."""
+    from sv_inputs import config_dims
+    dims = config_dims(4, nqubits=6)
+    _, gates7 = config_circuit(4, nqubits=7)
+    gates = [gates7[179], gates7[181], gates7[179], gates7[181]]
+    assert all(g.target < len(dims) and all(c < len(dims) for c in g.ctrl) for g in gates)
+    D = int(np.prod(dims, dtype=object))
+    states = []
+    try:
+        for groups in (1, 2):
+            st = P.State(dims)
+            states.append(st)
+            st.set_option(P.sv.SV_OPT_PASS_GROUPS, groups)
+            st.set_option(P.sv.SV_OPT_PASS_STAGES, 3)
+            st.set_amplitudes(0, labelled_state(0, 1 << 20))       # non-zero, exact values
+            st.apply_circuit(gates, check=False, block=True)
+            st.sync()
+        chunk = 1 << 24
+        for first in range(0, D, chunk):
+            n = min(chunk, D - first)
+            assert np.array_equal(states[0].amplitudes(first, n), states[1].amplitudes(first, n)), first
+    finally:
+        for st in states:
+            st.close()
