@@ -127,7 +127,7 @@ def cpu_baseline(cfg: int, budget_s: float = 20.0):
     applied in order until ~budget_s of CPU time."""
     from oracle import blocksim as O2
     from sv_inputs import config_circuit
-    nq = {3: 11, 4: 5, 5: 4}.get(cfg, None)        # ~10-20 s of O-2 work on 16 cores
+    nq = {3: 12, 4: 5, 5: 4}.get(cfg, None)        # ~10-20 s of O-2 work on 16 cores
     dims, gates = config_circuit(cfg, nqubits=nq)
     D = int(np.prod(dims))
     psi = np.zeros(D, dtype=np.complex128)
