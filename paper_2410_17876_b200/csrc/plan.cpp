@@ -250,6 +250,34 @@ std::vector<GateSpec> merge_same_qudit(const std::vector<GateSpec> &in) {
 }
 
 // ------------------------------------------------------------------- multi-gate passes
+static bool commute(const GateSpec &a, const GateSpec &b);
+
+// Commutation-aware merging: a gate joins the latest earlier gate with the same target and the
+// same controls when every gate in between commutes with it (it can be moved back next to that
+// gate, where the two are one matrix product, later gate on the left).  The window bounds the
+// backward scan.
+std::vector<GateSpec> merge_commuting(const std::vector<GateSpec> &in, int window) {
+    std::vector<GateSpec> out;
+    out.reserve(in.size());
+    for (const GateSpec &g : in) {
+        bool merged = false;
+        if (g.span == 1) {
+            const int lo = (int)out.size() - window < 0 ? 0 : (int)out.size() - window;
+            for (int j = (int)out.size() - 1; j >= lo; --j) {
+                GateSpec &h = out[j];
+                if (h.span == 1 && h.target == g.target && same_ctrl(h.ctrl, g.ctrl)) {
+                    h.U = matmul(g.U, h.U, g.d);
+                    merged = true;
+                    break;
+                }
+                if (!commute(h, g)) break;
+            }
+        }
+        if (!merged) out.push_back(g);
+    }
+    return out;
+}
+
 static bool commute(const GateSpec &a, const GateSpec &b) {
     if (a.target == b.target) return false;
     for (const auto &c : b.ctrl)

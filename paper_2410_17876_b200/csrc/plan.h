@@ -52,6 +52,10 @@ std::vector<GateSpec> fuse_gates(const Register &reg, const std::vector<GateSpec
 // Consecutive gates on the same target with identical controls -> one matrix product.
 std::vector<GateSpec> merge_same_qudit(const std::vector<GateSpec> &in);
 
+// Commutation-aware merging of same-target, same-control gates across gates that commute with
+// the later one (a superset of merge_same_qudit); used before multi-gate pass planning.
+std::vector<GateSpec> merge_commuting(const std::vector<GateSpec> &in, int window);
+
 // Multi-gate cache-blocked passes.  A pass applies several gates to every
 // tile of the state while the tile sits in shared memory: the tile holds all digit values of
 // a set Q of "in-tile" qudits (the low prefix q_0..q_{m0-1} whose stride is < 32 is always

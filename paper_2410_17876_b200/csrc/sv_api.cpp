@@ -234,7 +234,7 @@ sv_status run_local_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_t 
     std::vector<PassPlan> passes;
     if ((flags & SV_BLOCK) && h->c64) flags = (flags & ~SV_BLOCK) | SV_FUSE;   // pass kernel: c128 only
     if (flags & SV_BLOCK) {
-        specs = merge_same_qudit(specs);
+        specs = merge_commuting(specs, 64);
         passes = plan_passes(h->local, specs, (uint64_t)h->cfg.pass_tile, h->cfg.pass_gates, 64);
     } else {
         if (flags & SV_FUSE) specs = fuse_gates(h->local, specs);
