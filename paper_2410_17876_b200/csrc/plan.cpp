@@ -278,12 +278,35 @@ std::vector<GateSpec> merge_commuting(const std::vector<GateSpec> &in, int windo
     return out;
 }
 
+// Whether the gate's matrix is diagonal (§2.1 phase gates): every off-diagonal entry exactly 0.
+static bool is_diag(const GateSpec &g) {
+    for (int i = 0; i < g.d; ++i)
+        for (int j = 0; j < g.d; ++j)
+            if (i != j && (g.U[i * g.d + j].x != 0.0 || g.U[i * g.d + j].y != 0.0)) return false;
+    return true;
+}
+
+// Sufficient commutation test for two (controlled) single-qudit gates, as operators on the
+// register: gates on different digits commute unless one's target is a control of the other
+// and that target gate is not diagonal (a diagonal gate on a digit commutes with everything
+// that is block-diagonal in that digit, i.e. with any gate merely controlled on it); two gates
+// on the same digit commute when both are diagonal.
 static bool commute(const GateSpec &a, const GateSpec &b) {
-    if (a.target == b.target) return false;
+    if (a.span != 1 || b.span != 1) {            // fused spans: plain disjointness of the digits
+        auto in = [](int q, const GateSpec &g) { return q >= g.target && q < g.target + g.span; };
+        for (int k = 0; k < a.span; ++k)
+            if (in(a.target + k, b)) return false;
+        for (const auto &c : b.ctrl)
+            if (in(c.q, a)) return false;
+        for (const auto &c : a.ctrl)
+            if (in(c.q, b)) return false;
+        return true;
+    }
+    if (a.target == b.target) return is_diag(a) && is_diag(b);
     for (const auto &c : b.ctrl)
-        if (c.q == a.target) return false;
+        if (c.q == a.target && !is_diag(a)) return false;
     for (const auto &c : a.ctrl)
-        if (c.q == b.target) return false;
+        if (c.q == b.target && !is_diag(b)) return false;
     return true;
 }
 
