@@ -24,7 +24,7 @@
 
 namespace svi {
 
-constexpr int kMaxPassGates = 24;
+constexpr int kMaxPassGates = 32;            // fire bits: one 32-bit ballot
 constexpr int kMaxMembers = 128;
 constexpr int kPoolC = 768;
 constexpr int kMaxPassCtrl = 4;
@@ -74,6 +74,8 @@ struct PassParams {
     PassGateP g[kMaxPassGates];
     double2 U[kPoolC];    // general: row-major d x d; monomial: coefficient per member
 };
+
+static_assert(sizeof(PassParams) <= 32764, "kernel parameter space (32 KB on sm_100)");
 
 namespace {
 

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--threads", default="512,256")
     ap.add_argument("--gates", default="24,8,4,2")
     ap.add_argument("--groups", default="1")
+    ap.add_argument("--windows", default="64")
     ap.add_argument("--reps", type=int, default=1)
     args = ap.parse_args()
     import torch
@@ -35,11 +36,12 @@ def main():
     ext = torch.cuda.ExternalStream(st.info().cuda_stream)
     ga = P.sv._GateArray(gates)
     cases = [("noblock", 0, 0, 0, 0)]
-    for te, s, nt, ng, gr in itertools.product(*[[int(x) for x in a.split(",")] for a in
-                                                 (args.tiles, args.stages, args.threads, args.gates, args.groups)]):
+    for te, s, nt, ng, gr, wi in itertools.product(*[[int(x) for x in a.split(",")] for a in
+                                                     (args.tiles, args.stages, args.threads, args.gates, args.groups,
+                                                      args.windows)]):
         if te * 16 * s > 210 * 1024 or s < gr:
             continue
-        cases.append(("block", te, s, nt, ng, gr))
+        cases.append(("block", te, s, nt, ng, gr, wi))
     for kind, te, s, nt, ng, *rest in cases:
         block = kind == "block"
         if block:
@@ -48,6 +50,7 @@ def main():
             st.set_option(P.sv.SV_OPT_PASS_THREADS, nt)
             st.set_option(P.sv.SV_OPT_PASS_GATES, ng)
             st.set_option(P.sv.SV_OPT_PASS_GROUPS, rest[0])
+            st.set_option(P.sv.SV_OPT_PASS_WINDOW, rest[1])
         st.reset(0)
         st.apply_circuit(ga, fuse=True, check=False, block=block)
         st.sync()
@@ -62,7 +65,7 @@ def main():
         ms = e0.elapsed_time(e1) / args.reps
         launches = (st.info().kernel_launches - n0) // args.reps
         print(json.dumps({"config": args.config, "D": D, "gates": len(gates), "mode": kind, "tile": te,
-                          "stages": s, "threads": nt, "groups": rest[0] if rest else 0, "max_gates": ng, "ms": ms, "launches": launches,
+                          "stages": s, "threads": nt, "groups": rest[0] if rest else 0, "window": rest[1] if rest else 0, "max_gates": ng, "ms": ms, "launches": launches,
                           "updates_per_s": T / (ms / 1e3), "equiv_GBps": 32.0 * T / (ms / 1e3) / 1e9,
                           "pass_GBps": 32.0 * D * launches / (ms / 1e3) / 1e9}), flush=True)
     st.close()
