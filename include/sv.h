@@ -234,6 +234,18 @@ SV_API sv_status sv_fuse_plan(const int32_t *dims, int32_t n, const sv_gate *gat
                        int32_t *out_nctrl, int32_t *out_ctrl, int32_t *out_vals,
                        double *out_U, int64_t *out_n);
 
+/* Host-only: the SV_BLOCK pre-pass that merges gates (PAPER.md:256 applies gates one at a time;
+ * merging is this build's addition): each gate joins the latest earlier gate with the same
+ * target and the same controls when every gate in between commutes with it (different digits
+ * and neither target a control of the other unless that target gate is diagonal, or both on one
+ * digit and both diagonal), looking back at most `window` gates; merged matrices are products
+ * (later gate on the left).  Output layout as sv_fuse_plan (out_span[i] = 1).  Errors as
+ * sv_fuse_plan, plus SV_ERR_INVALID_ARG for window < 1. */
+SV_API sv_status sv_merge_plan(const int32_t *dims, int32_t n, const sv_gate *gates, int64_t ngates,
+                               int32_t window, int32_t *out_target, int32_t *out_span, int32_t *out_dim,
+                               int32_t *out_nctrl, int32_t *out_ctrl, int32_t *out_vals,
+                               double *out_U, int64_t *out_n);
+
 /* Host-only: run the SV_BLOCK pass planner (without same-qudit merging) on a gate list.
  * out_order[i] = index of the i-th gate in application order; out_pass[i] = its pass id;
  * out_tile[p] = amplitudes per shared-memory tile of pass p (room for ngates entries);

@@ -590,9 +590,13 @@ sv_status sv_enumerate_fibres(const int32_t *dims, int32_t n, int32_t target, co
     return SV_OK;
 }
 
-sv_status sv_fuse_plan(const int32_t *dims, int32_t n, const sv_gate *gates, int64_t ngates,
-                       int32_t *out_target, int32_t *out_span, int32_t *out_dim, int32_t *out_nctrl,
-                       int32_t *out_ctrl, int32_t *out_vals, double *out_U, int64_t *out_n) {
+}  // extern "C"
+
+template <class Planner>
+static sv_status host_gate_plan(const int32_t *dims, int32_t n, const sv_gate *gates, int64_t ngates,
+                                int32_t *out_target, int32_t *out_span, int32_t *out_dim, int32_t *out_nctrl,
+                                int32_t *out_ctrl, int32_t *out_vals, double *out_U, int64_t *out_n,
+                                Planner plan) {
     Register reg;
     sv_status s = make_register(dims, n, &reg, &g_err);
     if (s != SV_OK) return s;
@@ -604,7 +608,7 @@ sv_status sv_fuse_plan(const int32_t *dims, int32_t n, const sv_gate *gates, int
         if (s != SV_OK) return s;
         specs.push_back(make_spec(reg, g.target, g.ctrl, g.ctrl_vals, g.nctrl, g.U));
     }
-    std::vector<GateSpec> f = fuse_gates(reg, specs);
+    std::vector<GateSpec> f = plan(reg, specs);
     int64_t co = 0;
     for (size_t i = 0; i < f.size(); ++i) {
         out_target[i] = f[i].target;
@@ -619,6 +623,24 @@ sv_status sv_fuse_plan(const int32_t *dims, int32_t n, const sv_gate *gates, int
     }
     *out_n = (int64_t)f.size();
     return SV_OK;
+}
+
+extern "C" {
+
+sv_status sv_fuse_plan(const int32_t *dims, int32_t n, const sv_gate *gates, int64_t ngates,
+                       int32_t *out_target, int32_t *out_span, int32_t *out_dim, int32_t *out_nctrl,
+                       int32_t *out_ctrl, int32_t *out_vals, double *out_U, int64_t *out_n) {
+    return host_gate_plan(dims, n, gates, ngates, out_target, out_span, out_dim, out_nctrl, out_ctrl, out_vals,
+                          out_U, out_n, [](const Register &r, const std::vector<GateSpec> &g) { return fuse_gates(r, g); });
+}
+
+sv_status sv_merge_plan(const int32_t *dims, int32_t n, const sv_gate *gates, int64_t ngates, int32_t window,
+                        int32_t *out_target, int32_t *out_span, int32_t *out_dim, int32_t *out_nctrl,
+                        int32_t *out_ctrl, int32_t *out_vals, double *out_U, int64_t *out_n) {
+    if (window < 1) return fail(SV_ERR_INVALID_ARG, "window >= 1");
+    return host_gate_plan(dims, n, gates, ngates, out_target, out_span, out_dim, out_nctrl, out_ctrl, out_vals,
+                          out_U, out_n,
+                          [window](const Register &, const std::vector<GateSpec> &g) { return merge_commuting(g, window); });
 }
 
 sv_status sv_block_plan(const int32_t *dims, int32_t n, const sv_gate *gates, int64_t ngates,

@@ -97,6 +97,8 @@ _sig("sv_enumerate_fibres", [_i32p, C.c_int32, C.c_int32, _i32p, _i32p, C.c_int3
                              C.c_uint64, _u64p])
 _sig("sv_fuse_plan", [_i32p, C.c_int32, C.POINTER(sv_gate), C.c_int64, _i32p, _i32p, _i32p, _i32p,
                       _i32p, _i32p, _dp, C.POINTER(C.c_int64)])
+_sig("sv_merge_plan", [_i32p, C.c_int32, C.POINTER(sv_gate), C.c_int64, C.c_int32, _i32p, _i32p, _i32p, _i32p,
+                       _i32p, _i32p, _dp, C.POINTER(C.c_int64)])
 _sig("sv_shard_plan", [_i32p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _i32p, _i32p, C.c_int32,
                        _i32p, _i32p, _i32p])
 _sig("sv_version", [], C.c_char_p)
@@ -115,7 +117,7 @@ _sig("sv_block_plan", [_i32p, C.c_int32, C.POINTER(sv_gate), C.c_int64, C.c_int6
 EXPORTS = ["sv_create", "sv_create_ex", "sv_create_sharded", "sv_nccl_unique_id", "sv_destroy",
            "sv_reset", "sv_apply_gate", "sv_apply_circuit", "sv_amplitudes", "sv_set_amplitudes",
            "sv_norm", "sv_sync", "sv_last_error", "sv_get_info", "sv_set_option", "sv_plan_gate",
-           "sv_enumerate_fibres", "sv_fuse_plan", "sv_shard_plan", "sv_version", "sv_profile_read", "sv_block_plan",
+           "sv_enumerate_fibres", "sv_fuse_plan", "sv_merge_plan", "sv_shard_plan", "sv_version", "sv_profile_read", "sv_block_plan",
            "sv_sparse_create", "sv_sparse_destroy", "sv_sparse_reset", "sv_sparse_apply_gate",
            "sv_sparse_apply_circuit", "sv_sparse_nnz", "sv_sparse_entries", "sv_sparse_launches"]
 
@@ -289,8 +291,7 @@ def enumerate_fibres(dims, target, ctrl=(), vals=(), first: int = 0, count: int 
     return out[:int(count)]
 
 
-def fuse_plan(dims, gates):
-    """Host fusion planner: list of (target, span, dim, ctrl tuple, vals tuple, U ndarray)."""
+def _host_plan(fn, dims, gates, *extra):
     gates = list(gates)
     ga = _GateArray(gates)
     n = max(1, len(gates))
@@ -300,9 +301,8 @@ def fuse_plan(dims, gates):
     U = np.zeros(n * 512, np.float64)
     nout = C.c_int64()
     d = _i32(dims)
-    _check(_lib.sv_fuse_plan(d.ctypes.data_as(_i32p), d.size, ga.arr, ga.n, _p(t, _i32p), _p(sp, _i32p),
-                             _p(dm, _i32p), _p(nc, _i32p), _p(oc, _i32p), _p(ov, _i32p),
-                             U.ctypes.data_as(_dp), C.byref(nout)))
+    _check(fn(d.ctypes.data_as(_i32p), d.size, ga.arr, ga.n, *extra, _p(t, _i32p), _p(sp, _i32p),
+              _p(dm, _i32p), _p(nc, _i32p), _p(oc, _i32p), _p(ov, _i32p), U.ctypes.data_as(_dp), C.byref(nout)))
     res, co = [], 0
     for i in range(nout.value):
         k = int(dm[i])
@@ -311,6 +311,16 @@ def fuse_plan(dims, gates):
                     tuple(int(x) for x in ov[co:co + nc[i]]), u))
         co += int(nc[i])
     return res
+
+
+def fuse_plan(dims, gates):
+    """Host fusion planner: list of (target, span, dim, ctrl tuple, vals tuple, U ndarray)."""
+    return _host_plan(_lib.sv_fuse_plan, dims, gates)
+
+
+def merge_plan(dims, gates, window: int = 64):
+    """Host commutation-aware merge (the SV_BLOCK pre-pass): same output layout as fuse_plan."""
+    return _host_plan(_lib.sv_merge_plan, dims, gates, C.c_int32(int(window)))
 
 
 def block_plan(dims, gates, tile_cap: int = 4096):

@@ -218,3 +218,53 @@ def test_block_planner_reorders_only_commuting_gates():
         ref = O2.run(dims, gates, psi0)
         got = O2.run(dims, [gates[i] for i in order], psi0)
         assert np.max(np.abs(got - ref)) < 1e-12
+
+
+def test_merge_planner_preserves_the_circuit():
+    """The SV_BLOCK pre-pass (sv_merge_plan): gates move back across gates they commute with and
+    merge with an earlier same-target, same-control gate.  The merged list must give the same
+    state as the original (O-2), and must merge where the commutation rules allow it."""
+    from sv_inputs import t_gate, hadamard
+    rng = np.random.default_rng(41)
+    for s in range(30):
+        dims = [int(x) for x in rng.integers(2, 5, size=5)]
+        _, gates = random_circuit(700 + s, dims, 50, max_ctrl=2)
+        # diagonal gates and repeats so the diagonal rules and merges fire
+        extra = []
+        for g in gates:
+            extra.append(g)
+            r = rng.random()
+            if r < 0.25:
+                extra.append(Gate(g.target, (), (), np.diag(np.exp(1j * rng.random(dims[g.target])))))
+            elif r < 0.5:
+                extra.append(Gate(g.target, g.ctrl, g.vals, haar_unitary(dims[g.target], rng)))
+        gates = extra
+        merged = P.merge_plan(dims, gates, 64)
+        assert len(merged) < len(gates)
+        assert all(m[1] == 1 for m in merged)
+        psi0 = random_state(int(np.prod(dims)), 300 + s)
+        ref = O2.run(dims, gates, psi0)
+        got = psi0.copy()
+        for m in merged:
+            _merged_apply(got, dims, m)
+        assert np.max(np.abs(got - ref)) < 1e-13
+
+
+def test_merge_planner_commutation_rules():
+    """Closed cases: H on q0, CNOT(q1 -> q2), H on q0 merges (disjoint); T on q1 passes a gate
+    controlled on q1 (diagonal); a non-diagonal gate on q1 does not; same-digit diagonals commute."""
+    from sv_inputs import t_gate, hadamard, shift_x
+    dims = [2, 2, 2]
+    H, T, X = hadamard(), t_gate(), shift_x(2, 1)
+    cnot = Gate(2, (1,), (1,), X)
+    m = P.merge_plan(dims, [Gate(0, (), (), H), cnot, Gate(0, (), (), H)])
+    assert len(m) == 2 and np.allclose(m[0][5], np.eye(2))          # H H = I merged past the CNOT
+    m = P.merge_plan(dims, [Gate(1, (), (), T), cnot, Gate(1, (), (), T)])
+    assert len(m) == 2 and np.allclose(m[0][5], T @ T)              # T commutes with a control on q1
+    m = P.merge_plan(dims, [Gate(1, (), (), H), cnot, Gate(1, (), (), H)])
+    assert len(m) == 3                                              # H does not
+    Z = np.diag([1.0, -1.0]).astype(np.complex128)
+    m = P.merge_plan(dims, [Gate(1, (), (), T), Gate(1, (0,), (1,), Z), Gate(1, (), (), T)])
+    assert len(m) == 2                                              # diagonals on one digit commute
+    m = P.merge_plan(dims, [Gate(0, (), (), H), cnot, Gate(0, (), (), H)], window=1)
+    assert len(m) == 3                                              # the window bounds the scan
