@@ -28,7 +28,8 @@ constexpr int kMaxPassGates = 32;            // fire bits: one 32-bit ballot
 constexpr int kMaxMembers = 128;
 constexpr int kPoolC = 768;
 constexpr int kMaxPassCtrl = 4;
-constexpr int kMaxIns = 1 + kMaxPassCtrl;   // inserted in-tile digits: the target + pinned controls
+constexpr int kMaxIns = 2 + kMaxPassCtrl;   // inserted in-tile digits: the target(s) + pinned controls
+constexpr int kMaxPairDim = 4;             // pair gates: d_a d_b <= 4 (qubit pairs)
 
 // in-pass gate kinds: general y = U x (§2.3), monomial y_{sigma(j)} = c_j x_j (§2.1-2.2),
 // and the pure permutation (every moving coefficient exactly 1: no arithmetic at all)
@@ -72,6 +73,8 @@ struct PassParams {
     int32_t upool;        // used entries of U (copied to shared memory at kernel start)
     uint64_t moff[kMaxMembers];
     PassGateP g[kMaxPassGates];
+    uint32_t moff_t[kMaxPassGates][kMaxDim];   // per gate: tile offset of class member j
+    uint32_t soff_t[kMaxPassGates][kMaxDim];   // per gate: offset of member sigma(j) (monomial)
     double2 U[kPoolC];    // general: row-major d x d; monomial: coefficient per member
 };
 
@@ -202,7 +205,9 @@ __device__ __forceinline__ uint32_t class_e0(uint32_t c, const PassGateP &g, con
 struct TileGate {
     uint32_t LT, mLT, len, flags;
     const uint32_t *lowoff;     // shared memory: run offsets of the run-digit controls
-    const uint32_t *soff;       // shared memory: sigma(j) * st of a monomial gate
+    const uint32_t *moff;       // shared memory: tile offset of class member j (j st, or the
+                                //   two-digit offset of a pair gate)
+    const uint32_t *soff;       // shared memory: offset of member sigma(j) (monomial gates)
 };
 
 // whether class e0 exists (ragged last tile of a run) and its in-tile controls hold
@@ -256,7 +261,11 @@ template <int D, int K, int NT>
 __device__ __forceinline__ void gate_tile_general(const TileGate &tg, const PassGateP &g, double2 *__restrict__ buf,
                                                   const double2 *__restrict__ U, uint32_t cbeg, uint32_t cend,
                                                   uint32_t ncls, bool needck, int tid) {
-    const uint32_t st = g.st;
+    // member offsets, read once from shared memory (the stores below may alias that table as
+    // far as the compiler knows, so it keeps them in registers)
+    uint32_t mo[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) mo[j] = tg.moff[j];
     const Ins1 first = ins_at(g, 0);
     const bool more = g.nins > 1;
 #pragma unroll 1
@@ -269,7 +278,7 @@ __device__ __forceinline__ void gate_tile_general(const TileGate &tg, const Pass
 #pragma unroll
         for (int k = 0; k < K; ++k)
 #pragma unroll
-            for (int j = 0; j < D; ++j) x[k][j] = buf[e[k] + j * st];
+            for (int j = 0; j < D; ++j) x[k][j] = buf[e[k] + mo[j]];
 #pragma unroll
         for (int i = 0; i < D; ++i) {
             double2 acc[K];
@@ -283,7 +292,7 @@ __device__ __forceinline__ void gate_tile_general(const TileGate &tg, const Pass
             }
 #pragma unroll
             for (int k = 0; k < K; ++k)
-                if (ok[k]) buf[e[k] + i * st] = acc[k];
+                if (ok[k]) buf[e[k] + mo[i]] = acc[k];
         }
     }
 }
@@ -296,16 +305,18 @@ template <int D, int K, int NT, bool PERM>
 __device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const PassGateP &g, double2 *__restrict__ buf,
                                                    const double2 *__restrict__ U, uint32_t cbeg, uint32_t cend,
                                                    uint32_t ncls, bool needck, int tid) {
-    const uint32_t st = g.st;
     const uint32_t act = g.active;
     const Ins1 first = ins_at(g, 0);
     const bool more = g.nins > 1;
     // destination offsets sigma(j) * st, read once from shared memory: the stores below may
     // alias that table as far as the compiler knows, so it keeps them in registers instead of
     // re-reading the parameter bank inside the loop
-    uint32_t so[D];
+    uint32_t so[D], mo[D];
 #pragma unroll
-    for (int j = 0; j < D; ++j) so[j] = tg.soff[j];
+    for (int j = 0; j < D; ++j) {
+        so[j] = tg.soff[j];
+        mo[j] = tg.moff[j];
+    }
 #pragma unroll 1
     for (uint32_t c0 = cbeg + (uint32_t)tid; c0 < cend; c0 += (uint32_t)(NT * K)) {
         uint32_t e[K];
@@ -316,7 +327,7 @@ __device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const Pas
         for (int j = 0; j < D; ++j) {
             const bool aj = (act >> j) & 1;
 #pragma unroll
-            for (int k = 0; k < K; ++k) x[k][j] = aj ? buf[e[k] + j * st] : make_double2(0.0, 0.0);
+            for (int k = 0; k < K; ++k) x[k][j] = aj ? buf[e[k] + mo[j]] : make_double2(0.0, 0.0);
         }
 #pragma unroll
         for (int j = 0; j < D; ++j)
@@ -345,17 +356,17 @@ __device__ __noinline__ void gate_tile_generic(const TileGate tg, const PassGate
         if (needck && !class_ok(tg, g, e0)) continue;
         double2 x[kMaxDim];
         if (g.kind == kPGeneral) {
-            for (int j = 0; j < d; ++j) x[j] = buf[e0 + j * g.st];
+            for (int j = 0; j < d; ++j) x[j] = buf[e0 + tg.moff[j]];
             for (int i = 0; i < d; ++i) {
                 double2 acc = make_double2(0.0, 0.0);
                 for (int j = 0; j < d; ++j) cfma(acc, U[i * d + j], x[j]);
-                buf[e0 + i * g.st] = acc;
+                buf[e0 + tg.moff[i]] = acc;
             }
         } else {
             for (int j = 0; j < d; ++j)
-                if ((g.active >> j) & 1) x[j] = buf[e0 + j * g.st];
+                if ((g.active >> j) & 1) x[j] = buf[e0 + tg.moff[j]];
             for (int j = 0; j < d; ++j)
-                if ((g.active >> j) & 1) buf[e0 + g.sigma[j] * g.st] = cmul(U[j], x[j]);
+                if ((g.active >> j) & 1) buf[e0 + tg.soff[j]] = cmul(U[j], x[j]);
         }
     }
 }
@@ -410,7 +421,8 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant_
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double2 *bufs = reinterpret_cast<double2 *>(smem_raw);
     double2 *Us = bufs + (size_t)S * TE;                       // the pass's matrices
-    uint32_t *soffs = reinterpret_cast<uint32_t *>(Us + p.upool);   // per gate: sigma(j) * st
+    uint32_t *moffs = reinterpret_cast<uint32_t *>(Us + p.upool);   // per gate: member offsets
+    uint32_t *soffs = moffs + kMaxPassGates * kMaxDim;               // per gate: sigma-member offsets
     StageInfo *sinfo = reinterpret_cast<StageInfo *>(soffs + kMaxPassGates * kMaxDim);
     uint64_t *full = reinterpret_cast<uint64_t *>(sinfo + S);
     uint64_t *done = full + S;
@@ -420,8 +432,10 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant_
         fence_mbar_init();
     }
     for (int k = tid; k < p.upool; k += NT + 32) Us[k] = p.U[k];
-    for (int k = tid; k < p.ngates * kMaxDim; k += NT + 32)
-        soffs[k] = (uint32_t)p.g[k / kMaxDim].sigma[k % kMaxDim] * p.g[k / kMaxDim].st;
+    for (int k = tid; k < p.ngates * kMaxDim; k += NT + 32) {
+        moffs[k] = (&p.moff_t[0][0])[k];
+        soffs[k] = (&p.soff_t[0][0])[k];
+    }
     __syncthreads();
     const uint64_t first = blockIdx.x, step = gridDim.x;
     if (first >= p.ntiles) return;
@@ -475,6 +489,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant_
             tg.len = len;
             tg.flags = g.flags;
             tg.lowoff = si.lowoff[gi];
+            tg.moff = moffs + gi * kMaxDim;
             tg.soff = soffs + gi * kMaxDim;
             const bool needck = g.flags != 0 || len < p.LT;
             const double2 *U = Us + g.uoff;
@@ -550,44 +565,130 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
     p.tpr_m = make_fastdiv64(p.tpr).m;
     const uint64_t nruns = reg.D / (M * R);
     p.ntiles = nruns * p.tpr;
+    auto in_tile = [&](int q) {
+        return q < m0 || std::find(pp.H.begin(), pp.H.end(), q) != pp.H.end();
+    };
+    auto tile_stride = [&](int q) -> uint64_t { return q < m0 ? reg.b[q] : W[q] * LT; };
+    for (int i : pp.gates) {
+        const GateSpec &g = gates[i];
+        if (g.span != 1 || !in_tile(g.target) || (int)g.ctrl.size() > kMaxPassCtrl) return false;
+    }
+    // Pair gates: a gate joins an earlier, still single gate of the pass on another in-tile digit
+    // with the same controls (neither target controlling the other) when every gate in between
+    // commutes with it; the two then act as one gate on the two digits, U_b (x) U_a, with
+    // d_a d_b <= kMaxPairDim classes members: one shared-memory round trip instead of two.
+    struct Item { int a, b; };          // gate indices (b = -1: single)
+    std::vector<Item> items;
+    for (int i : pp.gates) {
+        const GateSpec &g = gates[i];
+        bool paired = false;
+        for (int j = (int)items.size() - 1; j >= 0; --j) {
+            Item &it = items[j];
+            const GateSpec &h = gates[it.a];
+            if (it.b < 0 && h.target != g.target && h.d <= 5 && g.d <= 5 && h.d * g.d <= kMaxPairDim &&
+                same_controls(h, g)) {
+                bool cross = false;
+                for (const auto &c : g.ctrl) cross = cross || c.q == h.target;
+                for (const auto &c : h.ctrl) cross = cross || c.q == g.target;
+                if (!cross) {
+                    it.b = i;
+                    paired = true;
+                    break;
+                }
+            }
+            if (!commute(gates[it.a], g) || (it.b >= 0 && !commute(gates[it.b], g))) break;
+        }
+        if (!paired) items.push_back({i, -1});
+    }
     // gates
     int uoff = 0;
     *touched = 0.0;
-    p.ngates = (int32_t)pp.gates.size();
-    for (size_t gi = 0; gi < pp.gates.size(); ++gi) {
-        const GateSpec &g = gates[pp.gates[gi]];
+    p.ngates = (int32_t)items.size();
+    for (size_t gi = 0; gi < items.size(); ++gi) {
+        const GateSpec &g = gates[items[gi].a];
         GatePlan gp;
         std::string err;
         if (plan_gate(reg, g, false, &gp, &err) != SV_OK) return false;
         *touched += (double)gp.touched;
         PassGateP &q = p.g[gi];
-        q.d = gp.d;
-        q.kind = gp.kind == kGeneral ? kPGeneral : kPMonomial;
-        if (q.kind == kPMonomial) {            // every moving coefficient exactly 1: pure data movement
-            bool perm = true;
-            for (int j = 0; j < gp.d; ++j)
-                if (((gp.active >> j) & 1) && !(gp.U[j].x == 1.0 && gp.U[j].y == 0.0)) perm = false;
-            if (perm) q.kind = kPPerm;
-        }
-        q.active = gp.active;
-        for (int j = 0; j < kMaxDim; ++j) q.sigma[j] = (int8_t)(j < gp.d ? gp.sigma[j] : j);
-        const int need = gp.kind == kGeneral ? gp.d * gp.d : gp.d;
-        if (uoff + need > kPoolC) return false;
-        q.uoff = uoff;
-        for (int k = 0; k < need; ++k) p.U[uoff + k] = gp.U[k];
-        uoff += need;
-        p.upool = uoff;
         const int t = g.target;
-        if (g.span != 1 || (t >= m0 && std::find(pp.H.begin(), pp.H.end(), t) == pp.H.end())) return false;
-        const uint64_t st = (t < m0) ? reg.b[t] : W[t] * LT;
+        const uint64_t st = tile_stride(t);
         q.st = (uint32_t)st;
         q.mst = make_fastdiv32(q.st).m;
-        if ((int)g.ctrl.size() > kMaxPassCtrl) return false;
-        // in-tile controls on H / low-prefix digits are inserted into the class index with
-        // their pinned values (only firing classes are visited); the rest are decided at run time
         struct Ins { uint64_t s; uint32_t d, pin; };
         std::vector<Ins> ins{{st, (uint32_t)gp.d, 0u}};
         uint64_t cls_div = (uint64_t)gp.d;
+        int D = gp.d;
+        // member offsets, coefficients / matrix, sigma of this (possibly pair) gate
+        std::vector<uint32_t> moff(kMaxDim, 0), sig(kMaxDim, 0);
+        std::vector<double2> Ud;                  // dense D x D or coefficients
+        int kind = gp.kind;
+        if (items[gi].b < 0) {
+            for (int j = 0; j < D; ++j) { moff[j] = (uint32_t)(j * st); sig[j] = (uint32_t)gp.sigma[j]; }
+            q.active = gp.active;
+            const int need = gp.kind == kGeneral ? D * D : D;
+            Ud.assign(gp.U, gp.U + need);
+        } else {
+            const GateSpec &h = gates[items[gi].b];      // h acts on digit b (second), g on a
+            GatePlan hp;
+            if (plan_gate(reg, h, false, &hp, &err) != SV_OK) return false;
+            *touched += (double)hp.touched;
+            const int da = gp.d, db = hp.d;
+            D = da * db;
+            const uint64_t stb = tile_stride(h.target);
+            ins.push_back({stb, (uint32_t)db, 0u});
+            cls_div *= (uint64_t)db;
+            for (int jb = 0; jb < db; ++jb)
+                for (int ja = 0; ja < da; ++ja) moff[ja + da * jb] = (uint32_t)(ja * st + jb * stb);
+            if (gp.kind == kMonomial && hp.kind == kMonomial) {
+                kind = kMonomial;
+                uint32_t act = 0;
+                Ud.resize(D);
+                for (int jb = 0; jb < db; ++jb)
+                    for (int ja = 0; ja < da; ++ja) {
+                        const int J = ja + da * jb;
+                        sig[J] = (uint32_t)(gp.sigma[ja] + da * hp.sigma[jb]);
+                        const double2 ca = gp.U[ja], cb = hp.U[jb];
+                        Ud[J] = make_double2(ca.x * cb.x - ca.y * cb.y, ca.x * cb.y + ca.y * cb.x);
+                        if (sig[J] != (uint32_t)J || Ud[J].x != 1.0 || Ud[J].y != 0.0) act |= 1u << J;
+                    }
+                q.active = act;
+            } else {
+                kind = kGeneral;
+                q.active = (1u << D) - 1u;
+                Ud.resize((size_t)D * D);
+                for (int ib = 0; ib < db; ++ib)
+                    for (int ia = 0; ia < da; ++ia)
+                        for (int jb = 0; jb < db; ++jb)
+                            for (int ja = 0; ja < da; ++ja) {
+                                const double2 ua = g.U[ia * da + ja], ub = h.U[ib * db + jb];
+                                Ud[(ia + da * ib) * D + (ja + da * jb)] =
+                                    make_double2(ua.x * ub.x - ua.y * ub.y, ua.x * ub.y + ua.y * ub.x);
+                            }
+                for (int J = 0; J < D; ++J) sig[J] = (uint32_t)J;
+            }
+        }
+        q.d = D;
+        q.kind = kind == kGeneral ? kPGeneral : kPMonomial;
+        if (q.kind == kPMonomial) {            // every moving coefficient exactly 1: pure data movement
+            bool perm = true;
+            for (int j = 0; j < D; ++j)
+                if (((q.active >> j) & 1) && !(Ud[j].x == 1.0 && Ud[j].y == 0.0)) perm = false;
+            if (perm) q.kind = kPPerm;
+        }
+        for (int j = 0; j < kMaxDim; ++j) {
+            q.sigma[j] = (int8_t)(j < D ? sig[j] : j);
+            p.moff_t[gi][j] = moff[j];
+            p.soff_t[gi][j] = j < D ? moff[sig[j]] : 0u;
+        }
+        const int need = (int)Ud.size();
+        if (uoff + need > kPoolC) return false;
+        q.uoff = uoff;
+        for (int k = 0; k < need; ++k) p.U[uoff + k] = Ud[k];
+        uoff += need;
+        p.upool = uoff;
+        // in-tile controls on H / low-prefix digits are inserted into the class index with
+        // their pinned values (only firing classes are visited); the rest are decided at run time
         int nc = 0;
         for (size_t k = 0; k < g.ctrl.size(); ++k) {
             const int c = g.ctrl[k].q;
@@ -619,6 +720,7 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
             }
         }
         q.nctrl = nc;
+        if ((int)ins.size() > kMaxIns) return false;
         std::sort(ins.begin(), ins.end(), [](const Ins &a, const Ins &b) { return a.s < b.s; });
         q.nins = (int32_t)ins.size();
         for (size_t i = 0; i < ins.size(); ++i) {
@@ -637,7 +739,7 @@ cudaError_t launch_pass_t(const PassParams &p, cudaStream_t st, const LaunchCfg 
     const int S = cfg.pass_stages, TE = cfg.pass_tile;
     // size for the largest matrix pool so the attribute and the occupancy are set once per config
     const size_t smem = (size_t)S * TE * sizeof(double2) + (size_t)kPoolC * sizeof(double2) +
-                        (size_t)kMaxPassGates * kMaxDim * sizeof(uint32_t) +
+                        (size_t)2 * kMaxPassGates * kMaxDim * sizeof(uint32_t) +
                         (size_t)S * sizeof(StageInfo) + (size_t)2 * S * sizeof(uint64_t);
     static size_t configured = 0, occ_for = 0;
     static int occ = 1;

@@ -201,6 +201,8 @@ static bool same_ctrl(const std::vector<CtrlSpec> &a, const std::vector<CtrlSpec
     return true;
 }
 
+bool same_controls(const GateSpec &a, const GateSpec &b) { return same_ctrl(a.ctrl, b.ctrl); }
+
 std::vector<GateSpec> fuse_gates(const Register &reg, const std::vector<GateSpec> &in) {
     std::vector<GateSpec> out;
     bool have = false;
@@ -250,7 +252,6 @@ std::vector<GateSpec> merge_same_qudit(const std::vector<GateSpec> &in) {
 }
 
 // ------------------------------------------------------------------- multi-gate passes
-static bool commute(const GateSpec &a, const GateSpec &b);
 
 // Commutation-aware merging: a gate joins the latest earlier gate with the same target and the
 // same controls when every gate in between commutes with it (it can be moved back next to that
@@ -291,7 +292,7 @@ static bool is_diag(const GateSpec &g) {
 // and that target gate is not diagonal (a diagonal gate on a digit commutes with everything
 // that is block-diagonal in that digit, i.e. with any gate merely controlled on it); two gates
 // on the same digit commute when both are diagonal.
-static bool commute(const GateSpec &a, const GateSpec &b) {
+bool commute(const GateSpec &a, const GateSpec &b) {
     if (a.span != 1 || b.span != 1) {            // fused spans: plain disjointness of the digits
         auto in = [](int q, const GateSpec &g) { return q >= g.target && q < g.target + g.span; };
         for (int k = 0; k < a.span; ++k)

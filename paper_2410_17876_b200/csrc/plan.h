@@ -49,6 +49,11 @@ sv_status plan_gate(const Register &reg, const GateSpec &g, bool check_unitary, 
 // into one gate of dimension <= 16.
 std::vector<GateSpec> fuse_gates(const Register &reg, const std::vector<GateSpec> &in);
 
+// Sufficient commutation test of two (controlled) single-qudit gates (reading R19).
+bool commute(const GateSpec &a, const GateSpec &b);
+// Identical control sets (qudits and values, any order).
+bool same_controls(const GateSpec &a, const GateSpec &b);
+
 // Consecutive gates on the same target with identical controls -> one matrix product.
 std::vector<GateSpec> merge_same_qudit(const std::vector<GateSpec> &in);
 

@@ -29,6 +29,7 @@ def main():
     b = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(b)
     print(b.build(force=True))
+    shutil.rmtree(os.path.join(out, "build"), ignore_errors=True)     # objects: keep the gpurun snapshot small
 
 
 if __name__ == "__main__":
