@@ -242,45 +242,64 @@ sv_status shard_apply_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_
     // Runs of gates with a local target go through the local circuit driver on every slice
     // this handle owns (fusion / multi-gate passes included).  Controls on sharded digits are
     // a rank predicate (rule ii): per slice, the gate is dropped when its rank fails them and
-    // kept without them otherwise, so they do not break the run.
+    // kept without them otherwise, so they do not break the run.  With SV_BLOCK, gates are first
+    // merged across commuting neighbours (merge_commuting, also merging gates on sharded qubits:
+    // fewer exchanges), and a local gate moves ahead of pending exchange gates it commutes with,
+    // so local runs stay long and exchanges cluster.
     const std::vector<int> ranks = ranks_of(h->shard);
     const int first_sh = h->local.n;
+    if (flags & SV_BLOCK) specs = merge_commuting(specs, 64);
     std::vector<std::vector<GateSpec>> runs(ranks.size());
+    std::vector<const GateSpec *> pending;         // exchange gates not applied yet, in order
     bool any = false;
     auto flush = [&]() -> sv_status {
-        if (!any) return SV_OK;
-        const uint32_t local_flags = flags & (SV_FUSE | SV_BLOCK);
-        for (size_t i = 0; i < ranks.size(); ++i) {
-            if (runs[i].empty()) continue;
-            sv_status s = run_local_circuit(h, runs[i], local_flags, slice_of(h->shard, ranks[i]));
-            if (s != SV_OK) return s;
-            runs[i].clear();
+        if (any) {
+            const uint32_t local_flags = flags & (SV_FUSE | SV_BLOCK);
+            for (size_t i = 0; i < ranks.size(); ++i) {
+                if (runs[i].empty()) continue;
+                sv_status s = run_local_circuit(h, runs[i], local_flags, slice_of(h->shard, ranks[i]));
+                if (s != SV_OK) return s;
+                runs[i].clear();
+            }
+            any = false;
         }
-        any = false;
+        for (const GateSpec *g : pending) {
+            sv_status s = shard_apply(h, *g, false);
+            if (s != SV_OK) return s;
+        }
+        pending.clear();
         return SV_OK;
     };
+    const bool reorder = (flags & SV_BLOCK) != 0;
     for (const GateSpec &g : specs) {
-        if (g.target < first_sh) {
-            for (size_t i = 0; i < ranks.size(); ++i) {
-                GateSpec lg = g;
-                lg.ctrl.clear();
-                bool fires = true;
-                for (const auto &c : g.ctrl) {
-                    if (c.q < first_sh) { lg.ctrl.push_back(c); continue; }
-                    const int bit = (ranks[i] >> (c.q - first_sh)) & 1;   // rank bit j = digit of q_{n-s+j}
-                    if (bit != c.v) fires = false;
-                }
-                if (fires) {
-                    runs[i].push_back(std::move(lg));
-                    any = true;
-                }
+        if (g.target >= first_sh) {
+            pending.push_back(&g);
+            if (!reorder) {
+                sv_status s = flush();
+                if (s != SV_OK) return s;
             }
             continue;
         }
-        sv_status s = flush();
-        if (s != SV_OK) return s;
-        s = shard_apply(h, g, false);
-        if (s != SV_OK) return s;
+        bool ahead = true;                          // may this local gate pass the pending ones?
+        for (const GateSpec *q : pending) ahead = ahead && commute(*q, g);
+        if (!ahead) {
+            sv_status s = flush();
+            if (s != SV_OK) return s;
+        }
+        for (size_t i = 0; i < ranks.size(); ++i) {
+            GateSpec lg = g;
+            lg.ctrl.clear();
+            bool fires = true;
+            for (const auto &c : g.ctrl) {
+                if (c.q < first_sh) { lg.ctrl.push_back(c); continue; }
+                const int bit = (ranks[i] >> (c.q - first_sh)) & 1;   // rank bit j = digit of q_{n-s+j}
+                if (bit != c.v) fires = false;
+            }
+            if (fires) {
+                runs[i].push_back(std::move(lg));
+                any = true;
+            }
+        }
     }
     return flush();
 }
