@@ -184,6 +184,8 @@ SV_API sv_status sv_get_info(sv_handle h, sv_info *out);
 #define SV_OPT_PASS_GROUPS 10   /* consumer warp groups of the pass kernel working on different tiles
                                    (1, 2 or 4; at most the number of stages)                          */
 #define SV_OPT_PASS_WINDOW 11   /* gates the pass planner scans ahead (1..4096)                    */
+#define SV_OPT_PASS_MERGE  12   /* 1 (default): merge commuting same-target gates before SV_BLOCK passes;
+                                   0: keep every gate (per-gate microbenchmarks)                   */
 SV_API sv_status sv_set_option(sv_handle h, int32_t option, int64_t value);
 
 /* Per-launch timing of the gate kernels recorded while SV_OPT_PROFILE is on: the summed

@@ -248,7 +248,7 @@ sv_status shard_apply_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_
     // so local runs stay long and exchanges cluster.
     const std::vector<int> ranks = ranks_of(h->shard);
     const int first_sh = h->local.n;
-    if (flags & SV_BLOCK) specs = merge_commuting(specs, 64);
+    if ((flags & SV_BLOCK) && h->cfg.pass_merge) specs = merge_commuting(specs, 64);
     std::vector<std::vector<GateSpec>> runs(ranks.size());
     std::vector<const GateSpec *> pending;         // exchange gates not applied yet, in order
     bool any = false;

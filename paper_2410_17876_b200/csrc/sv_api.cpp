@@ -64,6 +64,7 @@ void default_cfg(LaunchCfg &c, int device) {
     c.pass_threads = 512;
     c.pass_gates = 24;
     c.pass_window = 64;        // gates scanned ahead when filling a pass
+    c.pass_merge = 1;          // commutation-aware merging before pass planning
     c.pass_groups = 2;         // two consumer groups ping-pong over tiles
 }
 
@@ -235,7 +236,7 @@ sv_status run_local_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_t 
     std::vector<PassPlan> passes;
     if ((flags & SV_BLOCK) && h->c64) flags = (flags & ~SV_BLOCK) | SV_FUSE;   // pass kernel: c128 only
     if (flags & SV_BLOCK) {
-        specs = merge_commuting(specs, 64);
+        if (h->cfg.pass_merge) specs = merge_commuting(specs, 64);
         passes = plan_passes(h->local, specs, (uint64_t)h->cfg.pass_tile, h->cfg.pass_gates, h->cfg.pass_window);
     } else {
         if (flags & SV_FUSE) specs = fuse_gates(h->local, specs);
@@ -500,6 +501,9 @@ sv_status sv_set_option(sv_handle h, int32_t option, int64_t value) {
         case SV_OPT_PASS_GROUPS:
             if (value != 1 && value != 2 && value != 4) return fail(SV_ERR_INVALID_ARG, "pass groups 1, 2 or 4");
             h->cfg.pass_groups = (int)value;
+            return SV_OK;
+        case SV_OPT_PASS_MERGE:
+            h->cfg.pass_merge = value != 0;
             return SV_OK;
         case SV_OPT_PASS_WINDOW:
             if (value < 1 || value > 4096) return fail(SV_ERR_INVALID_ARG, "pass window 1..4096");

@@ -183,6 +183,7 @@ struct LaunchCfg {
     int pass_threads;  // threads per CTA of the pass kernel (256 or 512)
     int pass_gates;    // max gates per pass
     int pass_window;   // gates scanned ahead (commuting past skipped ones) when filling a pass
+    int pass_merge;    // 1: merge same-target same-control gates across commuting ones first
     int pass_groups;   // consumer warp groups of the pass kernel (ping-pong over tiles)
     int c64;           // 1: the state is complex64 (float2), else complex128 (double2)
 };

@@ -49,6 +49,7 @@ def main():
         "phase_qutrits_H": cyc(qutrits[:3], lambda t, i: Gate(t, (), (), clock_z(3))),
     }
     st = P.State(dims)
+    st.set_option(P.sv.SV_OPT_PASS_MERGE, 0)       # one application per listed gate
     ext = torch.cuda.ExternalStream(st.info().cuda_stream)
     for name, gates in mixes.items():
         if args.only and name not in args.only.split(","):
