@@ -254,6 +254,19 @@ __device__ __forceinline__ uint32_t opaque_zero(uint32_t v) {
     return z;
 }
 
+// Tile accesses through 32-bit shared-window addresses computed once per gate: with the
+// pointer form, ptxas (at 96 registers) re-derived the CTA's shared window base (S2R
+// SR_CgaCtaId + LEA) for every store.  volatile keeps their order (class gathers before
+// scatters, gates separated by the group barrier).
+__device__ __forceinline__ double2 lds2(uint32_t a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts2(uint32_t a, double2 v) {
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
+
 // One general gate (y = U x per class) on one tile, K classes per thread
 // iteration.  All K*D gathers are issued before the matvecs; buf and U are restrict-qualified
 // so the matrix reads may be scheduled across the stores of earlier rows.
@@ -265,7 +278,8 @@ __device__ __forceinline__ void gate_tile_general(const TileGate &tg, const Pass
     // far as the compiler knows, so it keeps them in registers)
     uint32_t mo[D];
 #pragma unroll
-    for (int j = 0; j < D; ++j) mo[j] = tg.moff[j];
+    for (int j = 0; j < D; ++j) mo[j] = tg.moff[j] * (uint32_t)sizeof(double2);
+    const uint32_t sb = smem_u32(buf);
     const Ins1 first = ins_at(g, 0);
     const bool more = g.nins > 1;
 #pragma unroll 1
@@ -278,7 +292,7 @@ __device__ __forceinline__ void gate_tile_general(const TileGate &tg, const Pass
 #pragma unroll
         for (int k = 0; k < K; ++k)
 #pragma unroll
-            for (int j = 0; j < D; ++j) x[k][j] = buf[e[k] + mo[j]];
+            for (int j = 0; j < D; ++j) x[k][j] = lds2(sb + e[k] * (uint32_t)sizeof(double2) + mo[j]);
 #pragma unroll
         for (int i = 0; i < D; ++i) {
             double2 acc[K];
@@ -292,7 +306,7 @@ __device__ __forceinline__ void gate_tile_general(const TileGate &tg, const Pass
             }
 #pragma unroll
             for (int k = 0; k < K; ++k)
-                if (ok[k]) buf[e[k] + mo[i]] = acc[k];
+                if (ok[k]) sts2(sb + e[k] * (uint32_t)sizeof(double2) + mo[i], acc[k]);
         }
     }
 }
@@ -314,9 +328,10 @@ __device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const Pas
     uint32_t so[D], mo[D];
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-        so[j] = tg.soff[j];
-        mo[j] = tg.moff[j];
+        so[j] = tg.soff[j] * (uint32_t)sizeof(double2);
+        mo[j] = tg.moff[j] * (uint32_t)sizeof(double2);
     }
+    const uint32_t sb = smem_u32(buf);
 #pragma unroll 1
     for (uint32_t c0 = cbeg + (uint32_t)tid; c0 < cend; c0 += (uint32_t)(NT * K)) {
         uint32_t e[K];
@@ -327,7 +342,8 @@ __device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const Pas
         for (int j = 0; j < D; ++j) {
             const bool aj = (act >> j) & 1;
 #pragma unroll
-            for (int k = 0; k < K; ++k) x[k][j] = aj ? buf[e[k] + mo[j]] : make_double2(0.0, 0.0);
+            for (int k = 0; k < K; ++k)
+                x[k][j] = aj ? lds2(sb + e[k] * (uint32_t)sizeof(double2) + mo[j]) : make_double2(0.0, 0.0);
         }
 #pragma unroll
         for (int j = 0; j < D; ++j)
@@ -335,12 +351,12 @@ __device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const Pas
                 if (PERM) {
 #pragma unroll
                     for (int k = 0; k < K; ++k)
-                        if (ok[k]) buf[e[k] + so[j]] = x[k][j];
+                        if (ok[k]) sts2(sb + e[k] * (uint32_t)sizeof(double2) + so[j], x[k][j]);
                 } else {
                     const double2 u = U[j];
 #pragma unroll
                     for (int k = 0; k < K; ++k)
-                        if (ok[k]) buf[e[k] + so[j]] = cmul(u, x[k][j]);
+                        if (ok[k]) sts2(sb + e[k] * (uint32_t)sizeof(double2) + so[j], cmul(u, x[k][j]));
                 }
             }
     }
