@@ -156,6 +156,7 @@ def run_reference(args, rank, world):
     from oracle import blocksim as O2
     from sv_inputs import config_circuit, CONFIG_NAMES
     import paper_2410_17876_b200 as P
+    full_dims = config_circuit(args.config, ngates=0)[0]      # the workload the arm is quoted on
     nq = {3: 7, 4: 5, 5: 4}.get(args.config, None)
     dims, gates = config_circuit(args.config, nqubits=nq)
     D = int(np.prod(dims))
@@ -181,7 +182,9 @@ def run_reference(args, rank, world):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * t / max(1, args.steps), "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": CONFIG_NAMES[args.config], "dims_q0_first": dims},
+            "data": "synthetic",
+            "config": {"workload": CONFIG_NAMES[args.config], "dims_q0_first": full_dims,
+                       "sample_dims_q0_first": dims},
             "cpu_baseline": b,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
