@@ -268,3 +268,24 @@ def test_merge_planner_commutation_rules():
     assert len(m) == 2                                              # diagonals on one digit commute
     m = P.merge_plan(dims, [Gate(0, (), (), H), cnot, Gate(0, (), (), H)], window=1)
     assert len(m) == 3                                              # the window bounds the scan
+
+
+def test_bench_reference_arm_line():
+    """bench.py --impl reference (the oracle timed on the host, the tier's reference arm) prints
+    one JSON line with the contract's keys; the config names the full c4 workload."""
+    import json
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference",
+                          "--steps", "1", "--warmup", "1"], capture_output=True, text=True, timeout=600,
+                         cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["value"] > 0 and d["steps"] == 1
+    assert d["config"]["dims_q0_first"] == [5, 5, 4, 4, 4, 4] + [3] * 6 + [2] * 10
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["e2e"]["h2d_bytes_per_step"] == 0
