@@ -181,8 +181,8 @@ SV_API sv_status sv_get_info(sv_handle h, sv_info *out);
 #define SV_OPT_PASS_STAGES  7   /* shared-memory ring stages of the pass kernel (2..6)             */
 #define SV_OPT_PASS_THREADS 8   /* compute threads per CTA of the pass kernel (256, 384 or 512)    */
 #define SV_OPT_PASS_GATES   9   /* max gates applied per pass (1..32)                              */
-#define SV_OPT_PASS_GROUPS 10   /* consumer warp groups of the pass kernel working on different tiles
-                                   (1, 2 or 4; at most the number of stages)                          */
+#define SV_OPT_PASS_GROUPS 10   /* consumer warp groups of the pass kernel, each on its own tile
+                                   (1, 2, or 4 with 512 threads; at most the number of stages)     */
 #define SV_OPT_PASS_WINDOW 11   /* gates the pass planner scans ahead (1..4096)                    */
 #define SV_OPT_PASS_MERGE  12   /* 1 (default): merge commuting same-target gates before SV_BLOCK passes;
                                    0: keep every gate (per-gate microbenchmarks)                   */
