@@ -157,3 +157,46 @@ def test_c4_labelled_every_target(P):
 
 def test_c4_circuit_then_adjoint(P):
     _adjoint_return(P, 4)
+
+
+def test_c3_many_controls_labelled(P):
+    """multi-controlled gates (3 and 4 controls, on low-stride and high-stride
+    digits, with values other than the top one) at full c3 size, through the single-gate kernels
+    and through SV_BLOCK passes, on the index-labelled state against the oracle's one-index
+    evaluator (only control-satisfying classes change)."""
+    dims = config_circuit(3, ngates=0)[0]                # [3]*8 + [2]*16
+    n, D = len(dims), int(np.prod(dims))
+    rng = np.random.default_rng(303)
+    starts, width = _windows(D, rng)
+    idx = _idx(starts, width)
+    exp_lab = np.empty(idx.size, dtype=np.complex128)
+    exp_lab.real = idx.astype(np.float64) + 1.0
+    exp_lab.imag = -(idx.astype(np.float64) + 1.0) / 2.0
+    b = np.cumprod([1] + dims[:-1]).astype(np.float64)
+    # permutations first: they keep the state exactly labelled (the general gates' round
+    # trips leave rounding behind)
+    cases = [
+        Gate(5, (1, 4, 17), (0, 2, 1), shift_x(3, 2), "perm_3ctrl"),
+        Gate(22, (0, 1, 2, 15), (2, 2, 0, 1), shift_x(2, 1), "perm_4ctrl"),
+        Gate(9, (0, 3, 20), (2, 1, 1), haar_unitary(2, rng), "haar_3ctrl"),
+        Gate(2, (0, 8, 12, 23), (1, 1, 0, 1), haar_unitary(3, rng), "haar_4ctrl"),
+    ]
+    with P.State(dims) as st:
+        for block in (False, True):
+            _upload_labelled(st, D)
+            for g in cases:
+                if block:
+                    st.apply_circuit([g], block=True)
+                else:
+                    st.apply_gate(g.target, g.U, g.ctrl, g.vals)
+                got = _sample(st, starts, width)
+                exp = O2.gate_output_labelled(dims, g, idx)
+                if g.name.startswith("perm"):
+                    assert np.array_equal(got, exp), (block, g.name)
+                else:
+                    scale = idx.astype(np.float64) + dims[g.target] * b[g.target] + 1.0
+                    assert np.max(np.abs(got - exp) / scale) <= 1e-13, (block, g.name)
+                st.apply_gate(g.target, g.U.conj().T, g.ctrl, g.vals)       # undo
+                back = _sample(st, starts, width)
+                if g.name.startswith("perm"):
+                    assert np.array_equal(back, exp_lab), (block, g.name)
