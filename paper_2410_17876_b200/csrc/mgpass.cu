@@ -135,7 +135,8 @@ struct StageInfo {
     uint32_t lowoff[kMaxPassGates][kMaxPassCtrl];    // (s0 mod b_c d_c) for run-digit controls
 };
 
-__device__ __forceinline__ void issue_loads(const PassParams &p, uint64_t t, double2 *buf, uint64_t *bar,
+template <typename V>
+__device__ __forceinline__ void issue_loads(const PassParams &p, uint64_t t, V *buf, uint64_t *bar,
                                             StageInfo *si, int lane) {
     const TileInfo ti = tile_info(p, t);
     // lane g decides gate g for this tile
@@ -162,10 +163,11 @@ __device__ __forceinline__ void issue_loads(const PassParams &p, uint64_t t, dou
         si->fire = bits;
     }
     __syncwarp();
-    if (lane == 0) mbar_expect_tx(bar, (uint32_t)p.M * ti.len * (uint32_t)sizeof(double2));
+    if (lane == 0) mbar_expect_tx(bar, (uint32_t)p.M * ti.len * (uint32_t)sizeof(V));
     __syncwarp();
     for (int m = lane; m < p.M; m += 32)
-        bulk_load(buf + (size_t)m * p.LT, p.psi + ti.gbase + p.moff[m], ti.len * (uint32_t)sizeof(double2), bar);
+        bulk_load(buf + (size_t)m * p.LT, reinterpret_cast<const V *>(p.psi) + ti.gbase + p.moff[m],
+                  ti.len * (uint32_t)sizeof(V), bar);
 }
 
 // In-tile division (x < 2^16, d < 2^16): with m = floor(2^32/d) + 1, umulhi(x, m) is exact
@@ -258,27 +260,36 @@ __device__ __forceinline__ uint32_t opaque_zero(uint32_t v) {
 // pointer form, ptxas (at 96 registers) re-derived the CTA's shared window base (S2R
 // SR_CgaCtaId + LEA) for every store.  volatile keeps their order (class gathers before
 // scatters, gates separated by the group barrier).
-__device__ __forceinline__ double2 lds2(uint32_t a) {
+template <typename V> __device__ __forceinline__ V lds2(uint32_t a);
+template <> __device__ __forceinline__ double2 lds2<double2>(uint32_t a) {
     double2 v;
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+template <> __device__ __forceinline__ float2 lds2<float2>(uint32_t a) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
     return v;
 }
 __device__ __forceinline__ void sts2(uint32_t a, double2 v) {
     asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
 }
+__device__ __forceinline__ void sts2(uint32_t a, float2 v) {
+    asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
+}
 
 // One general gate (y = U x per class) on one tile, K classes per thread
 // iteration.  All K*D gathers are issued before the matvecs; buf and U are restrict-qualified
 // so the matrix reads may be scheduled across the stores of earlier rows.
-template <int D, int K, int NT>
-__device__ __forceinline__ void gate_tile_general(const TileGate &tg, const PassGateP &g, double2 *__restrict__ buf,
-                                                  const double2 *__restrict__ U, uint32_t cbeg, uint32_t cend,
+template <int D, int K, int NT, typename V>
+__device__ __forceinline__ void gate_tile_general(const TileGate &tg, const PassGateP &g, V *__restrict__ buf,
+                                                  const V *__restrict__ U, uint32_t cbeg, uint32_t cend,
                                                   uint32_t ncls, bool needck, int tid) {
     // member offsets, read once from shared memory (the stores below may alias that table as
     // far as the compiler knows, so it keeps them in registers)
     uint32_t mo[D];
 #pragma unroll
-    for (int j = 0; j < D; ++j) mo[j] = tg.moff[j] * (uint32_t)sizeof(double2);
+    for (int j = 0; j < D; ++j) mo[j] = tg.moff[j] * (uint32_t)sizeof(V);
     const uint32_t sb = smem_u32(buf);
     const Ins1 first = ins_at(g, 0);
     const bool more = g.nins > 1;
@@ -287,26 +298,26 @@ __device__ __forceinline__ void gate_tile_general(const TileGate &tg, const Pass
         uint32_t e[K];
         bool ok[K];
         class_batch<K, NT>(tg, g, first, more, c0, ncls, needck, e, ok);
-        const double2 *__restrict__ Ui = U + opaque_zero(c0);
-        double2 x[K][D];
+        const V *__restrict__ Ui = U + opaque_zero(c0);
+        V x[K][D];
 #pragma unroll
         for (int k = 0; k < K; ++k)
 #pragma unroll
-            for (int j = 0; j < D; ++j) x[k][j] = lds2(sb + e[k] * (uint32_t)sizeof(double2) + mo[j]);
+            for (int j = 0; j < D; ++j) x[k][j] = lds2<V>(sb + e[k] * (uint32_t)sizeof(V) + mo[j]);
 #pragma unroll
         for (int i = 0; i < D; ++i) {
-            double2 acc[K];
+            V acc[K];
 #pragma unroll
-            for (int k = 0; k < K; ++k) acc[k] = make_double2(0.0, 0.0);
+            for (int k = 0; k < K; ++k) acc[k] = cz<V>();
 #pragma unroll
             for (int j = 0; j < D; ++j) {
-                const double2 u = Ui[i * D + j];
+                const V u = Ui[i * D + j];
 #pragma unroll
                 for (int k = 0; k < K; ++k) cfma(acc[k], u, x[k][j]);
             }
 #pragma unroll
             for (int k = 0; k < K; ++k)
-                if (ok[k]) sts2(sb + e[k] * (uint32_t)sizeof(double2) + mo[i], acc[k]);
+                if (ok[k]) sts2(sb + e[k] * (uint32_t)sizeof(V) + mo[i], acc[k]);
         }
     }
 }
@@ -315,9 +326,9 @@ __device__ __forceinline__ void gate_tile_general(const TileGate &tg, const Pass
 // tile; PERM: every moving coefficient is exactly 1, so the gate only moves data.  Only the
 // members that move or scale are read and written (select-form predicated gathers: a branch
 // per member makes ptxas spill the array).
-template <int D, int K, int NT, bool PERM>
-__device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const PassGateP &g, double2 *__restrict__ buf,
-                                                   const double2 *__restrict__ U, uint32_t cbeg, uint32_t cend,
+template <int D, int K, int NT, bool PERM, typename V>
+__device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const PassGateP &g, V *__restrict__ buf,
+                                                   const V *__restrict__ U, uint32_t cbeg, uint32_t cend,
                                                    uint32_t ncls, bool needck, int tid) {
     const uint32_t act = g.active;
     const Ins1 first = ins_at(g, 0);
@@ -328,8 +339,8 @@ __device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const Pas
     uint32_t so[D], mo[D];
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-        so[j] = tg.soff[j] * (uint32_t)sizeof(double2);
-        mo[j] = tg.moff[j] * (uint32_t)sizeof(double2);
+        so[j] = tg.soff[j] * (uint32_t)sizeof(V);
+        mo[j] = tg.moff[j] * (uint32_t)sizeof(V);
     }
     const uint32_t sb = smem_u32(buf);
 #pragma unroll 1
@@ -337,13 +348,13 @@ __device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const Pas
         uint32_t e[K];
         bool ok[K];
         class_batch<K, NT>(tg, g, first, more, c0, ncls, needck, e, ok);
-        double2 x[K][D];
+        V x[K][D];
 #pragma unroll
         for (int j = 0; j < D; ++j) {
             const bool aj = (act >> j) & 1;
 #pragma unroll
             for (int k = 0; k < K; ++k)
-                x[k][j] = aj ? lds2(sb + e[k] * (uint32_t)sizeof(double2) + mo[j]) : make_double2(0.0, 0.0);
+                x[k][j] = aj ? lds2<V>(sb + e[k] * (uint32_t)sizeof(V) + mo[j]) : cz<V>();
         }
 #pragma unroll
         for (int j = 0; j < D; ++j)
@@ -351,12 +362,12 @@ __device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const Pas
                 if (PERM) {
 #pragma unroll
                     for (int k = 0; k < K; ++k)
-                        if (ok[k]) sts2(sb + e[k] * (uint32_t)sizeof(double2) + so[j], x[k][j]);
+                        if (ok[k]) sts2(sb + e[k] * (uint32_t)sizeof(V) + so[j], x[k][j]);
                 } else {
-                    const double2 u = U[j];
+                    const V u = U[j];
 #pragma unroll
                     for (int k = 0; k < K; ++k)
-                        if (ok[k]) sts2(sb + e[k] * (uint32_t)sizeof(double2) + so[j], cmul(u, x[k][j]));
+                        if (ok[k]) sts2(sb + e[k] * (uint32_t)sizeof(V) + so[j], cmul(u, x[k][j]));
                 }
             }
     }
@@ -364,17 +375,18 @@ __device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const Pas
 
 // generic dimension (fused or d > 5): out of line so its 16-wide register arrays do not
 // inflate the kernel
-__device__ __noinline__ void gate_tile_generic(const TileGate tg, const PassGateP &g, double2 *buf,
-                                               const double2 *U, uint32_t ncls, bool needck, int tid, int nt) {
+template <typename V>
+__device__ __noinline__ void gate_tile_generic(const TileGate tg, const PassGateP &g, V *buf,
+                                               const V *U, uint32_t ncls, bool needck, int tid, int nt) {
     const int d = g.d;
     for (uint32_t c = tid; c < ncls; c += nt) {
         const uint32_t e0 = class_e0(c, g, ins_at(g, 0), true);
         if (needck && !class_ok(tg, g, e0)) continue;
-        double2 x[kMaxDim];
+        V x[kMaxDim];
         if (g.kind == kPGeneral) {
             for (int j = 0; j < d; ++j) x[j] = buf[e0 + tg.moff[j]];
             for (int i = 0; i < d; ++i) {
-                double2 acc = make_double2(0.0, 0.0);
+                V acc = cz<V>();
                 for (int j = 0; j < d; ++j) cfma(acc, U[i * d + j], x[j]);
                 buf[e0 + tg.moff[i]] = acc;
             }
@@ -397,22 +409,22 @@ template <int NT> struct PassK<5, NT> { static constexpr int value = NT >= 384 ?
 
 // NT = compute threads of the CTA (sets the register budget), NTG = threads of one consumer
 // group (the class stride)
-template <int D, int NT, int NTG>
-__device__ __forceinline__ void apply_gate_tile(const TileGate &tg, const PassGateP &g, double2 *buf,
-                                                const double2 *U, uint32_t ncls, bool needck, int tid) {
+template <int D, int NT, int NTG, typename V>
+__device__ __forceinline__ void apply_gate_tile(const TileGate &tg, const PassGateP &g, V *buf,
+                                                const V *U, uint32_t ncls, bool needck, int tid) {
     constexpr int K = PassK<D, NT>::value;
     // full batches of K classes per thread, then the remainder one class per thread (no idle
     // batch slots in the tail)
     const uint32_t full = ncls / (uint32_t)(NTG * K) * (uint32_t)(NTG * K);
     if (g.kind == kPGeneral) {
-        gate_tile_general<D, K, NTG>(tg, g, buf, U, 0, full, ncls, needck, tid);
-        gate_tile_general<D, 1, NTG>(tg, g, buf, U, full, ncls, ncls, needck, tid);
+        gate_tile_general<D, K, NTG, V>(tg, g, buf, U, 0, full, ncls, needck, tid);
+        gate_tile_general<D, 1, NTG, V>(tg, g, buf, U, full, ncls, ncls, needck, tid);
     } else if (g.kind == kPPerm) {
-        gate_tile_monomial<D, K, NTG, true>(tg, g, buf, U, 0, full, ncls, needck, tid);
-        gate_tile_monomial<D, 1, NTG, true>(tg, g, buf, U, full, ncls, ncls, needck, tid);
+        gate_tile_monomial<D, K, NTG, true, V>(tg, g, buf, U, 0, full, ncls, needck, tid);
+        gate_tile_monomial<D, 1, NTG, true, V>(tg, g, buf, U, full, ncls, ncls, needck, tid);
     } else {
-        gate_tile_monomial<D, K, NTG, false>(tg, g, buf, U, 0, full, ncls, needck, tid);
-        gate_tile_monomial<D, 1, NTG, false>(tg, g, buf, U, full, ncls, ncls, needck, tid);
+        gate_tile_monomial<D, K, NTG, false, V>(tg, g, buf, U, 0, full, ncls, needck, tid);
+        gate_tile_monomial<D, 1, NTG, false, V>(tg, g, buf, U, full, ncls, ncls, needck, tid);
     }
 }
 
@@ -431,12 +443,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 // compute warps have finished it (after fence.proxy.async, so the bulk store sees their writes).
 // The compute warps form G consumer groups of NT/G threads; group g takes the CTA's tiles
 // g, g+G, ... (ping-pong), so one group's barrier waits overlap the other groups' work.
-template <int NT, int G>
+template <int NT, int G, typename V>
 __global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant__ PassParams p, int S, int TE) {
     constexpr int NTG = NT / G;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    double2 *bufs = reinterpret_cast<double2 *>(smem_raw);
-    double2 *Us = bufs + (size_t)S * TE;                       // the pass's matrices
+    V *bufs = reinterpret_cast<V *>(smem_raw);
+    V *Us = bufs + (size_t)S * TE;                             // the pass's matrices (in V's precision)
     uint32_t *moffs = reinterpret_cast<uint32_t *>(Us + p.upool);   // per gate: member offsets
     uint32_t *soffs = moffs + kMaxPassGates * kMaxDim;               // per gate: sigma-member offsets
     StageInfo *sinfo = reinterpret_cast<StageInfo *>(soffs + kMaxPassGates * kMaxDim);
@@ -447,7 +459,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant_
         for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&done[s], 1); }
         fence_mbar_init();
     }
-    for (int k = tid; k < p.upool; k += NT + 32) Us[k] = p.U[k];
+    for (int k = tid; k < p.upool; k += NT + 32) Us[k] = to_v<V>(p.U[k]);
     for (int k = tid; k < p.ngates * kMaxDim; k += NT + 32) {
         moffs[k] = (&p.moff_t[0][0])[k];
         soffs[k] = (&p.soff_t[0][0])[k];
@@ -467,8 +479,8 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant_
                 mbar_wait(&done[s], (uint32_t)((j / (uint64_t)S) & 1));
                 const StageInfo &si = sinfo[s];
                 for (int m = lane; m < p.M; m += 32)
-                    bulk_store(p.psi + si.ti.gbase + p.moff[m], bufs + (size_t)s * TE + (size_t)m * p.LT,
-                               si.ti.len * (uint32_t)sizeof(double2));
+                    bulk_store(reinterpret_cast<V *>(p.psi) + si.ti.gbase + p.moff[m],
+                               bufs + (size_t)s * TE + (size_t)m * p.LT, si.ti.len * (uint32_t)sizeof(V));
                 bulk_commit();
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 __syncwarp();
@@ -484,7 +496,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant_
     const int grp = tid / NTG, gtid = tid % NTG;
     for (uint64_t i = (uint64_t)grp; i < my; i += (uint64_t)G) {
         const int s = (int)(i % (uint64_t)S);
-        double2 *buf = bufs + (size_t)s * TE;
+        V *buf = bufs + (size_t)s * TE;
         // With several groups, consecutive tiles of a stage belong to different groups, so this
         // group may reach tile i while the stage's previous tile (i - S, another group) is not
         // even loaded: full[s] would still be in the phase before the one awaited, and a parity
@@ -508,13 +520,13 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant_
             tg.moff = moffs + gi * kMaxDim;
             tg.soff = soffs + gi * kMaxDim;
             const bool needck = g.flags != 0 || len < p.LT;
-            const double2 *U = Us + g.uoff;
+            const V *U = Us + g.uoff;
             switch (g.d) {
-                case 2: apply_gate_tile<2, NT, NTG>(tg, g, buf, U, g.ncls, needck, gtid); break;
-                case 3: apply_gate_tile<3, NT, NTG>(tg, g, buf, U, g.ncls, needck, gtid); break;
-                case 4: apply_gate_tile<4, NT, NTG>(tg, g, buf, U, g.ncls, needck, gtid); break;
-                case 5: apply_gate_tile<5, NT, NTG>(tg, g, buf, U, g.ncls, needck, gtid); break;
-                default: gate_tile_generic(tg, g, buf, U, g.ncls, needck, gtid, NTG); break;
+                case 2: apply_gate_tile<2, NT, NTG, V>(tg, g, buf, U, g.ncls, needck, gtid); break;
+                case 3: apply_gate_tile<3, NT, NTG, V>(tg, g, buf, U, g.ncls, needck, gtid); break;
+                case 4: apply_gate_tile<4, NT, NTG, V>(tg, g, buf, U, g.ncls, needck, gtid); break;
+                case 5: apply_gate_tile<5, NT, NTG, V>(tg, g, buf, U, g.ncls, needck, gtid); break;
+                default: gate_tile_generic<V>(tg, g, buf, U, g.ncls, needck, gtid, NTG); break;
             }
             compute_barrier(1 + grp, NTG);
         }
@@ -750,52 +762,57 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
     return p.ntiles > 0;
 }
 
-template <int NT, int G>
+template <int NT, int G, typename V>
 cudaError_t launch_pass_t(const PassParams &p, cudaStream_t st, const LaunchCfg &cfg) {
     const int S = cfg.pass_stages, TE = cfg.pass_tile;
     // size for the largest matrix pool so the attribute and the occupancy are set once per config
-    const size_t smem = (size_t)S * TE * sizeof(double2) + (size_t)kPoolC * sizeof(double2) +
+    const size_t smem = (size_t)S * TE * sizeof(V) + (size_t)kPoolC * sizeof(V) +
                         (size_t)2 * kMaxPassGates * kMaxDim * sizeof(uint32_t) +
                         (size_t)S * sizeof(StageInfo) + (size_t)2 * S * sizeof(uint64_t);
     static size_t configured = 0, occ_for = 0;
     static int occ = 1;
     if (configured < smem) {
-        cudaError_t e = cudaFuncSetAttribute(k_gate_pass<NT, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(k_gate_pass<NT, G, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         configured = smem;
     }
     if (occ_for != smem) {   // resident CTAs per SM at this smem size (persistent grid)
         int o = 1;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_gate_pass<NT, G>, NT + 32, smem) != cudaSuccess || o < 1) o = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_gate_pass<NT, G, V>, NT + 32, smem) != cudaSuccess || o < 1) o = 1;
         occ = o;
         occ_for = smem;
     }
     const uint64_t cap = (uint64_t)cfg.num_sms * (uint64_t)occ;
     const unsigned grid = (unsigned)(p.ntiles < cap ? p.ntiles : cap);
-    k_gate_pass<NT, G><<<grid, NT + 32, smem, st>>>(p, S, TE);
+    k_gate_pass<NT, G, V><<<grid, NT + 32, smem, st>>>(p, S, TE);
     return cudaGetLastError();
 }
 
 cudaError_t launch_pass(const PassParams &p, cudaStream_t st, const LaunchCfg &cfg) {
+    if (cfg.c64) return launch_pass_t<512, 2, float2>(p, st, cfg);   // complex64: one configuration
     int G = cfg.pass_groups;                      // one stage per group at least
     while (G > 1 && cfg.pass_stages < G) G /= 2;
     if (cfg.pass_threads >= 512) {
-        if (G >= 4) return launch_pass_t<512, 4>(p, st, cfg);
-        if (G == 2) return launch_pass_t<512, 2>(p, st, cfg);
-        return launch_pass_t<512, 1>(p, st, cfg);
+        if (G >= 4) return launch_pass_t<512, 4, double2>(p, st, cfg);
+        if (G == 2) return launch_pass_t<512, 2, double2>(p, st, cfg);
+        return launch_pass_t<512, 1, double2>(p, st, cfg);
     }
     if (cfg.pass_threads >= 384) {
-        if (G >= 2) return launch_pass_t<384, 2>(p, st, cfg);
-        return launch_pass_t<384, 1>(p, st, cfg);
+        if (G >= 2) return launch_pass_t<384, 2, double2>(p, st, cfg);
+        return launch_pass_t<384, 1, double2>(p, st, cfg);
     }
-    if (G >= 2) return launch_pass_t<256, 2>(p, st, cfg);
-    return launch_pass_t<256, 1>(p, st, cfg);
+    if (G >= 2) return launch_pass_t<256, 2, double2>(p, st, cfg);
+    return launch_pass_t<256, 1, double2>(p, st, cfg);
 }
 
 cudaError_t run_pass(const Register &reg, const std::vector<GateSpec> &gates, const PassPlan &pp, double2 *psi,
                      cudaStream_t st, const LaunchCfg &cfg, bool *handled, double *touched) {
     static thread_local PassParams p;   // ~23 KB; parameters are copied at launch
     *handled = build_pass(reg, gates, pp, psi, cfg.pass_tile, p, touched);
+    // complex64 (8-byte elements): every bulk copy must start at a 16-byte aligned address and
+    // move a multiple of 16 bytes; tile runs are multiples of L = b_{m0} and start at multiples
+    // of L, so an even L suffices (the stage needs the tile plus the fp32 matrix pool)
+    if (*handled && cfg.c64 && (p.L % 2 != 0 || p.LT % 2 != 0)) *handled = false;
     if (!*handled) return cudaSuccess;
     return launch_pass(p, st, cfg);
 }

@@ -182,7 +182,8 @@ static sv_status launch_pass_on(sv_handle h, const std::vector<GateSpec> &specs,
             cudaEventRecord(b, h->stream);
             // algorithmic bytes per SURVEY.md §8(d): 32 B per touched amplitude of every gate the
             // pass applies; the pass itself moves the local state once (16 B read + 16 B write)
-            h->prof.push_back({a, b, 32.0 * touched, touched, 32.0 * (double)h->local.D});
+            const double bpu = 2.0 * (double)h->elem;     // one read + one write per amplitude
+            h->prof.push_back({a, b, bpu * touched, touched, bpu * (double)h->local.D});
         }
         return SV_OK;
     }
@@ -234,7 +235,6 @@ sv_status run_local_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_t 
         }
     }
     std::vector<PassPlan> passes;
-    if ((flags & SV_BLOCK) && h->c64) flags = (flags & ~SV_BLOCK) | SV_FUSE;   // pass kernel: c128 only
     if (flags & SV_BLOCK) {
         if (h->cfg.pass_merge) specs = merge_commuting(specs, 64);
         passes = plan_passes(h->local, specs, (uint64_t)h->cfg.pass_tile, h->cfg.pass_gates, h->cfg.pass_window);

@@ -64,10 +64,10 @@ def test_random_sweep_c64(P):
         _, gates = random_circuit(64_000 + s, dims, 40, max_ctrl=2)
         psi0 = random_state(int(np.prod(dims)), s)
         ref = O2.run(dims, gates, psi0)
-        for kernel in (1, 2):
-            got, _ = run_c64(P, dims, gates, psi0, kernel=kernel)
+        for kernel, block in ((1, False), (2, False), (0, True)):
+            got, _ = run_c64(P, dims, gates, psi0, kernel=kernel, block=block)
             # input rounding to fp32 adds at most sqrt(2) u per amplitude (||.||_2 <= sqrt(2) u)
-            assert np.linalg.norm(got - ref) <= bound(gates, dims, np.sqrt(2) * U32)
+            assert np.linalg.norm(got - ref) <= bound(gates, dims, np.sqrt(2) * U32), (kernel, block)
 
 
 def test_labelled_permutations_bit_exact_c64(P):
@@ -85,9 +85,9 @@ def test_labelled_permutations_bit_exact_c64(P):
         gates.append(Gate(t, ctrl, vals, permutation_matrix(rng.permutation(dims[t]))))
     lab = labelled_state(0, D)
     ref = O2.run(dims, gates, lab)
-    for kernel in (1, 2):
-        got, _ = run_c64(P, dims, gates, lab, kernel=kernel)
-        assert np.array_equal(got, ref)
+    for kernel, block in ((1, False), (2, False), (0, True)):      # block: the c64 pass kernel (L = 60)
+        got, _ = run_c64(P, dims, gates, lab, kernel=kernel, block=block)
+        assert np.array_equal(got, ref), (kernel, block)
 
 
 def test_ghz_c64_exact_to_fp32(P):
@@ -110,3 +110,22 @@ def test_c64_state_is_half_the_bytes(P):
     st.close()
     D = 3 ** 12
     assert used < 16 * D          # 8 B per amplitude (+ small scratch), not 16
+
+
+def test_c64_pass_kernel_used_and_matches(P):
+    """The complex64 pass kernel runs when the tile is 16-byte aligned (even L = b_{m0}): a
+    c4-shaped register (L = 100) in block mode launches fewer kernels than gates and matches the
+    fp64 oracle within the fp32 bound; an odd-L register (c3 shape, L = 81) falls back to the
+    single-gate kernels with the same result quality."""
+    for cfg, nq in ((4, 1), (3, 4)):
+        dims, gates = config_circuit(cfg, nqubits=nq)
+        gates = gates[:200]
+        ref = O2.run(dims, gates)
+        with P.State(dims, dtype="c64") as st:
+            n0 = st.info().kernel_launches
+            st.apply_circuit(gates, block=True)
+            got = st.amplitudes()
+            launched = st.info().kernel_launches - n0
+        assert np.linalg.norm(got - ref) <= bound(gates, dims)
+        if cfg == 4:
+            assert launched < len(gates) // 4, launched
