@@ -90,6 +90,7 @@ sv_status state_init_device(sv_handle h, int device, void *cuda_stream, void *ex
         h->own_stream = true;
     }
     h->cfg.c64 = h->c64 ? 1 : 0;
+    if (h->c64) h->cfg.pass_tile = 8192;   // 8-byte elements: twice the amplitudes per stage (c4: 1.78 -> 1.25 s)
     const uint64_t bytes = h->local.D * h->elem;
     if (ext) {
         if (ext_bytes < bytes || ((uintptr_t)ext & 15))

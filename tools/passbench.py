@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--gates", default="24,8,4,2")
     ap.add_argument("--groups", default="1")
     ap.add_argument("--windows", default="64")
+    ap.add_argument("--dtype", default="c128", choices=["c128", "c64"])
     ap.add_argument("--reps", type=int, default=1)
     args = ap.parse_args()
     import torch
@@ -32,14 +33,14 @@ def main():
     dims, gates = config_circuit(args.config, ngates=args.ngates, nqubits=args.nqubits)
     T = sum(int(P.plan_gate(dims, g.target, g.U, g.ctrl, g.vals).touched) for g in gates)
     D = int(np.prod(dims, dtype=object))
-    st = P.State(dims)
+    st = P.State(dims, dtype=args.dtype)
     ext = torch.cuda.ExternalStream(st.info().cuda_stream)
     ga = P.sv._GateArray(gates)
     cases = [("noblock", 0, 0, 0, 0)]
     for te, s, nt, ng, gr, wi in itertools.product(*[[int(x) for x in a.split(",")] for a in
                                                      (args.tiles, args.stages, args.threads, args.gates, args.groups,
                                                       args.windows)]):
-        if te * 16 * s > 210 * 1024 or s < gr or (gr == 3 and nt % 96):
+        if te * (16 if args.dtype == 'c128' else 8) * s > 210 * 1024 or s < gr or (gr == 3 and nt % 96):
             continue
         cases.append(("block", te, s, nt, ng, gr, wi))
     for kind, te, s, nt, ng, *rest in cases:
