@@ -289,3 +289,28 @@ def test_bench_reference_arm_line():
     assert d["impl"] == "reference" and d["value"] > 0 and d["steps"] == 1
     assert d["config"]["dims_q0_first"] == [5, 5, 4, 4, 4, 4] + [3] * 6 + [2] * 10
     assert d["cpu_baseline"]["kind"] == "oracle" and d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_block_planner_order_is_equivalent():
+    """sv_block_plan (the SV_BLOCK pass planner): gates are pulled into a pass only past gates
+    they commute with, so applying them in the planner's order gives the same state (O-2) —
+    with diagonal gates, whose commutation with gates controlled on their digit the planner
+    uses (R19).  Every gate appears exactly once and pass ids are non-decreasing."""
+    rng = np.random.default_rng(77)
+    for s in range(20):
+        dims = [int(x) for x in rng.integers(2, 5, size=6)]
+        _, gates = random_circuit(900 + s, dims, 60, max_ctrl=2)
+        extra = []
+        for g in gates:
+            extra.append(g)
+            if rng.random() < 0.3:
+                t = int(rng.integers(len(dims)))
+                extra.append(Gate(t, (), (), np.diag(np.exp(1j * rng.random(dims[t])))))
+        gates = extra
+        order, pid, tiles = P.block_plan(dims, gates, 256)
+        assert sorted(order.tolist()) == list(range(len(gates)))
+        assert all(np.diff(pid) >= 0)
+        psi0 = random_state(int(np.prod(dims)), 1000 + s)
+        ref = O2.run(dims, gates, psi0)
+        got = O2.run(dims, [gates[i] for i in order], psi0)
+        assert np.max(np.abs(got - ref)) < 1e-13
