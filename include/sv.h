@@ -52,9 +52,10 @@ extern "C" {
 typedef struct sv_state_s *sv_handle;
 
 /* Element type of the state.  SV_C128: complex128 (the BASELINE configs).  SV_C64: complex64
- * (8 B per amplitude, arithmetic in fp32; single-GPU handles only -- sharded SV_C64 returns
- * SV_ERR_UNSUPPORTED -- and SV_BLOCK falls back to single-gate passes).  The ABI's amplitude
- * buffers and matrices are always doubles; SV_C64 rounds them on the way in. */
+ * (8 B per amplitude, arithmetic in fp32, also sharded: exchanges move fp32 pairs; SV_BLOCK
+ * passes run when the tile's bulk copies are 16-byte aligned, i.e. b_{m0} is even, else the
+ * gates fall back to single-gate passes).  The ABI's amplitude buffers and matrices are always
+ * doubles; SV_C64 rounds them on the way in and widens them on the way out. */
 typedef enum { SV_C128 = 0, SV_C64 = 1 } sv_dtype;
 
 typedef enum {

@@ -143,9 +143,10 @@ __global__ void __launch_bounds__(kNormThreads) k_norm_final(const double *parti
 // has one member on this rank and one on the partner, at the same local index.
 // psi_loc <- a psi_loc + b psi_partner where the local control digits match.
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_combine(double2 *__restrict__ loc,
-                                                 const double2 *__restrict__ par, uint64_t n,
-                                                 uint64_t base, double2 a, double2 b,
+template <typename V>
+__global__ void __launch_bounds__(256) k_combine(V *__restrict__ loc,
+                                                 const V *__restrict__ par, uint64_t n,
+                                                 uint64_t base, V a, V b,
                                                  const __grid_constant__ CombineCtrl cc) {
     const uint64_t step = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += step) {
@@ -157,8 +158,8 @@ __global__ void __launch_bounds__(256) k_combine(double2 *__restrict__ loc,
             ok = ok && (r2 == cc.v[c]);
         }
         if (ok) {
-            const double2 x = loc[i], z = par[i];
-            double2 y = make_double2(0.0, 0.0);
+            const V x = loc[i], z = par[i];
+            V y = cz<V>();
             cfma(y, a, x);
             cfma(y, b, z);
             loc[i] = y;
@@ -231,11 +232,16 @@ int norm_parts() { return kNormParts; }
 
 cudaError_t launch_combine(double2 *loc, const double2 *partner, uint64_t n, uint64_t base,
                            double2 a, double2 b, const CombineCtrl &cc, cudaStream_t st,
-                           uint64_t *launches) {
+                           uint64_t *launches, bool c64) {
     if (n == 0) return cudaSuccess;
     const uint64_t want = (n + 255) / 256;
     const unsigned blocks = (unsigned)(want < 148 * 16 ? want : 148 * 16);
-    k_combine<<<blocks, 256, 0, st>>>(loc, partner, n, base, a, b, cc);
+    if (c64)       // complex64 slices: the same combine in fp32 (loc / partner point at float2)
+        k_combine<float2><<<blocks, 256, 0, st>>>(reinterpret_cast<float2 *>(loc),
+                                                  reinterpret_cast<const float2 *>(partner), n, base,
+                                                  to_v<float2>(a), to_v<float2>(b), cc);
+    else
+        k_combine<double2><<<blocks, 256, 0, st>>>(loc, partner, n, base, a, b, cc);
     if (launches) ++*launches;
     return cudaGetLastError();
 }

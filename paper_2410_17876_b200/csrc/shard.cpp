@@ -18,6 +18,7 @@
 
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "nccl.h"
 #include "shard.h"
@@ -125,6 +126,11 @@ std::vector<int> ranks_of(const ShardCtx *c) {
 
 double2 *slice_of(const ShardCtx *c, int r) { return c->loopback() ? c->slices[r] : c->slices[0]; }
 
+// element `off` of a state buffer whose elements are `elem` bytes (complex128 or complex64)
+inline double2 *at(double2 *p, uint64_t off, size_t elem) {
+    return reinterpret_cast<double2 *>(reinterpret_cast<char *>(p) + off * elem);
+}
+
 CombineCtrl local_ctrl(const Register &local, const std::vector<CtrlSpec> &ctrl) {
     CombineCtrl cc;
     std::memset(&cc, 0, sizeof(cc));
@@ -154,15 +160,17 @@ sv_status exchange_nccl(sv_handle h, const GateSpec &g, const ShardAction &a) {
         const int sb = (int)(k & 1);
         if (k >= 2) cudaStreamWaitEvent(c->comm_stream, c->ev_done[sb], 0);   // stage free again
         ncclResult_t r = nccl().GroupStart();
-        if (r == ncclSuccess) r = nccl().Send(c->slices[0] + off, 2 * len, ncclFloat64, a.partner, c->comm, c->comm_stream);
-        if (r == ncclSuccess) r = nccl().Recv(c->stage[sb], 2 * len, ncclFloat64, a.partner, c->comm, c->comm_stream);
+        const ncclDataType_t ty = h->c64 ? ncclFloat32 : ncclFloat64;     // 2 reals per amplitude
+        if (r == ncclSuccess) r = nccl().Send(at(c->slices[0], off, h->elem), 2 * len, ty, a.partner, c->comm, c->comm_stream);
+        if (r == ncclSuccess) r = nccl().Recv(c->stage[sb], 2 * len, ty, a.partner, c->comm, c->comm_stream);
         ncclResult_t r2 = nccl().GroupEnd();
         if (r != ncclSuccess) return nccl_fail(h, r, "ncclSend/Recv");
         if (r2 != ncclSuccess) return nccl_fail(h, r2, "ncclGroupEnd");
         e = cudaEventRecord(c->ev_recv[sb], c->comm_stream);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(h->stream, c->ev_recv[sb], 0);
         if (e == cudaSuccess)
-            e = launch_combine(c->slices[0] + off, c->stage[sb], len, off, A, B, cc, h->stream, &h->launches);
+            e = launch_combine(at(c->slices[0], off, h->elem), c->stage[sb], len, off, A, B, cc, h->stream,
+                               &h->launches, h->c64);
         if (e == cudaSuccess) e = cudaEventRecord(c->ev_done[sb], h->stream);
         if (e != cudaSuccess) return cuda_fail_h(h, e, "exchange chunk");
     }
@@ -180,15 +188,17 @@ sv_status exchange_loopback(sv_handle h, const GateSpec &g, int r, const ShardAc
     const uint64_t L = h->local.D;
     for (uint64_t off = 0; off < L; off += c->chunk) {
         const uint64_t len = (L - off < c->chunk) ? L - off : c->chunk;
-        cudaError_t e = cudaMemcpyAsync(c->stage[0], c->slices[r] + off, len * sizeof(double2),
+        cudaError_t e = cudaMemcpyAsync(c->stage[0], at(c->slices[r], off, h->elem), len * h->elem,
                                         cudaMemcpyDeviceToDevice, h->stream);
         if (e == cudaSuccess)
-            e = cudaMemcpyAsync(c->stage[1], c->slices[p] + off, len * sizeof(double2),
+            e = cudaMemcpyAsync(c->stage[1], at(c->slices[p], off, h->elem), len * h->elem,
                                 cudaMemcpyDeviceToDevice, h->stream);
         if (e == cudaSuccess)
-            e = launch_combine(c->slices[r] + off, c->stage[1], len, off, Ar, Br, cc, h->stream, &h->launches);
+            e = launch_combine(at(c->slices[r], off, h->elem), c->stage[1], len, off, Ar, Br, cc, h->stream,
+                               &h->launches, h->c64);
         if (e == cudaSuccess)
-            e = launch_combine(c->slices[p] + off, c->stage[0], len, off, Ap, Bp, cc, h->stream, &h->launches);
+            e = launch_combine(at(c->slices[p], off, h->elem), c->stage[0], len, off, Ap, Bp, cc, h->stream,
+                               &h->launches, h->c64);
         if (e != cudaSuccess) return cuda_fail_h(h, e, "loopback exchange");
     }
     ++h->exchanges;
@@ -311,9 +321,9 @@ sv_status shard_reset(sv_handle h, uint64_t idx) {
     for (int r : ranks_of(c)) {
         cudaError_t e;
         if (r == owner)
-            e = launch_set_basis(slice_of(c, r), L, idx - (uint64_t)owner * L, h->stream, &h->launches);
+            e = launch_set_basis(slice_of(c, r), L, idx - (uint64_t)owner * L, h->stream, &h->launches, h->c64);
         else
-            e = cudaMemsetAsync(slice_of(c, r), 0, L * sizeof(double2), h->stream);
+            e = cudaMemsetAsync(slice_of(c, r), 0, L * h->elem, h->stream);
         if (e != cudaSuccess) return cuda_fail_h(h, e, "sharded reset");
     }
     return SV_OK;
@@ -326,6 +336,20 @@ sv_status shard_set_amplitudes(sv_handle h, uint64_t first, uint64_t count, cons
         const uint64_t lo = (uint64_t)r * L, hi = lo + L;
         const uint64_t a = first > lo ? first : lo, b = (first + count) < hi ? first + count : hi;
         if (a >= b) continue;
+        if (h->c64) {                        // complex64: round the ABI's doubles on the host
+            const uint64_t chunk = 1ull << 22;
+            std::vector<float2> tmp((size_t)((b - a) < chunk ? (b - a) : chunk));
+            for (uint64_t o = a; o < b; o += chunk) {
+                const uint64_t n = (b - o) < chunk ? b - o : chunk;
+                for (uint64_t i = 0; i < n; ++i)
+                    tmp[i] = make_float2((float)in[2 * (o - first + i)], (float)in[2 * (o - first + i) + 1]);
+                cudaError_t e = cudaMemcpyAsync(at(slice_of(c, r), o - lo, h->elem), tmp.data(), n * h->elem,
+                                                cudaMemcpyHostToDevice, h->stream);
+                if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+                if (e != cudaSuccess) return cuda_fail_h(h, e, "sharded upload");
+            }
+            continue;
+        }
         cudaError_t e = cudaMemcpyAsync(slice_of(c, r) + (a - lo), in + 2 * (a - first),
                                         (b - a) * sizeof(double2), cudaMemcpyHostToDevice, h->stream);
         if (e != cudaSuccess) return cuda_fail_h(h, e, "sharded upload");
@@ -342,18 +366,46 @@ sv_status shard_amplitudes(sv_handle h, uint64_t first, uint64_t count, double *
         const uint64_t lo = (uint64_t)r * L, hi = lo + L;
         const uint64_t a = first > lo ? first : lo, b = (first + count) < hi ? first + count : hi;
         if (a >= b) continue;
-        if (c->loopback()) {
+        if (c->loopback() && !h->c64) {
             cudaError_t e = cudaMemcpyAsync(out + 2 * (a - first), c->slices[r] + (a - lo),
                                             (b - a) * sizeof(double2), cudaMemcpyDeviceToHost, h->stream);
             if (e != cudaSuccess) return cuda_fail_h(h, e, "sharded readback");
             continue;
         }
+        if (c->loopback()) {                 // complex64: widen to the ABI's doubles on the host
+            const uint64_t chunk = 1ull << 22;
+            std::vector<float2> tmp((size_t)((b - a) < chunk ? (b - a) : chunk));
+            for (uint64_t o = a; o < b; o += chunk) {
+                const uint64_t n = (b - o) < chunk ? b - o : chunk;
+                cudaError_t e = cudaMemcpyAsync(tmp.data(), at(c->slices[r], o - lo, h->elem), n * h->elem,
+                                                cudaMemcpyDeviceToHost, h->stream);
+                if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+                if (e != cudaSuccess) return cuda_fail_h(h, e, "sharded readback");
+                for (uint64_t i = 0; i < n; ++i) {
+                    out[2 * (o - first + i)] = tmp[i].x;
+                    out[2 * (o - first + i) + 1] = tmp[i].y;
+                }
+            }
+            continue;
+        }
         for (uint64_t p = a; p < b; p += c->chunk) {     // owner broadcasts, chunk by chunk
             const uint64_t len = (b - p < c->chunk) ? b - p : c->chunk;
-            const void *src = (r == c->rank) ? (const void *)(c->slices[0] + (p - lo)) : nullptr;
+            const void *src = (r == c->rank) ? (const void *)at(c->slices[0], p - lo, h->elem) : nullptr;
             ncclResult_t rr = nccl().Broadcast(src ? src : c->stage[0], c->stage[0], 2 * len,
-                                               ncclFloat64, r, c->comm, h->stream);
+                                               h->c64 ? ncclFloat32 : ncclFloat64, r, c->comm, h->stream);
             if (rr != ncclSuccess) return nccl_fail(h, rr, "ncclBroadcast");
+            if (h->c64) {
+                std::vector<float2> tmp((size_t)len);
+                cudaError_t e = cudaMemcpyAsync(tmp.data(), c->stage[0], len * h->elem, cudaMemcpyDeviceToHost,
+                                                h->stream);
+                if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+                if (e != cudaSuccess) return cuda_fail_h(h, e, "sharded readback");
+                for (uint64_t i = 0; i < len; ++i) {
+                    out[2 * (p - first + i)] = tmp[i].x;
+                    out[2 * (p - first + i) + 1] = tmp[i].y;
+                }
+                continue;
+            }
             cudaError_t e = cudaMemcpyAsync(out + 2 * (p - first), c->stage[0], len * sizeof(double2),
                                             cudaMemcpyDeviceToHost, h->stream);
             if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
@@ -411,7 +463,7 @@ sv_status sv_create_sharded(const int32_t *dims, int32_t n, sv_dtype dt, int32_t
     *out = nullptr;
     if (nranks == 1 && rank <= 0)
         return sv_create_ex(dims, n, dt, device, cuda_stream, nullptr, 0, out);
-    if (dt != SV_C128) return fail_msg(SV_ERR_UNSUPPORTED, "only complex128 is implemented");
+    if (dt != SV_C128 && dt != SV_C64) return fail_msg(SV_ERR_INVALID_ARG, "unknown dtype");
     if (nranks < 1 || (nranks & (nranks - 1))) return fail_msg(SV_ERR_INVALID_ARG, "nranks must be a power of two");
     if (rank < -1 || rank >= nranks) return fail_msg(SV_ERR_INVALID_ARG, "rank out of range");
     sv_handle h = new (std::nothrow) sv_state_s();
@@ -426,6 +478,8 @@ sv_status sv_create_sharded(const int32_t *dims, int32_t n, sv_dtype dt, int32_t
         if (dims[k] != 2) { delete h; return fail_msg(SV_ERR_UNSUPPORTED, "sharded digits must be qubits"); }
     s = make_register(dims, n - sh, &h->local, err);
     if (s != SV_OK) { delete h; return s; }
+    h->c64 = dt == SV_C64;
+    h->elem = h->c64 ? sizeof(float2) : sizeof(double2);
     ShardCtx *c = new ShardCtx();
     c->P = nranks;
     c->s = sh;
@@ -439,7 +493,7 @@ sv_status sv_create_sharded(const int32_t *dims, int32_t n, sv_dtype dt, int32_t
     if (c->loopback()) {
         for (int r = 1; r < nranks && e == cudaSuccess; ++r) {
             double2 *p = nullptr;
-            e = cudaMalloc(&p, L * sizeof(double2));
+            e = cudaMalloc(&p, L * h->elem);
             if (e == cudaSuccess) c->slices.push_back(p);
         }
         if (e != cudaSuccess) { cudaGetLastError(); state_free(h); return fail_msg(SV_ERR_NOMEM, "slice allocation"); }
@@ -455,7 +509,7 @@ sv_status sv_create_sharded(const int32_t *dims, int32_t n, sv_dtype dt, int32_t
     c->chunk = ch ? strtoull(ch, nullptr, 10) : (16ull << 20);     // 16 Mi amplitudes = 256 MiB
     if (c->chunk == 0) c->chunk = 16ull << 20;
     if (c->chunk > L) c->chunk = L;
-    for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaMalloc(&c->stage[i], c->chunk * sizeof(double2));
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaMalloc(&c->stage[i], c->chunk * h->elem);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_scalar, sizeof(double));
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking);
     for (int i = 0; i < 2 && e == cudaSuccess; ++i) {

@@ -44,6 +44,6 @@ struct CombineCtrl {
 };
 cudaError_t launch_combine(double2 *loc, const double2 *partner, uint64_t n, uint64_t base,
                            double2 a, double2 b, const CombineCtrl &cc, cudaStream_t st,
-                           uint64_t *launches);
+                           uint64_t *launches, bool c64 = false);
 
 }  // namespace svi

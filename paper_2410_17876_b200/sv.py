@@ -183,18 +183,19 @@ class State:
 
     @classmethod
     def sharded(cls, dims, rank: int, nranks: int, nccl_id: bytes | None, device: int = 0,
-                stream=None) -> "State":
+                stream=None, dtype: str = "c128") -> "State":
         d = _i32(dims)
         h = _h()
         idbuf = C.create_string_buffer(bytes(nccl_id), 128) if nccl_id else None
-        _check(_lib.sv_create_sharded(d.ctypes.data_as(_i32p), d.size, SV_C128, int(rank), int(nranks),
+        dt = {"c128": SV_C128, "c64": SV_C64}[dtype]
+        _check(_lib.sv_create_sharded(d.ctypes.data_as(_i32p), d.size, dt, int(rank), int(nranks),
                                       idbuf, int(device), C.c_void_p(stream) if stream else None,
                                       C.byref(h)))
         return cls(dims, _handle=h)
 
     @classmethod
-    def loopback(cls, dims, nranks: int, device: int = 0) -> "State":
-        return cls.sharded(dims, -1, nranks, None, device)
+    def loopback(cls, dims, nranks: int, device: int = 0, dtype: str = "c128") -> "State":
+        return cls.sharded(dims, -1, nranks, None, device, dtype=dtype)
 
     def close(self):
         if getattr(self, "_h", None):

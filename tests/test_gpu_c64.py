@@ -129,3 +129,39 @@ def test_c64_pass_kernel_used_and_matches(P):
         assert np.linalg.norm(got - ref) <= bound(gates, dims)
         if cfg == 4:
             assert launched < len(gates) // 4, launched
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_loopback_sharded_c64(P, nranks):
+    """Sharded complex64 (loopback transport on one GPU): sharded targets exchange fp32 slices,
+    sharded controls predicate, local runs use the complex64 pass kernel; against the fp64
+    oracle within the fp32 bound, and labelled permutations bit-exact across shards."""
+    import os
+    os.environ["SV_EXCHANGE_CHUNK"] = "1000"
+    try:
+        from sv_inputs import hadamard, fourier
+        dims = [4, 5, 2, 2, 2, 2, 2, 2]
+        n, D = len(dims), int(np.prod(dims))
+        rng = np.random.default_rng(40 + nranks)
+        _, gates = random_circuit(640 + nranks, dims, 100, max_ctrl=2)
+        gates += [Gate(7, (), (), hadamard()), Gate(6, (0,), (2,), haar_unitary(2, rng)),
+                  Gate(5, (7,), (1,), shift_x(2, 1)), Gate(1, (6, 7), (1, 0), fourier(5))]
+        psi0 = random_state(D, 9)
+        ref = O2.run(dims, gates, psi0)
+        for block in (False, True):
+            with P.State.loopback(dims, nranks, dtype="c64") as st:
+                st.set_amplitudes(0, psi0)
+                st.apply_circuit(gates, block=block)
+                got = st.amplitudes()
+                assert st.info().exchanges > 0
+            assert np.linalg.norm(got - ref) <= bound(gates, dims, np.sqrt(2) * U32), block
+        perm = [Gate(7, (), (), shift_x(2, 1)), Gate(6, (2,), (1,), shift_x(2, 1)),
+                Gate(1, (7,), (1,), shift_x(5, 3)), Gate(5, (6, 0), (0, 1), shift_x(2, 1))]
+        lab = labelled_state(0, D)
+        with P.State.loopback(dims, nranks, dtype="c64") as st:
+            st.set_amplitudes(0, lab)
+            st.apply_circuit(perm, block=True)
+            got = st.amplitudes()
+        assert np.array_equal(got, O2.run(dims, perm, lab))
+    finally:
+        del os.environ["SV_EXCHANGE_CHUNK"]
