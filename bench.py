@@ -240,7 +240,7 @@ def main():
         if rank == 0:
             idt.copy_(torch.frombuffer(bytearray(P.nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(idt, 0)
-        st = P.State.sharded(dims, rank, world, bytes(idt.cpu().numpy()), device=local_rank)
+        st = P.State.sharded(dims, rank, world, bytes(idt.cpu().numpy()), device=local_rank, dtype=args.dtype)
     else:
         st = P.State(dims, device=local_rank, dtype=args.dtype)
     st.set_option(P.sv.SV_OPT_KERNEL, args.kernel)
