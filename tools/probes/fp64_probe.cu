@@ -1,6 +1,7 @@
 // fp64_probe.cu — measured FP64 throughput on this GPU: DFMA (vector pipe) and the FP64 MMA
 // shapes (mma.sync ... .f64) that sm_100a accepts.  Used to decide whether general gates in
-// the pass kernel should go through the FP64 tensor path.  nvcc -arch=sm_100a -O3.
+// the pass kernel should go through the FP64 tensor path.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o fp64_probe fp64_probe.cu
 #include <cstdio>
 #include <cuda_runtime.h>
 

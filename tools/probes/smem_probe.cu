@@ -1,6 +1,7 @@
 // smem_probe.cu — shared-memory throughput of the pass kernel's access pattern: every thread
 // gathers K classes of d = 3 complex128 amplitudes (stride st) and scatters them permuted,
 // over a 3072-amplitude tile, with a CTA barrier per "gate".  Reports bytes/clk/SM.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o smem_probe smem_probe.cu
 #include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
