@@ -769,20 +769,20 @@ cudaError_t launch_pass_t(const PassParams &p, cudaStream_t st, const LaunchCfg 
     const size_t smem = (size_t)S * TE * sizeof(V) + (size_t)kPoolC * sizeof(V) +
                         (size_t)2 * kMaxPassGates * kMaxDim * sizeof(uint32_t) +
                         (size_t)S * sizeof(StageInfo) + (size_t)2 * S * sizeof(uint64_t);
-    static size_t configured = 0, occ_for = 0;
-    static int occ = 1;
-    if (configured < smem) {
+    static LaunchAttr attr;
+    const int dv = current_device_slot();
+    if (attr.configured[dv] < smem) {
         cudaError_t e = cudaFuncSetAttribute(k_gate_pass<NT, G, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        configured = smem;
+        attr.configured[dv] = smem;
     }
-    if (occ_for != smem) {   // resident CTAs per SM at this smem size (persistent grid)
+    if (attr.occ_for[dv] != smem) {   // resident CTAs per SM at this smem size (persistent grid)
         int o = 1;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_gate_pass<NT, G, V>, NT + 32, smem) != cudaSuccess || o < 1) o = 1;
-        occ = o;
-        occ_for = smem;
+        attr.occ[dv] = o;
+        attr.occ_for[dv] = smem;
     }
-    const uint64_t cap = (uint64_t)cfg.num_sms * (uint64_t)occ;
+    const uint64_t cap = (uint64_t)cfg.num_sms * (uint64_t)attr.occ[dv];
     const unsigned grid = (unsigned)(p.ntiles < cap ? p.ntiles : cap);
     k_gate_pass<NT, G, V><<<grid, NT + 32, smem, st>>>(p, S, TE);
     return cudaGetLastError();

@@ -455,12 +455,13 @@ sv_status sparse_run(sv_sparse_handle h, const std::vector<GateSpec> &specs) {
         if (e != cudaSuccess) return sp_cuda(h, e, "sparse gate table");
         h->gp_host = sm;
     }
-    static bool configured = false;
-    if (!configured) {
+    static LaunchAttr attr;                  // per device (cudaFuncSetAttribute is per device)
+    const int dv = current_device_slot();
+    if (!attr.configured[dv]) {
         cudaError_t e = cudaFuncSetAttribute(k_sparse_small<1024, kSmallCap>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)small_smem<kSmallCap>());
         if (e != cudaSuccess) return sp_cuda(h, e, "sparse small attribute");
-        configured = true;
+        attr.configured[dv] = 1;
     }
     size_t i = 0;
     while (i < ps.size()) {

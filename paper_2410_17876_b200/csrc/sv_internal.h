@@ -99,6 +99,20 @@ __host__ __device__ __forceinline__ uint64_t insert_digits(uint64_t f, int nrem,
 
 enum GateKind : int32_t { kGeneral = 0, kMonomial = 1 };
 
+// One-time launch configuration of a kernel (dynamic shared-memory attribute, resident CTAs per
+// SM), per device: cudaFuncSetAttribute applies to the current device only.
+struct LaunchAttr {
+    static constexpr int kDevices = 64;
+    size_t configured[kDevices] = {};
+    size_t occ_for[kDevices] = {};
+    int occ[kDevices] = {};
+};
+inline int current_device_slot() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) dev = 0;
+    return dev % LaunchAttr::kDevices;
+}
+
 // complex element types: V = double2 (complex128, SV_C128) or float2 (complex64, SV_C64);
 // the arithmetic is done in V's precision (the paper fixes none; R11).
 template <typename V> struct RealOf;

@@ -485,21 +485,21 @@ cudaError_t launch_tiled_k(const TileParams<MD, V> &p, const LaunchCfg &cfg, cud
     const int S = cfg.tile_stages, TE = cfg.tile_elems;
     const size_t smem = (size_t)S * TE * sizeof(V) + (size_t)S * (TE / 32) * sizeof(Piece) +
                         (size_t)((S + 1) & ~1) * sizeof(uint32_t) + (size_t)S * sizeof(uint64_t);
-    static size_t configured = 0;
-    static size_t occ_for = 0;
-    static int occ = 1;
+    static LaunchAttr attr;
+    const int dv = current_device_slot();
     auto kfn = k_gate_tiled<DIM, MD, MODE, KIND, V>;
-    if (configured < smem) {
+    if (attr.configured[dv] < smem) {
         cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        configured = smem;
+        attr.configured[dv] = smem;
     }
-    if (occ_for != smem) {   // resident CTAs per SM for this smem size (persistent grid)
+    if (attr.occ_for[dv] != smem) {   // resident CTAs per SM for this smem size (persistent grid)
         int o = 1;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kfn, kTileThreads, smem) != cudaSuccess || o < 1) o = 1;
-        occ = o;
-        occ_for = smem;
+        attr.occ[dv] = o;
+        attr.occ_for[dv] = smem;
     }
+    const int occ = attr.occ[dv];
     const int per_sm = cfg.ctas_per_sm < occ ? cfg.ctas_per_sm : occ;
     const uint64_t cap = (uint64_t)cfg.num_sms * per_sm;
     const unsigned grid = (unsigned)(p.ntiles < cap ? p.ntiles : cap);
