@@ -227,7 +227,7 @@ def main():
     dims, gates = config_circuit(args.config, ngates=args.ngates)
     # circuit-driver mode per workload (measured, profiles/r01/passbench_*): multi-gate passes
     # (SV_BLOCK) on c1-c4, plus a cached CUDA graph for the launch-bound c1/c2; sharded runs
-    # use single-gate passes with pair fusion on each slice.
+    # run the same passes on each slice between the pairwise exchanges of sharded targets.
     fuse = not args.no_fuse
     block = args.block or (args.config in (1, 2, 3, 4) and not args.no_block)
     graph = args.graph or (args.config in (1, 2) and not args.no_graph)
