@@ -455,3 +455,41 @@ def test_pass_groups_stage_reuse_regression(P):
     finally:
         for st in states:
             st.close()
+
+
+MODES = [dict(), dict(fuse=True), dict(block=True), dict(block=True, graph=True), dict(fuse=True, graph=True)]
+
+
+@pytest.mark.parametrize("mode", range(len(MODES)))
+def test_edge_cases_every_driver_mode(P, mode):
+    """Degenerate inputs through every circuit-driver mode against the oracle: the empty
+    circuit, one-qudit registers (d = 2 and 16), identity gates (no class to visit), a d = 16
+    qudit among small ones (the generic path inside passes), gates with 4 controls (the pass
+    kernel's maximum) and 5 controls (a single-gate fallback)."""
+    kw = MODES[mode]
+    rng = np.random.default_rng(mode)
+    # empty circuit: e_0 stays e_0
+    dims = [3, 2, 4]
+    got, nrm, _ = run_gpu(P, dims, [], **kw)
+    assert got[0] == 1.0 and np.count_nonzero(got) == 1 and nrm == 1.0
+    # one-qudit registers
+    for d in (2, 16):
+        gates = [Gate(0, (), (), haar_unitary(d, rng)) for _ in range(5)]
+        got, nrm, _ = run_gpu(P, [d], gates, **kw)
+        assert np.max(np.abs(got - O1.run([d], gates))) <= 1e-12
+    # identity gates, a 16-dimensional qudit, many controls
+    dims = [2, 3, 16, 2, 2, 3, 2, 2]
+    gates = [Gate(1, (), (), np.eye(3, dtype=np.complex128)),
+             Gate(2, (), (), haar_unitary(16, rng)),
+             Gate(0, (2,), (7,), haar_unitary(2, rng)),
+             Gate(2, (0, 1), (1, 2), haar_unitary(16, rng)),
+             Gate(4, (0, 1, 3, 5), (1, 0, 1, 2), haar_unitary(2, rng)),
+             Gate(6, (0, 1, 3, 4, 7), (1, 2, 0, 1, 1), haar_unitary(2, rng)),
+             Gate(5, (6, 7, 0, 2), (1, 1, 1, 15), shift_x(3, 1)),
+             Gate(3, (), (), np.eye(2, dtype=np.complex128))]
+    gates += [Gate(int(t), (), (), haar_unitary(dims[int(t)], rng)) for t in rng.integers(0, len(dims), 12)]
+    psi0 = random_state(int(np.prod(dims)), 17 + mode)
+    ref = O2.run(dims, gates, psi0)
+    got, nrm, _ = run_gpu(P, dims, gates, psi0, **kw)
+    assert np.max(np.abs(got - ref)) <= 1e-12
+    assert abs(nrm - 1.0) <= 1e-10
