@@ -517,8 +517,8 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant_
             tg.len = len;
             tg.flags = g.flags;
             tg.lowoff = si.lowoff[gi];
-            tg.moff = moffs + gi * kMaxDim;
-            tg.soff = soffs + gi * kMaxDim;
+            tg.moff = &p.moff_t[gi][0];          // parameter bank (uniform across the CTA)
+            tg.soff = &p.soff_t[gi][0];
             const bool needck = g.flags != 0 || len < p.LT;
             const V *U = Us + g.uoff;
             switch (g.d) {
