@@ -14,6 +14,10 @@
 //     Cartesian product), so only firing classes are visited;
 //   * per class from the tile's run offset: controls on run digits above the low prefix;
 //   * once per tile: controls on digits outside the tile (the producer's fire bits).
+// Two commuting qubit gates with the same controls may be applied together as one 4-member
+// class (a "pair gate", member offsets from a per-gate table).  The compute threads form G
+// consumer groups that ping-pong over the CTA's tiles.  The kernel is templated on the element
+// type (complex128, or complex64 when every bulk copy is 16-byte aligned).
 #include <cuda_runtime.h>
 
 #include <algorithm>
