@@ -360,6 +360,9 @@ def main():
                          "kernel": ("k_gate_pass (multi-gate passes) + single-gate kernels" if block
                                     else "single-gate kernels (k_gate_tiled / k_gate_direct)"),
                          "algorithmic": "32 B x sum of touched amplitudes of the gates applied (SURVEY.md 8(d))",
+                         "note": ("a multi-gate pass applies ~10 gates per HBM round trip of the state, so the "
+                                  "per-gate algorithmic rate exceeds the HBM peak; the pass kernel's own binding "
+                                  "resource and fraction are in pass_roofline") if block else None,
                          "bytes_per_launch": bytes_per_launch, "ms_per_launch": ms_per_launch,
                          "state_bytes_per_launch": state_bytes_per_launch,
                          "state_gbs": state_gbs,
