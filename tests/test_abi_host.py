@@ -314,3 +314,20 @@ def test_block_planner_order_is_equivalent():
         ref = O2.run(dims, gates, psi0)
         got = O2.run(dims, [gates[i] for i in order], psi0)
         assert np.max(np.abs(got - ref)) < 1e-13
+
+
+def test_bench_reference_arm_under_torchrun():
+    """The driver launches N > 1 through torch.distributed.run; for the reference arm rank 0
+    alone runs and prints one JSON line, the other ranks exit 0 without work."""
+    import json
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(root, "bench.py"),
+           "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "1"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
