@@ -191,15 +191,16 @@ SV_API sv_status sv_set_option(sv_handle h, int32_t option, int64_t value);
 
 /* Per-launch timing of the gate kernels recorded while SV_OPT_PROFILE is on: the summed
  * device time between the events bracketing each gate launch, the number of launches, and
- * the algorithmic bytes those launches move (32 B per touched amplitude: one 16 B read and
- * one 16 B write).  Synchronises; reset != 0 clears the record. */
+ * the algorithmic bytes those launches move (one read and one write per touched amplitude:
+ * 32 B for complex128, 16 B for complex64).  Synchronises; reset != 0 clears
+ * the record. */
 typedef struct {
     uint64_t launches;
     double kernel_ms;
-    double algorithmic_bytes;  /* 32 B x sum of T over the gates the launches applied           */
+    double algorithmic_bytes;  /* 2 x element bytes x sum of T over the gates the launches applied */
     double touched;            /* amplitude updates (sum of T over the launched gates)          */
     double state_bytes;        /* bytes the launches must move at least: a single-gate launch
-                                  32 B x T; a multi-gate pass (SV_BLOCK) 32 B x the state once  */
+                                  2 x elem x T; a multi-gate pass (SV_BLOCK) 2 x elem x the state */
 } sv_profile;
 SV_API sv_status sv_profile_read(sv_handle h, int32_t reset, sv_profile *out);
 
