@@ -109,7 +109,11 @@ SV_API sv_status sv_create_ex(const int32_t *dims, int32_t n, sv_dtype dt, int d
                        sv_handle *out);
 
 /* Sharded state over nranks = 2^s GPUs (one process per GPU).  The s most-significant
- * digits must be qubits; rank r owns global indices [r*D/P, (r+1)*D/P).
+ * digits must be qubits; rank r initially owns global indices [r*D/P, (r+1)*D/P) (SURVEY.md
+ * §8(e)).  Gates on a sharded qubit that need no partner data move none: a diagonal gate is a
+ * per-slice local phase, and an anti-diagonal gate with no local controls relabels the slices
+ * (afterwards rank r may own a different logical slice; sv_amplitudes / sv_set_amplitudes
+ * address global indices either way, and sv_reset restores the initial ownership).
  * nccl_unique_id: the 128-byte ncclUniqueId produced by sv_nccl_unique_id on rank 0 and
  * broadcast by the caller (e.g. through torch.distributed).  cuda_stream as in sv_create_ex.
  * rank = -1 creates a LOOPBACK handle: all nranks slices live in this one handle on one

@@ -9,6 +9,14 @@
 //         psi_loc <- U[beta][beta] psi_loc + U[beta][1-beta] psi_partner on the local indices
 //         whose local control digits match (beta = this rank's digit of q_target): the class
 //         of PAPER.md:198-222 now spans two ranks and the partner holds the other member.
+//   (iv)  diagonal gate on sharded qubit j -> no exchange: each rank applies the phase
+//         U[beta][beta] to its local amplitudes whose local controls match (a local gate);
+//   (v)   anti-diagonal (X-like) gate on sharded qubit j with no local controls -> no data
+//         moves: the slices swap their logical labels (rank relabelling) and a
+//         slice is scaled when its entry of U is not exactly 1.
+// Rank relabelling: physical rank r holds the slice of logical index lrank[r] (bit j of the
+// logical index = digit of q_{n-s+j}); every rank keeps the same map because every rank
+// plans the same gate list.  sv_reset restores the identity map.
 // Transport: NCCL send/recv over NVLink (one process per GPU; NCCL is dlopen'ed so the core
 // library loads without it), chunked and double-buffered on a comm stream so the transfer of
 // chunk c+1 overlaps the combine of chunk c.  A loopback transport (all P slices in one
@@ -94,7 +102,13 @@ struct ShardCtx {
     cudaEvent_t ev_done[2] = {nullptr, nullptr};
     cudaEvent_t ev_start = nullptr;
     double *d_scalar = nullptr;
+    std::vector<int> lrank, prank; // physical rank -> logical slice index, and its inverse
     bool loopback() const { return rank < 0; }
+    void identity_map() {
+        lrank.resize(P);
+        prank.resize(P);
+        for (int r = 0; r < P; ++r) lrank[r] = prank[r] = r;
+    }
 };
 
 void shard_destroy(ShardCtx *c) {
@@ -145,6 +159,83 @@ CombineCtrl local_ctrl(const Register &local, const std::vector<CtrlSpec> &ctrl)
     }
     return cc;
 }
+
+enum ShardKind { SK_LOCAL, SK_PHASE, SK_RELABEL, SK_EXCHANGE };
+
+inline bool is_zero(double2 z) { return z.x == 0.0 && z.y == 0.0; }
+inline bool is_one(double2 z) { return z.x == 1.0 && z.y == 0.0; }
+
+// How a gate is applied under sharding (rules i, iii, iv, v above).
+ShardKind classify(const Register &local, const GateSpec &g) {
+    if (g.target < local.n) return SK_LOCAL;
+    if (is_zero(g.U[1]) && is_zero(g.U[2])) return SK_PHASE;
+    bool local_ctrl = false;
+    for (const auto &c : g.ctrl) local_ctrl = local_ctrl || c.q < local.n;
+    if (is_zero(g.U[0]) && is_zero(g.U[3]) && !local_ctrl) return SK_RELABEL;
+    return SK_EXCHANGE;
+}
+
+// Rule ii on logical slice index l: do the gate's sharded controls hold there?
+bool fires_on(const std::vector<CtrlSpec> &ctrl, int first_sh, int l) {
+    for (const auto &c : ctrl)
+        if (c.q >= first_sh && ((l >> (c.q - first_sh)) & 1) != c.v) return false;
+    return true;
+}
+
+// The gate u * I on q_0: a uniform scale of a slice.
+GateSpec scale_gate(const Register &local, double2 u) {
+    GateSpec s;
+    s.target = 0;
+    s.d = local.dims[0];
+    s.U.assign((size_t)s.d * s.d, make_double2(0.0, 0.0));
+    for (int i = 0; i < s.d; ++i) s.U[(size_t)i * s.d + i] = u;
+    return s;
+}
+
+// Rule iv: the local form, on logical slice l, of a diagonal gate on a sharded qubit.  The
+// phase u = U[beta][beta] multiplies the amplitudes whose local control digits match: with
+// local controls, a diagonal gate on the first one (entry u at its control value, 1
+// elsewhere) controlled on the rest; without, u * I on q_0.  False when u is exactly 1.
+bool phase_local(const Register &local, const GateSpec &g, int l, GateSpec *out) {
+    const int first_sh = local.n;
+    const int beta = (l >> (g.target - first_sh)) & 1;
+    const double2 u = g.U[beta * 2 + beta];
+    if (is_one(u)) return false;
+    std::vector<CtrlSpec> lc;
+    for (const auto &c : g.ctrl)
+        if (c.q < first_sh) lc.push_back(c);
+    if (lc.empty()) { *out = scale_gate(local, u); return true; }
+    GateSpec p;
+    p.target = lc[0].q;
+    p.d = local.dims[p.target];
+    p.U.assign((size_t)p.d * p.d, make_double2(0.0, 0.0));
+    for (int i = 0; i < p.d; ++i) p.U[(size_t)i * p.d + i] = (i == lc[0].v) ? u : make_double2(1.0, 0.0);
+    p.ctrl.assign(lc.begin() + 1, lc.end());
+    *out = std::move(p);
+    return true;
+}
+
+// Rule v: y_{b'} = U[b'][1-b'] x_{1-b'} on sharded qubit j.  On every logical slice l whose
+// sharded controls hold, the slice holding x_beta becomes logical l ^ 2^j, scaled by
+// U[1-beta][beta].  Updates the map; returns (physical rank, factor) for factors != 1.
+std::vector<std::pair<int, double2>> relabel(ShardCtx *c, const GateSpec &g, int first_sh) {
+    const int j = g.target - first_sh;
+    std::vector<std::pair<int, double2>> scales;
+    std::vector<int> nl = c->lrank;
+    for (int r = 0; r < c->P; ++r) {
+        const int l = c->lrank[r];
+        if (!fires_on(g.ctrl, first_sh, l)) continue;
+        const int beta = (l >> j) & 1;
+        nl[r] = l ^ (1 << j);
+        const double2 u = g.U[(1 - beta) * 2 + beta];
+        if (!is_one(u)) scales.push_back({r, u});
+    }
+    c->lrank = nl;
+    for (int r = 0; r < c->P; ++r) c->prank[nl[r]] = r;
+    return scales;
+}
+
+bool owns(const ShardCtx *c, int r) { return c->loopback() || r == c->rank; }
 
 sv_status exchange_nccl(sv_handle h, const GateSpec &g, const ShardAction &a) {
     ShardCtx *c = h->shard;
@@ -214,6 +305,29 @@ sv_status shard_apply(sv_handle h, const GateSpec &g, bool check_unitary) {
         const double ue = unitarity_error(g.U.data(), g.d);
         if (!(ue <= 1e-12)) return fail_msg(SV_ERR_NOT_UNITARY, "U is not unitary");
     }
+    const ShardKind kind = classify(h->local, g);
+    if (kind == SK_PHASE) {
+        for (int r : ranks_of(c)) {
+            GateSpec pl;
+            if (!fires_on(g.ctrl, h->local.n, c->lrank[r]) || !phase_local(h->local, g, c->lrank[r], &pl))
+                continue;
+            GatePlan p;
+            sv_status s = plan_gate(h->local, pl, false, &p, err);
+            if (s == SV_OK) s = launch_on(h, p, slice_of(c, r));
+            if (s != SV_OK) return s;
+        }
+        return SV_OK;
+    }
+    if (kind == SK_RELABEL) {
+        for (const auto &rs : relabel(c, g, h->local.n)) {
+            if (!owns(c, rs.first)) continue;
+            GatePlan p;
+            sv_status s = plan_gate(h->local, scale_gate(h->local, rs.second), false, &p, err);
+            if (s == SV_OK) s = launch_on(h, p, slice_of(c, rs.first));
+            if (s != SV_OK) return s;
+        }
+        return SV_OK;
+    }
     // local view of the gate (sharded controls become the rank predicate)
     GateSpec gl = g;
     gl.ctrl.clear();
@@ -222,8 +336,8 @@ sv_status shard_apply(sv_handle h, const GateSpec &g, bool check_unitary) {
     std::vector<int> done(c->P, 0);
     for (int r : ranks_of(c)) {
         if (done[r]) continue;
-        ShardAction a;
-        sv_status s = shard_plan(h->reg, c->P, r, g.target, g.ctrl, &a, err);
+        ShardAction a;   // planned on logical slice indices; partner mapped back to a rank
+        sv_status s = shard_plan(h->reg, c->P, c->lrank[r], g.target, g.ctrl, &a, err);
         if (s != SV_OK) return s;
         if (a.action == 1) continue;
         if (a.action == 0) {
@@ -234,10 +348,13 @@ sv_status shard_apply(sv_handle h, const GateSpec &g, bool check_unitary) {
             if (s != SV_OK) return s;
             continue;
         }
+        const int lpartner = a.partner;
+        a.partner = c->prank[lpartner];
         if (c->loopback()) {
             ShardAction ap;
-            s = shard_plan(h->reg, c->P, a.partner, g.target, g.ctrl, &ap, err);
+            s = shard_plan(h->reg, c->P, lpartner, g.target, g.ctrl, &ap, err);
             if (s != SV_OK) return s;
+            ap.partner = r;
             s = exchange_loopback(h, g, r, a, ap);
             done[a.partner] = 1;
         } else {
@@ -281,8 +398,21 @@ sv_status shard_apply_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_
         return SV_OK;
     };
     const bool reorder = (flags & SV_BLOCK) != 0;
+    ShardCtx *c = h->shard;
     for (const GateSpec &g : specs) {
-        if (g.target >= first_sh) {
+        const ShardKind kind = classify(h->local, g);
+        if (kind == SK_RELABEL) {                   // pending exchanges are planned on the old map
+            sv_status s = flush();
+            if (s != SV_OK) return s;
+            for (const auto &rs : relabel(c, g, first_sh))
+                for (size_t i = 0; i < ranks.size(); ++i)
+                    if (ranks[i] == rs.first) {
+                        runs[i].push_back(scale_gate(h->local, rs.second));
+                        any = true;
+                    }
+            continue;
+        }
+        if (kind == SK_EXCHANGE) {
             pending.push_back(&g);
             if (!reorder) {
                 sv_status s = flush();
@@ -297,15 +427,21 @@ sv_status shard_apply_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_
             if (s != SV_OK) return s;
         }
         for (size_t i = 0; i < ranks.size(); ++i) {
+            const int l = c->lrank[ranks[i]];          // bit j of l = digit of q_{n-s+j}
+            if (!fires_on(g.ctrl, first_sh, l)) continue;
+            if (kind == SK_PHASE) {
+                GateSpec pl;
+                if (phase_local(h->local, g, l, &pl)) {
+                    runs[i].push_back(std::move(pl));
+                    any = true;
+                }
+                continue;
+            }
             GateSpec lg = g;
             lg.ctrl.clear();
-            bool fires = true;
-            for (const auto &c : g.ctrl) {
-                if (c.q < first_sh) { lg.ctrl.push_back(c); continue; }
-                const int bit = (ranks[i] >> (c.q - first_sh)) & 1;   // rank bit j = digit of q_{n-s+j}
-                if (bit != c.v) fires = false;
-            }
-            if (fires) {
+            for (const auto &cs : g.ctrl)
+                if (cs.q < first_sh) lg.ctrl.push_back(cs);
+            {
                 runs[i].push_back(std::move(lg));
                 any = true;
             }
@@ -316,6 +452,7 @@ sv_status shard_apply_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_
 
 sv_status shard_reset(sv_handle h, uint64_t idx) {
     ShardCtx *c = h->shard;
+    c->identity_map();
     const uint64_t L = h->local.D;
     const int owner = (int)(idx / L);
     for (int r : ranks_of(c)) {
@@ -333,7 +470,7 @@ sv_status shard_set_amplitudes(sv_handle h, uint64_t first, uint64_t count, cons
     ShardCtx *c = h->shard;
     const uint64_t L = h->local.D;
     for (int r : ranks_of(c)) {
-        const uint64_t lo = (uint64_t)r * L, hi = lo + L;
+        const uint64_t lo = (uint64_t)c->lrank[r] * L, hi = lo + L;
         const uint64_t a = first > lo ? first : lo, b = (first + count) < hi ? first + count : hi;
         if (a >= b) continue;
         if (h->c64) {                        // complex64: round the ABI's doubles on the host
@@ -363,7 +500,7 @@ sv_status shard_amplitudes(sv_handle h, uint64_t first, uint64_t count, double *
     ShardCtx *c = h->shard;
     const uint64_t L = h->local.D;
     for (int r = 0; r < c->P; ++r) {
-        const uint64_t lo = (uint64_t)r * L, hi = lo + L;
+        const uint64_t lo = (uint64_t)c->lrank[r] * L, hi = lo + L;
         const uint64_t a = first > lo ? first : lo, b = (first + count) < hi ? first + count : hi;
         if (a >= b) continue;
         if (c->loopback() && !h->c64) {
@@ -484,6 +621,7 @@ sv_status sv_create_sharded(const int32_t *dims, int32_t n, sv_dtype dt, int32_t
     c->P = nranks;
     c->s = sh;
     c->rank = rank;
+    c->identity_map();
     h->shard = c;
     s = state_init_device(h, device, cuda_stream, nullptr, 0);
     if (s != SV_OK) { state_free(h); return s; }

@@ -165,3 +165,22 @@ def test_loopback_sharded_c64(P, nranks):
         assert np.array_equal(got, O2.run(dims, perm, lab))
     finally:
         del os.environ["SV_EXCHANGE_CHUNK"]
+
+
+@pytest.mark.parametrize("nranks", [2, 8])
+def test_loopback_relabel_and_phase_c64(P, nranks):
+    """complex64 sharded state: gates on sharded qubits that move no data (relabelled slices,
+    local phases) against the fp64 oracle within the fp32 bound, with no exchange."""
+    from test_gpu_parity import _sharded_free_circuit
+    dims = [3, 2, 4, 2, 2, 2, 2, 2]
+    D = int(np.prod(dims))
+    gates = _sharded_free_circuit(dims, nranks, 70 + nranks)
+    psi0 = random_state(D, 12)
+    ref = O2.run(dims, gates, psi0)
+    for block in (False, True):
+        with P.State.loopback(dims, nranks, dtype="c64") as st:
+            st.set_amplitudes(0, psi0)
+            st.apply_circuit(gates, block=block)
+            got = st.amplitudes()
+            assert st.info().exchanges == 0
+        assert np.linalg.norm(got - ref) <= bound(gates, dims, np.sqrt(2) * U32), block

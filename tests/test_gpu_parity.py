@@ -320,6 +320,90 @@ def test_external_torch_buffer_and_stream(P):
     assert np.max(np.abs(got - ref)) <= 1e-10
 
 
+def _sharded_free_circuit(dims, nranks, seed):
+    """Gates whose sharded-target members move no data (rules iv, v of shard.cpp): diagonal
+    gates (with and without local controls) and X-like gates with only sharded controls,
+    interleaved with local gates controlled on sharded qubits."""
+    rng = np.random.default_rng(seed)
+    n = len(dims)
+    s = nranks.bit_length() - 1
+    sh = list(range(n - s, n))
+    loc = list(range(n - s))
+    y = np.array([[0, -1j], [1j, 0]])
+    mono = np.array([[0, np.exp(0.3j)], [np.exp(-1.1j), 0]])
+    gates = []
+    for i in range(60):
+        k = i % 6
+        t = int(rng.choice(sh))
+        others = [q for q in sh if q != t]
+        if k == 0:
+            gates.append(Gate(t, (), (), shift_x(2, 1)))
+        elif k == 1:
+            c = tuple(int(x) for x in others[:1])
+            gates.append(Gate(t, c, tuple(int(rng.integers(2)) for _ in c), y if i % 12 else mono))
+        elif k == 2:
+            gates.append(Gate(t, (), (), t_gate() if i % 12 else np.diag([1, -1]).astype(complex)))
+        elif k == 3:
+            c = int(rng.choice(loc))
+            gates.append(Gate(t, (c,), (int(rng.integers(dims[c])),), np.diag(np.exp(1j * rng.random(2)))))
+        elif k == 4:
+            q = int(rng.choice(loc))
+            gates.append(Gate(q, (t,), (int(rng.integers(2)),), haar_unitary(dims[q], rng)))
+        else:
+            q = int(rng.choice(loc))
+            gates.append(Gate(q, (), (), haar_unitary(dims[q], rng)))
+    return gates
+
+
+@pytest.mark.parametrize("nranks", [2, 4, 8])
+def test_loopback_relabel_and_phase_move_no_data(P, nranks):
+    """Rank relabelling and local phases for gates on sharded qubits: the
+    result matches the oracle in every driver mode and through apply_gate, no exchange runs,
+    and readback, partial uploads and reset see the relabelled slices."""
+    dims = [3, 2, 4, 2, 2, 2, 2, 2]
+    D = int(np.prod(dims))
+    gates = _sharded_free_circuit(dims, nranks, 7 + nranks)
+    psi0 = random_state(D, 11)
+    ref = O2.run(dims, gates, psi0)
+    for mode in ("gate", False, True, "block"):
+        with P.State.loopback(dims, nranks) as st:
+            st.set_amplitudes(0, psi0)
+            if mode == "gate":
+                for g in gates:
+                    st.apply_gate(g.target, g.U, g.ctrl, g.vals)
+            else:
+                st.apply_circuit(gates, fuse=mode is True, block=mode == "block")
+            got = st.amplitudes()
+            assert st.info().exchanges == 0, mode
+            # partial reads and a partial upload across relabelled slice boundaries
+            L = D // nranks
+            lo, cnt = L // 2, L + 3
+            assert np.array_equal(st.amplitudes(lo, cnt), got[lo:lo + cnt])
+            patch = random_state(cnt, 3)
+            st.set_amplitudes(lo, patch)
+            full = got.copy()
+            full[lo:lo + cnt] = patch
+            assert np.array_equal(st.amplitudes(), full)
+            # a following exchange gate pairs the right slices
+            hx = [Gate(len(dims) - 1, (), (), hadamard())]
+            st.apply_circuit(hx)
+            assert st.info().exchanges == nranks // 2       # loopback counts slice pairs
+            assert np.max(np.abs(st.amplitudes() - O2.run(dims, hx, full))) <= 1e-12
+            st.reset(D - 5)
+            a = st.amplitudes()
+            assert a[D - 5] == 1.0 and np.count_nonzero(a) == 1
+        assert np.max(np.abs(got - ref)) <= 1e-12, mode
+    # bit-exact labelled permutations mixing relabels, exchanges and sharded predicates
+    perm = [g for g in gates if np.count_nonzero(g.U) == g.U.shape[0]
+            and np.all(np.abs(g.U[np.nonzero(g.U)] - 1) == 0)]
+    perm += [Gate(0, (len(dims) - 1,), (1,), shift_x(3, 2)), Gate(len(dims) - 1, (1,), (1,), shift_x(2, 1))]
+    lab = labelled_state(0, D)
+    with P.State.loopback(dims, nranks) as st:
+        st.set_amplitudes(0, lab)
+        st.apply_circuit(perm, block=True)
+        assert np.array_equal(st.amplitudes(), O2.run(dims, perm, lab))
+
+
 @pytest.mark.parametrize("nranks", [2, 4, 8])
 def test_loopback_sharded_matches_single_state(P, nranks):
     """Sharded mode with the loopback transport: sharded targets exchange,
