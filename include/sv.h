@@ -112,8 +112,10 @@ SV_API sv_status sv_create_ex(const int32_t *dims, int32_t n, sv_dtype dt, int d
  * digits must be qubits; rank r initially owns global indices [r*D/P, (r+1)*D/P) (SURVEY.md
  * §8(e)).  Gates on a sharded qubit that need no partner data move none: a diagonal gate is a
  * per-slice local phase, and an anti-diagonal gate with no local controls relabels the slices
- * (afterwards rank r may own a different logical slice; sv_amplitudes / sv_set_amplitudes
- * address global indices either way, and sv_reset restores the initial ownership).
+ * (afterwards rank r may own a different logical slice); any other gate on a sharded qubit
+ * swaps that qubit with a local qubit (SV_OPT_SHARD_SWAP) or exchanges slices.  sv_amplitudes
+ * / sv_set_amplitudes address global indices either way (they first swap remapped qubits
+ * back), and sv_reset restores the initial layout.
  * nccl_unique_id: the 128-byte ncclUniqueId produced by sv_nccl_unique_id on rank 0 and
  * broadcast by the caller (e.g. through torch.distributed).  cuda_stream as in sv_create_ex.
  * rank = -1 creates a LOOPBACK handle: all nranks slices live in this one handle on one
@@ -191,6 +193,10 @@ SV_API sv_status sv_get_info(sv_handle h, sv_info *out);
 #define SV_OPT_PASS_WINDOW 11   /* gates the pass planner scans ahead (1..4096)                    */
 #define SV_OPT_PASS_MERGE  12   /* 1 (default): merge commuting same-target gates before SV_BLOCK passes;
                                    0: keep every gate (per-gate microbenchmarks)                   */
+#define SV_OPT_SHARD_SWAP  13   /* sharded handles: 1 (default) = a gate on a sharded qubit that needs
+                                   the partner's amplitudes first swaps that qubit with the top local
+                                   qubit (half-slice transfer, then a local gate); 0 = pairwise
+                                   exchange + combine.  Ignored when the top local digit is not a qubit */
 SV_API sv_status sv_set_option(sv_handle h, int32_t option, int64_t value);
 
 /* Per-launch timing of the gate kernels recorded while SV_OPT_PROFILE is on: the summed

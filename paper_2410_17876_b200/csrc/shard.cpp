@@ -14,9 +14,18 @@
 //   (v)   anti-diagonal (X-like) gate on sharded qubit j with no local controls -> no data
 //         moves: the slices swap their logical labels (rank relabelling) and a
 //         slice is scaled when its entry of U is not exactly 1.
+//   (vi)  any other gate on sharded qubit j (default, SV_OPT_SHARD_SWAP) -> qubit remapping:
+//         the qubit at sharded position j swaps places with a local qubit k whose digit
+//         runs are long (b_k >= L/16; chosen by furthest next use, see pick_local).  Each rank
+//         sends the half of its slice whose digit k differs from its own digit j and
+//         receives the partner's matching half in its place (half the bytes of a pairwise
+//         exchange, no combine pass); the gate is then local and joins the multi-gate passes.
 // Rank relabelling: physical rank r holds the slice of logical index lrank[r] (bit j of the
-// logical index = digit of q_{n-s+j}); every rank keeps the same map because every rank
-// plans the same gate list.  sv_reset restores the identity map.
+// logical index = digit at sharded position n-s+j); every rank keeps the same maps because
+// every rank plans the same gate list.  Qubit remapping: logical qudit q sits at digit
+// position pos_of[q] (disjoint local <-> sharded qubit pairs); gates are
+// translated to positions before planning, and readback / uploads first swap the qubits
+// back home.  sv_reset restores both identity maps.
 // Transport: NCCL send/recv over NVLink (one process per GPU; NCCL is dlopen'ed so the core
 // library loads without it), chunked and double-buffered on a comm stream so the transfer of
 // chunk c+1 overlaps the combine of chunk c.  A loopback transport (all P slices in one
@@ -103,11 +112,15 @@ struct ShardCtx {
     cudaEvent_t ev_start = nullptr;
     double *d_scalar = nullptr;
     std::vector<int> lrank, prank; // physical rank -> logical slice index, and its inverse
+    std::vector<int> pos_of, log_at; // logical qudit -> digit position, and its inverse
     bool loopback() const { return rank < 0; }
-    void identity_map() {
+    void identity_map(int n) {
         lrank.resize(P);
         prank.resize(P);
         for (int r = 0; r < P; ++r) lrank[r] = prank[r] = r;
+        pos_of.resize(n);
+        log_at.resize(n);
+        for (int q = 0; q < n; ++q) pos_of[q] = log_at[q] = q;
     }
 };
 
@@ -237,6 +250,138 @@ std::vector<std::pair<int, double2>> relabel(ShardCtx *c, const GateSpec &g, int
 
 bool owns(const ShardCtx *c, int r) { return c->loopback() || r == c->rank; }
 
+// A logical gate at the current digit positions (rule vi).
+GateSpec to_phys(const ShardCtx *c, const GateSpec &g) {
+    GateSpec p = g;
+    p.target = c->pos_of[g.target];
+    for (auto &cs : p.ctrl) cs.q = c->pos_of[cs.q];
+    return p;
+}
+
+// Rule vi candidates: local qubit positions whose digit blocks are at least L/16 amplitudes
+// long (a half slice is at most 8 contiguous runs).
+bool swappable(sv_handle h, int k) {
+    return h->local.dims[k] == 2 && h->local.b[k] * 16 >= h->local.D;
+}
+
+bool diag_gate(const GateSpec &g) {
+    for (int a = 0; a < g.d; ++a)
+        for (int b = 0; b < g.d; ++b)
+            if (a != b && !is_zero(g.U[(size_t)a * g.d + b])) return false;
+    return true;
+}
+
+// Rule vi policy.  Remapped qubits always form disjoint pairs (local position k <-> sharded
+// position j), so the layout is a product of disjoint transpositions:
+//   * the qudit at sharded position j belongs at local position k (swapped out earlier):
+//     swap it home, undoing that pair;
+//   * otherwise pair j with a local qubit still at home: the one whose next non-diagonal gate
+//     (in specs after index i; none when specs is null) is furthest ahead, top first on ties.
+// Returns -1 when no local qubit qualifies (the gate then exchanges).
+int pick_local(sv_handle h, int j, const std::vector<GateSpec> *specs, size_t i) {
+    ShardCtx *c = h->shard;
+    const int q = c->log_at[h->local.n + j];
+    if (q < h->local.n) return q;
+    int best = -1;
+    size_t best_next = 0;
+    for (int k = h->local.n - 1; k >= 0; --k) {
+        if (!swappable(h, k) || c->log_at[k] != k) continue;
+        size_t next = specs ? specs->size() : 0;
+        if (specs)
+            for (size_t t = i + 1; t < specs->size(); ++t)
+                if ((*specs)[t].target == k && !diag_gate((*specs)[t])) { next = t; break; }
+        if (best < 0 || next > best_next) { best = k; best_next = next; }
+    }
+    return best;
+}
+
+// Rule vi: swap the qubits at local position k (stride b) and sharded position n-s+j.  A
+// rank whose digit j is beta keeps the amplitudes with digit k = beta and trades those with
+// digit k = 1-beta (runs of b amplitudes at m 2b + (1-beta) b) for the partner's amplitudes
+// with digit k = beta, which land in the same places.
+sv_status swap_qubits(sv_handle h, int k, int j) {
+    ShardCtx *c = h->shard;
+    const uint64_t L = h->local.D, b = h->local.b[k];
+    // (run offset, length) pieces of at most one chunk over the runs of digit k = v
+    auto pieces = [&](int v) {
+        std::vector<std::pair<uint64_t, uint64_t>> out;
+        for (uint64_t m = 0; m < L; m += 2 * b)
+            for (uint64_t o = 0; o < b; o += c->chunk)
+                out.push_back({m + (uint64_t)v * b + o, (b - o < c->chunk) ? b - o : c->chunk});
+        return out;
+    };
+    for (int r : ranks_of(c)) {
+        const int l = c->lrank[r];
+        const int beta = (l >> j) & 1;
+        const int p = c->prank[l ^ (1 << j)];
+        const auto mine = pieces(1 - beta);          // what this rank gives away
+        if (c->loopback()) {
+            if (p < r) continue;                      // each pair once
+            const auto theirs = pieces(beta);         // the partner's (its digit j is 1 - beta)
+            for (size_t x = 0; x < mine.size(); ++x) {
+                const size_t bytes = mine[x].second * h->elem;
+                double2 *a = at(c->slices[r], mine[x].first, h->elem);
+                double2 *bb = at(c->slices[p], theirs[x].first, h->elem);
+                cudaError_t e = cudaMemcpyAsync(c->stage[0], a, bytes, cudaMemcpyDeviceToDevice, h->stream);
+                if (e == cudaSuccess) e = cudaMemcpyAsync(a, bb, bytes, cudaMemcpyDeviceToDevice, h->stream);
+                if (e == cudaSuccess) e = cudaMemcpyAsync(bb, c->stage[0], bytes, cudaMemcpyDeviceToDevice, h->stream);
+                if (e != cudaSuccess) return cuda_fail_h(h, e, "loopback qubit swap");
+            }
+            ++h->exchanges;
+            continue;
+        }
+        cudaError_t e = cudaEventRecord(c->ev_start, h->stream);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(c->comm_stream, c->ev_start, 0);
+        if (e != cudaSuccess) return cuda_fail_h(h, e, "qubit swap setup");
+        const ncclDataType_t ty = h->c64 ? ncclFloat32 : ncclFloat64;     // 2 reals per amplitude
+        for (size_t x = 0; x < mine.size(); ++x) {
+            const uint64_t len = mine[x].second;
+            const int sb = (int)(x & 1);
+            if (x >= 2) cudaStreamWaitEvent(c->comm_stream, c->ev_done[sb], 0);   // stage free again
+            double2 *a = at(c->slices[0], mine[x].first, h->elem);
+            ncclResult_t rr = nccl().GroupStart();
+            if (rr == ncclSuccess) rr = nccl().Send(a, 2 * len, ty, p, c->comm, c->comm_stream);
+            if (rr == ncclSuccess) rr = nccl().Recv(c->stage[sb], 2 * len, ty, p, c->comm, c->comm_stream);
+            ncclResult_t r2 = nccl().GroupEnd();
+            if (rr != ncclSuccess) return nccl_fail(h, rr, "ncclSend/Recv");
+            if (r2 != ncclSuccess) return nccl_fail(h, r2, "ncclGroupEnd");
+            e = cudaEventRecord(c->ev_recv[sb], c->comm_stream);    // piece sent and received
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(h->stream, c->ev_recv[sb], 0);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(a, c->stage[sb], len * h->elem, cudaMemcpyDeviceToDevice, h->stream);
+            if (e == cudaSuccess) e = cudaEventRecord(c->ev_done[sb], h->stream);
+            if (e != cudaSuccess) return cuda_fail_h(h, e, "qubit swap chunk");
+        }
+        ++h->exchanges;
+    }
+    const int q = h->local.n + j;
+    std::swap(c->log_at[k], c->log_at[q]);
+    c->pos_of[c->log_at[k]] = k;
+    c->pos_of[c->log_at[q]] = q;
+    return SV_OK;
+}
+
+// Rule vi for a gate on sharded position j: remap if a local qubit qualifies.
+sv_status try_swap(sv_handle h, int j, const std::vector<GateSpec> *specs, size_t i, bool *swapped) {
+    *swapped = false;
+    if (!h->cfg.shard_swap) return SV_OK;
+    const int k = pick_local(h, j, specs, i);
+    if (k < 0) return SV_OK;
+    *swapped = true;
+    return swap_qubits(h, k, j);
+}
+
+// Swap every remapped pair back (before readback and uploads).
+sv_status restore_layout(sv_handle h) {
+    ShardCtx *c = h->shard;
+    for (int k = 0; k < h->local.n; ++k)
+        if (c->log_at[k] != k) {
+            sv_status s = swap_qubits(h, k, c->log_at[k] - h->local.n);
+            if (s != SV_OK) return s;
+        }
+    return SV_OK;
+}
+
 sv_status exchange_nccl(sv_handle h, const GateSpec &g, const ShardAction &a) {
     ShardCtx *c = h->shard;
     const double2 A = g.U[a.beta * 2 + a.beta], B = g.U[a.beta * 2 + (1 - a.beta)];
@@ -296,15 +441,10 @@ sv_status exchange_loopback(sv_handle h, const GateSpec &g, int r, const ShardAc
     return SV_OK;
 }
 
-}  // namespace
-
-sv_status shard_apply(sv_handle h, const GateSpec &g, bool check_unitary) {
+// One gate at digit positions (already translated), by rules i-v.
+sv_status apply_phys(sv_handle h, const GateSpec &g) {
     ShardCtx *c = h->shard;
     std::string *err = err_slot();
-    if (check_unitary) {
-        const double ue = unitarity_error(g.U.data(), g.d);
-        if (!(ue <= 1e-12)) return fail_msg(SV_ERR_NOT_UNITARY, "U is not unitary");
-    }
     const ShardKind kind = classify(h->local, g);
     if (kind == SK_PHASE) {
         for (int r : ranks_of(c)) {
@@ -365,6 +505,24 @@ sv_status shard_apply(sv_handle h, const GateSpec &g, bool check_unitary) {
     return SV_OK;
 }
 
+}  // namespace
+
+sv_status shard_apply(sv_handle h, const GateSpec &g_logical, bool check_unitary) {
+    ShardCtx *c = h->shard;
+    if (check_unitary) {
+        const double ue = unitarity_error(g_logical.U.data(), g_logical.d);
+        if (!(ue <= 1e-12)) return fail_msg(SV_ERR_NOT_UNITARY, "U is not unitary");
+    }
+    GateSpec g = to_phys(c, g_logical);
+    if (classify(h->local, g) == SK_EXCHANGE) {                     // rule vi
+        bool swapped;
+        sv_status s = try_swap(h, g.target - h->local.n, nullptr, 0, &swapped);
+        if (s != SV_OK) return s;
+        if (swapped) g = to_phys(c, g_logical);
+    }
+    return apply_phys(h, g);
+}
+
 sv_status shard_apply_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_t flags) {
     // Runs of gates with a local target go through the local circuit driver on every slice
     // this handle owns (fusion / multi-gate passes included).  Controls on sharded digits are
@@ -377,7 +535,7 @@ sv_status shard_apply_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_
     const int first_sh = h->local.n;
     if ((flags & SV_BLOCK) && h->cfg.pass_merge) specs = merge_commuting(specs, 64);
     std::vector<std::vector<GateSpec>> runs(ranks.size());
-    std::vector<const GateSpec *> pending;         // exchange gates not applied yet, in order
+    std::vector<GateSpec> pending;                 // exchange gates not applied yet, in order
     bool any = false;
     auto flush = [&]() -> sv_status {
         if (any) {
@@ -390,8 +548,8 @@ sv_status shard_apply_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_
             }
             any = false;
         }
-        for (const GateSpec *g : pending) {
-            sv_status s = shard_apply(h, *g, false);
+        for (const GateSpec &g : pending) {
+            sv_status s = apply_phys(h, g);
             if (s != SV_OK) return s;
         }
         pending.clear();
@@ -399,8 +557,18 @@ sv_status shard_apply_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_
     };
     const bool reorder = (flags & SV_BLOCK) != 0;
     ShardCtx *c = h->shard;
-    for (const GateSpec &g : specs) {
-        const ShardKind kind = classify(h->local, g);
+    for (size_t gi = 0; gi < specs.size(); ++gi) {
+        const GateSpec &gl0 = specs[gi];
+        GateSpec g = to_phys(c, gl0);
+        ShardKind kind = classify(h->local, g);
+        if (kind == SK_EXCHANGE && h->cfg.shard_swap && pick_local(h, g.target - first_sh, &specs, gi) >= 0) {
+            sv_status s = flush();                  // rule vi: remap, then the gate is local
+            bool swapped = false;
+            if (s == SV_OK) s = try_swap(h, g.target - first_sh, &specs, gi, &swapped);
+            if (s != SV_OK) return s;
+            g = to_phys(c, gl0);
+            kind = classify(h->local, g);
+        }
         if (kind == SK_RELABEL) {                   // pending exchanges are planned on the old map
             sv_status s = flush();
             if (s != SV_OK) return s;
@@ -413,7 +581,7 @@ sv_status shard_apply_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_
             continue;
         }
         if (kind == SK_EXCHANGE) {
-            pending.push_back(&g);
+            pending.push_back(g);
             if (!reorder) {
                 sv_status s = flush();
                 if (s != SV_OK) return s;
@@ -421,7 +589,7 @@ sv_status shard_apply_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_
             continue;
         }
         bool ahead = true;                          // may this local gate pass the pending ones?
-        for (const GateSpec *q : pending) ahead = ahead && commute(*q, g);
+        for (const GateSpec &q : pending) ahead = ahead && commute(q, g);
         if (!ahead) {
             sv_status s = flush();
             if (s != SV_OK) return s;
@@ -452,7 +620,7 @@ sv_status shard_apply_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_
 
 sv_status shard_reset(sv_handle h, uint64_t idx) {
     ShardCtx *c = h->shard;
-    c->identity_map();
+    c->identity_map(h->reg.n);
     const uint64_t L = h->local.D;
     const int owner = (int)(idx / L);
     for (int r : ranks_of(c)) {
@@ -468,6 +636,8 @@ sv_status shard_reset(sv_handle h, uint64_t idx) {
 
 sv_status shard_set_amplitudes(sv_handle h, uint64_t first, uint64_t count, const double *in) {
     ShardCtx *c = h->shard;
+    sv_status rs = restore_layout(h);
+    if (rs != SV_OK) return rs;
     const uint64_t L = h->local.D;
     for (int r : ranks_of(c)) {
         const uint64_t lo = (uint64_t)c->lrank[r] * L, hi = lo + L;
@@ -498,6 +668,8 @@ sv_status shard_set_amplitudes(sv_handle h, uint64_t first, uint64_t count, cons
 
 sv_status shard_amplitudes(sv_handle h, uint64_t first, uint64_t count, double *out) {
     ShardCtx *c = h->shard;
+    sv_status rs = restore_layout(h);
+    if (rs != SV_OK) return rs;
     const uint64_t L = h->local.D;
     for (int r = 0; r < c->P; ++r) {
         const uint64_t lo = (uint64_t)c->lrank[r] * L, hi = lo + L;
@@ -621,7 +793,7 @@ sv_status sv_create_sharded(const int32_t *dims, int32_t n, sv_dtype dt, int32_t
     c->P = nranks;
     c->s = sh;
     c->rank = rank;
-    c->identity_map();
+    c->identity_map(n);
     h->shard = c;
     s = state_init_device(h, device, cuda_stream, nullptr, 0);
     if (s != SV_OK) { state_free(h); return s; }

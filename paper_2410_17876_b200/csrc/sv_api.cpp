@@ -66,6 +66,7 @@ void default_cfg(LaunchCfg &c, int device) {
     c.pass_window = 128;       // gates scanned ahead when filling a pass (c4 -4%, c3 +2%: profiles/r01/ab/window_*)
     c.pass_merge = 1;          // commutation-aware merging before pass planning
     c.pass_groups = 2;         // two consumer groups ping-pong over tiles
+    c.shard_swap = 1;          // qubit remapping for gates on sharded qubits
 }
 
 }  // namespace
@@ -505,6 +506,9 @@ sv_status sv_set_option(sv_handle h, int32_t option, int64_t value) {
             return SV_OK;
         case SV_OPT_PASS_MERGE:
             h->cfg.pass_merge = value != 0;
+            return SV_OK;
+        case SV_OPT_SHARD_SWAP:
+            h->cfg.shard_swap = value != 0;
             return SV_OK;
         case SV_OPT_PASS_WINDOW:
             if (value < 1 || value > 4096) return fail(SV_ERR_INVALID_ARG, "pass window 1..4096");

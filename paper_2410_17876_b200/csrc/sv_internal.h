@@ -199,6 +199,7 @@ struct LaunchCfg {
     int pass_window;   // gates scanned ahead (commuting past skipped ones) when filling a pass
     int pass_merge;    // 1: merge same-target same-control gates across commuting ones first
     int pass_groups;   // consumer warp groups of the pass kernel (ping-pong over tiles)
+    int shard_swap;    // 1: sharded mode remaps qubits instead of pairwise exchanges (shard.cpp vi)
     int c64;           // 1: the state is complex64 (float2), else complex128 (double2)
 };
 

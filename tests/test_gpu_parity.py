@@ -419,25 +419,38 @@ def test_loopback_sharded_matches_single_state(P, nranks):
                   Gate(5, (7,), (1,), shift_x(2, 1)), Gate(1, (6, 7), (1, 0), fourier(3))]
         psi0 = random_state(D, 5)
         ref = O2.run(dims, gates, psi0)
-        for fuse in (False, True, "block"):
+        for swap in (1, 0):            # qubit remapping (default) / pairwise exchange + combine
+            for fuse in ("gate", False, True, "block"):
+                with P.State.loopback(dims, nranks) as st:
+                    st.set_option(P.sv.SV_OPT_SHARD_SWAP, swap)
+                    st.set_amplitudes(0, psi0)
+                    if fuse == "gate":
+                        for g in gates:
+                            st.apply_gate(g.target, g.U, g.ctrl, g.vals)
+                    else:
+                        st.apply_circuit(gates, fuse=fuse is True, block=fuse == "block")
+                    nrm = st.norm()             # before readback: on the remapped layout
+                    got = st.amplitudes()
+                    assert st.info().exchanges > 0
+                    # readback restored the layout: more gates continue correctly from there
+                    st.apply_circuit(gates[:40], block=True)
+                    again = st.amplitudes()
+                assert np.max(np.abs(got - ref)) <= 1e-12, (swap, fuse)
+                assert abs(nrm - 1.0) <= 1e-10
+                assert np.max(np.abs(again - O2.run(dims, gates[:40], ref))) <= 1e-12, (swap, fuse)
+            # bit-exact labelled permutations across shards
+            perm = [Gate(7, (), (), shift_x(2, 1)), Gate(6, (2,), (3,), shift_x(2, 1)),
+                    Gate(2, (7,), (1,), shift_x(4, 3)), Gate(5, (6, 0), (0, 1), shift_x(2, 1)),
+                    Gate(7, (2,), (1,), shift_x(2, 1)), Gate(6, (0,), (2,), shift_x(2, 1)),
+                    Gate(2, (6,), (1,), shift_x(4, 1)), Gate(5, (7,), (0,), shift_x(2, 1))]
+            lab = labelled_state(0, D)
             with P.State.loopback(dims, nranks) as st:
-                st.set_amplitudes(0, psi0)
-                st.apply_circuit(gates, fuse=fuse is True, block=fuse == "block")
+                st.set_option(P.sv.SV_OPT_SHARD_SWAP, swap)
+                st.set_amplitudes(0, lab)
+                for g in perm:
+                    st.apply_gate(g.target, g.U, g.ctrl, g.vals)
                 got = st.amplitudes()
-                nrm = st.norm()
-                assert st.info().exchanges > 0
-            assert np.max(np.abs(got - ref)) <= 1e-12
-            assert abs(nrm - 1.0) <= 1e-10
-        # bit-exact labelled permutations across shards
-        perm = [Gate(7, (), (), shift_x(2, 1)), Gate(6, (2,), (3,), shift_x(2, 1)),
-                Gate(2, (7,), (1,), shift_x(4, 3)), Gate(5, (6, 0), (0, 1), shift_x(2, 1))]
-        lab = labelled_state(0, D)
-        with P.State.loopback(dims, nranks) as st:
-            st.set_amplitudes(0, lab)
-            for g in perm:
-                st.apply_gate(g.target, g.U, g.ctrl, g.vals)
-            got = st.amplitudes()
-        assert np.array_equal(got, O2.run(dims, perm, lab))
+            assert np.array_equal(got, O2.run(dims, perm, lab))
     finally:
         del os.environ["SV_EXCHANGE_CHUNK"]
 

@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--nqubits", type=int, default=None)
     ap.add_argument("--block", type=int, default=1)
+    ap.add_argument("--swap", type=int, default=1, help="SV_OPT_SHARD_SWAP: qubit remapping (1) or exchange (0)")
     args = ap.parse_args()
     import torch
     import paper_2410_17876_b200 as P
@@ -27,6 +28,8 @@ def main():
     ga = P.sv._GateArray(gates)
     for nr in [int(x) for x in args.ranks.split(",")]:
         st = P.State(dims) if nr == 1 else P.State.loopback(dims, nr)
+        if nr > 1:
+            st.set_option(P.sv.SV_OPT_SHARD_SWAP, args.swap)
         ext = torch.cuda.ExternalStream(st.info().cuda_stream)
         st.reset(0)
         st.apply_circuit(ga, fuse=True, check=False, block=bool(args.block))
@@ -41,7 +44,7 @@ def main():
         st.sync()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / args.reps
-        print(json.dumps({"config": args.config, "ranks": nr, "ms_per_circuit": ms,
+        print(json.dumps({"config": args.config, "ranks": nr, "swap": args.swap, "ms_per_circuit": ms,
                           "ms_per_rank_slice": ms / nr,
                           "exchanges_per_circuit": (st.info().exchanges - x0) / args.reps}), flush=True)
         st.close()
