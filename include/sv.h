@@ -196,7 +196,10 @@ SV_API sv_status sv_get_info(sv_handle h, sv_info *out);
 #define SV_OPT_SHARD_SWAP  13   /* sharded handles: 1 (default) = a gate on a sharded qubit that needs
                                    the partner's amplitudes first swaps that qubit with the top local
                                    qubit (half-slice transfer, then a local gate); 0 = pairwise
-                                   exchange + combine.  Ignored when the top local digit is not a qubit */
+                                   exchange + combine.  Ignored when no local qubit has long digit runs */
+#define SV_OPT_PASS_SEARCH 14   /* 1 (default): each SV_BLOCK pass's in-tile qudit set is the one that
+                                   admits the most window gates (subset search); 0: first come, first
+                                   admitted */
 SV_API sv_status sv_set_option(sv_handle h, int32_t option, int64_t value);
 
 /* Per-launch timing of the gate kernels recorded while SV_OPT_PROFILE is on: the summed

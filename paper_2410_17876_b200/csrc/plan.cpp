@@ -3,6 +3,7 @@
 #include "plan.h"
 
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <cstring>
 
@@ -311,9 +312,91 @@ bool commute(const GateSpec &a, const GateSpec &b) {
     return true;
 }
 
+// In-tile set search for one pass: the window's gates W (not yet applied, in order), the
+// distinct targets above the low prefix among them, and every subset S of those targets whose
+// tile fits (b_{m0} prod_{q in S} d_q <= tile_cap).  Each S is scored by the gates the pass
+// would apply with in-tile set S — a gate qualifies when its target is in the low prefix or
+// in S and it commutes with every earlier gate of W left behind — and the best S (first found
+// on ties) restricts which targets the pass admits.  Pairwise commutation inside W is computed
+// once as bitsets, so scoring one S is O(|W|).
+// commute() with the diagonal flags precomputed (span-1 gates; others take commute()).
+static bool commute_fast(const GateSpec &a, bool da, const GateSpec &b, bool db) {
+    if (a.span != 1 || b.span != 1) return commute(a, b);
+    if (a.target == b.target) return da && db;
+    if (!da)
+        for (const auto &c : b.ctrl)
+            if (c.q == a.target) return false;
+    if (!db)
+        for (const auto &c : a.ctrl)
+            if (c.q == b.target) return false;
+    return true;
+}
+
+static std::vector<char> best_in_tile_set(const Register &reg, const std::vector<GateSpec> &g,
+                                          const std::vector<char> &diag,
+                                          const std::vector<char> &done, size_t first, int m0,
+                                          uint64_t base_tile, uint64_t tile_cap, int max_gates, int window) {
+    std::vector<size_t> W;
+    for (size_t i = first; i < g.size() && (int)W.size() < window && W.size() < 256; ++i)
+        if (!done[i]) W.push_back(i);
+    const size_t nw = W.size();
+    const size_t nwords = (nw + 63) / 64;
+    // blocked[b]: bitset of earlier window gates a with !commute(a, b)
+    std::vector<uint64_t> blocked(nw * nwords, 0);
+    std::vector<char> eligible(nw, 0);
+    std::vector<int> cand;
+    for (size_t b = 0; b < nw; ++b) {
+        const GateSpec &x = g[W[b]];
+        eligible[b] = x.span == 1 && x.ctrl.size() <= 4;
+        for (size_t a = 0; a < b; ++a)
+            if (!commute_fast(g[W[a]], diag[W[a]], x, diag[W[b]])) blocked[b * nwords + a / 64] |= 1ull << (a % 64);
+        if (x.target >= m0 && std::find(cand.begin(), cand.end(), x.target) == cand.end()) cand.push_back(x.target);
+    }
+    if (cand.size() > 12) cand.resize(12);     // bound the enumeration (first-seen targets kept;
+                                               // 12 plans c3/c4 as well as 20: 36 / 22 passes)
+    const uint64_t lim = tile_cap / base_tile;
+    std::vector<char> inS(reg.n, 0), best(reg.n, 0);
+    int best_n = -1;
+    std::vector<uint64_t> skipped(nwords);
+    auto score = [&]() {
+        std::fill(skipped.begin(), skipped.end(), 0);
+        int cnt = 0;
+        for (size_t b = 0; b < nw && cnt < max_gates; ++b) {
+            const GateSpec &x = g[W[b]];
+            bool ok = eligible[b] && (x.target < m0 || inS[x.target]);
+            for (size_t w = 0; ok && w < nwords; ++w)
+                if (skipped[w] & blocked[b * nwords + w]) ok = false;
+            if (ok) ++cnt;
+            else skipped[b / 64] |= 1ull << (b % 64);
+        }
+        if (cnt > best_n) { best_n = cnt; best = inS; }
+    };
+    // Depth-first over subsets in candidate order, pruned by the tile capacity.  The score is
+    // monotone in S (a gate admitted with S is admitted with any superset: by induction over
+    // the window, the superset leaves behind a subset of the gates), so only subsets that no
+    // later candidate extends are scored, and the search stops once a pass is full.
+    std::function<void(size_t, uint64_t)> rec = [&](size_t start, uint64_t prod) {
+        bool extended = false;
+        for (size_t k = start; k < cand.size() && best_n < max_gates; ++k) {
+            const uint64_t p = prod * (uint64_t)reg.dims[cand[k]];
+            if (p > lim) continue;
+            extended = true;
+            inS[cand[k]] = 1;
+            rec(k + 1, p);
+            inS[cand[k]] = 0;
+        }
+        if (!extended && best_n < max_gates) score();
+    };
+    rec(0, 1);
+    return best;
+}
+
 std::vector<PassPlan> plan_passes(const Register &reg, const std::vector<GateSpec> &g, uint64_t tile_cap,
-                                  int max_gates, int window) {
+                                  int max_gates, int window, bool search) {
     std::vector<PassPlan> passes;
+    std::vector<char> diag(g.size(), 0);
+    if (search)
+        for (size_t i = 0; i < g.size(); ++i) diag[i] = is_diag(g[i]);
     // forced low prefix: every qudit whose stride is < 32 amplitudes
     int m0 = 0;
     while (m0 < reg.n && reg.b[m0] < 32) ++m0;
@@ -329,6 +412,8 @@ std::vector<PassPlan> plan_passes(const Register &reg, const std::vector<GateSpe
         uint64_t tile = base_tile;
         std::vector<size_t> skipped;
         int seen = 0;
+        std::vector<char> allowed;
+        if (search) allowed = best_in_tile_set(reg, g, diag, done, first, m0, base_tile, tile_cap, max_gates, window);
         for (size_t i = first; i < g.size() && seen < window && (int)pp.gates.size() < max_gates; ++i) {
             if (done[i]) continue;
             ++seen;
@@ -338,6 +423,7 @@ std::vector<PassPlan> plan_passes(const Register &reg, const std::vector<GateSpe
                 if (ok && !commute(g[s], x)) ok = false;
             uint64_t need = tile;
             if (ok && x.target >= m0 && !inq[x.target]) need = tile * (uint64_t)reg.dims[x.target];
+            if (ok && x.target >= m0 && !allowed.empty() && !allowed[x.target]) ok = false;
             if (ok && need > tile_cap) ok = false;
             if (!ok) {
                 skipped.push_back(i);

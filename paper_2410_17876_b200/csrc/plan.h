@@ -74,8 +74,10 @@ struct PassPlan {
     int m0 = 0;                  // low prefix q_0..q_{m0-1}
     uint64_t tile = 0;           // amplitudes per tile = b_{m0} * prod_{h in H} d_h
 };
+// search: choose each pass's in-tile set by scoring every subset of the window's targets
+// that fits (else first come, first admitted).
 std::vector<PassPlan> plan_passes(const Register &reg, const std::vector<GateSpec> &g, uint64_t tile_cap,
-                                  int max_gates, int window);
+                                  int max_gates, int window, bool search = true);
 
 // Launch one multi-gate pass (mgpass.cu).  *handled = false if the pass does not fit the
 // kernel (the caller then applies its gates one by one); *touched = sum of T over its gates.

@@ -35,6 +35,11 @@ struct sv_state_s {
     std::vector<unsigned char> graph_key;
     cudaGraphExec_t graph_exec = nullptr;
     uint64_t graph_kernels = 0;
+    // SV_BLOCK: the last host plan (merged gates + passes), reused while the same gate list and
+    // configuration are submitted again (host memoisation only: every pass still launches)
+    std::vector<unsigned char> plan_key;
+    std::vector<svi::GateSpec> plan_specs;
+    std::vector<svi::PassPlan> plan_passes;
     // gate-time errors are reported through the thread-local message in sv_api.cpp
 };
 

@@ -67,6 +67,7 @@ void default_cfg(LaunchCfg &c, int device) {
     c.pass_merge = 1;          // commutation-aware merging before pass planning
     c.pass_groups = 2;         // two consumer groups ping-pong over tiles
     c.shard_swap = 1;          // qubit remapping for gates on sharded qubits
+    c.pass_search = 1;         // in-tile set chosen by subset search (c4 29 -> 22 passes)
 }
 
 }  // namespace
@@ -238,8 +239,18 @@ sv_status run_local_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_t 
     }
     std::vector<PassPlan> passes;
     if (flags & SV_BLOCK) {
-        if (h->cfg.pass_merge) specs = merge_commuting(specs, 64);
-        passes = plan_passes(h->local, specs, (uint64_t)h->cfg.pass_tile, h->cfg.pass_gates, h->cfg.pass_window);
+        std::vector<unsigned char> pkey = graph_key(h, specs, flags & (SV_BLOCK | SV_FUSE), nullptr);
+        if (pkey == h->plan_key) {                 // same gates and configuration: same plan
+            specs = h->plan_specs;
+            passes = h->plan_passes;
+        } else {
+            if (h->cfg.pass_merge) specs = merge_commuting(specs, 64);
+            passes = plan_passes(h->local, specs, (uint64_t)h->cfg.pass_tile, h->cfg.pass_gates,
+                                 h->cfg.pass_window, h->cfg.pass_search != 0);
+            h->plan_key.swap(pkey);
+            h->plan_specs = specs;
+            h->plan_passes = passes;
+        }
     } else {
         if (flags & SV_FUSE) specs = fuse_gates(h->local, specs);
         for (size_t i = 0; i < specs.size(); ++i) {
@@ -509,6 +520,9 @@ sv_status sv_set_option(sv_handle h, int32_t option, int64_t value) {
             return SV_OK;
         case SV_OPT_SHARD_SWAP:
             h->cfg.shard_swap = value != 0;
+            return SV_OK;
+        case SV_OPT_PASS_SEARCH:
+            h->cfg.pass_search = value != 0;
             return SV_OK;
         case SV_OPT_PASS_WINDOW:
             if (value < 1 || value > 4096) return fail(SV_ERR_INVALID_ARG, "pass window 1..4096");

@@ -200,6 +200,7 @@ struct LaunchCfg {
     int pass_merge;    // 1: merge same-target same-control gates across commuting ones first
     int pass_groups;   // consumer warp groups of the pass kernel (ping-pong over tiles)
     int shard_swap;    // 1: sharded mode remaps qubits instead of pairwise exchanges (shard.cpp vi)
+    int pass_search;   // 1: pass planner scores in-tile sets (plan.cpp best_in_tile_set)
     int c64;           // 1: the state is complex64 (float2), else complex128 (double2)
 };
 

@@ -590,3 +590,24 @@ def test_edge_cases_every_driver_mode(P, mode):
     got, nrm, _ = run_gpu(P, dims, gates, psi0, **kw)
     assert np.max(np.abs(got - ref)) <= 1e-12
     assert abs(nrm - 1.0) <= 1e-10
+
+
+def test_block_plan_cache_follows_the_gates(P):
+    """The SV_BLOCK host plan is memoised per handle: resubmitting a circuit reuses it, while a
+    changed matrix, gate order or option plans afresh (results against the oracle each time)."""
+    rng = np.random.default_rng(5)
+    dims = [3, 2, 4, 2, 3, 2, 2, 5, 2]
+    D = int(np.prod(dims))
+    _, gates = random_circuit(55, dims, 150, max_ctrl=2)
+    other = list(gates)
+    other[10] = Gate(other[10].target, other[10].ctrl, other[10].vals, haar_unitary(dims[other[10].target], rng))
+    psi = random_state(D, 2)
+    with P.State(dims) as st:
+        st.set_amplitudes(0, psi)
+        for circ in (gates, gates, other, gates[::-1], gates, "opt", gates):
+            if circ == "opt":
+                st.set_option(P.sv.SV_OPT_PASS_SEARCH, 0)
+                continue
+            st.apply_circuit(circ, block=True)
+            psi = O2.run(dims, circ, psi)
+            assert np.max(np.abs(st.amplitudes() - psi)) <= 1e-11

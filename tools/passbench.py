@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--windows", default="64")
     ap.add_argument("--dtype", default="c128", choices=["c128", "c64"])
     ap.add_argument("--reps", type=int, default=1)
+    ap.add_argument("--search", type=int, default=1, help="SV_OPT_PASS_SEARCH (in-tile set search)")
     args = ap.parse_args()
     import torch
     import paper_2410_17876_b200 as P
@@ -52,6 +53,7 @@ def main():
             st.set_option(P.sv.SV_OPT_PASS_GATES, ng)
             st.set_option(P.sv.SV_OPT_PASS_GROUPS, rest[0])
             st.set_option(P.sv.SV_OPT_PASS_WINDOW, rest[1])
+            st.set_option(P.sv.SV_OPT_PASS_SEARCH, args.search)
         st.reset(0)
         st.apply_circuit(ga, fuse=True, check=False, block=block)
         st.sync()
