@@ -220,6 +220,19 @@ def test_block_planner_reorders_only_commuting_gates():
         assert np.max(np.abs(got - ref)) < 1e-12
 
 
+def test_block_planner_subset_search_pass_count():
+    """The in-tile set search (plan.cpp best_in_tile_set): on the full c4 circuit after merging,
+    the pass count stays at or below the searched plan's 23 (first-come admission: 30 at this
+    window), and every tile fits."""
+    from sv_inputs import Gate
+    dims, gates = config_circuit(4)
+    merged = [Gate(t, c, v, U) for (t, sp, k, c, v, U) in P.merge_plan(dims, gates, 64)]
+    order, pid, tiles = P.block_plan(dims, merged, 4096)
+    assert sorted(order.tolist()) == list(range(len(merged)))
+    assert len(tiles) <= 23
+    assert all(t <= 4096 for t in tiles)
+
+
 def test_merge_planner_preserves_the_circuit():
     """The SV_BLOCK pre-pass (sv_merge_plan): gates move back across gates they commute with and
     merge with an earlier same-target, same-control gate.  The merged list must give the same
