@@ -62,8 +62,8 @@ void default_cfg(LaunchCfg &c, int device) {
     c.pass_tile = 4096;        // measured best on c2-c4 (profiles/r01/passbench_*_groups.jsonl)
     c.pass_stages = 3;
     c.pass_threads = 512;
-    c.pass_gates = 24;
-    c.pass_window = 128;       // gates scanned ahead when filling a pass (c4 -4%, c3 +2%: profiles/r01/ab/window_*)
+    c.pass_gates = 32;         // with the in-tile set search: c3 -1.4%, c4 unchanged (ab/gates_window_*)
+    c.pass_window = 256;       // gates scanned ahead when filling a pass (profiles/r01/ab/window_*, ab/gates_window_*)
     c.pass_merge = 1;          // commutation-aware merging before pass planning
     c.pass_groups = 2;         // two consumer groups ping-pong over tiles
     c.shard_swap = 1;          // qubit remapping for gates on sharded qubits
