@@ -95,11 +95,6 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def touched_total(dims, gates):
-    """sum_g T_g from the library's host planner (no device work)."""
-    return circuit_work(dims, gates)[0]
-
-
 def circuit_work(dims, gates):
     """Per circuit, from the library's host planner: sum_g T_g (touched amplitudes) and the
     FP64 flops of the general gates (8 d flop per touched amplitude: a d x d complex matvec per
@@ -122,41 +117,91 @@ FP64_TFLOPS = 35.7
 SMEM_B_PER_CLK_SM = 128
 
 
-def cpu_baseline(cfg: int, budget_s: float = 20.0):
-    """O-2 on a bounded sample: the same recipe on a register with fewer qubits (3), gates
-    applied in order until ~budget_s of CPU time."""
+def host_info():
+    """The host the oracle runs on: logical CPUs, sockets, cores, NUMA nodes, RAM."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            k, v = k.strip(), v.strip()
+            if k in ("Socket(s)", "Core(s) per socket", "Thread(s) per core", "NUMA node(s)", "Model name"):
+                info[k] = v
+    except Exception:
+        pass
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemTotal:"):
+                    info["ram_gb"] = round(int(line.split()[1]) / 1e6, 1)
+    except Exception:
+        pass
+    return info
+
+
+def workload_config(cfg: int, dtype: str = "c128"):
+    """The workload both arms are quoted on (identical dicts; implementation options go under
+    the line's "mode")."""
+    from sv_inputs import config_circuit, CONFIG_NAMES
+    dims = config_circuit(cfg, ngates=0)[0]
+    D = int(np.prod(dims, dtype=object))
+    ngates = len(config_circuit(cfg)[1])
+    elem = 16 if dtype == "c128" else 8
+    return {"workload": CONFIG_NAMES[cfg], "dims_q0_first": dims,
+            "state_dtype": "complex128" if dtype == "c128" else "complex64", "D": D, "gates": ngates,
+            "initial_state": "e_0", "l2": "state (%.1f GB) >> L2 (126 MB): no flush needed" % (elem * D / 1e9)}
+
+
+def _oracle_sample(cfg: int, budget_s: float, threads: int | None = None):
+    """O-2 on a bounded sample of the workload: the same recipe on a register with fewer qubits,
+    gates applied in order until ~budget_s of host time.  Work counted by oracle/work.py (the
+    metric's definition); the product library is not loaded."""
     from oracle import blocksim as O2
+    from oracle import work as W
     from sv_inputs import config_circuit
     nq = {3: 12, 4: 5, 5: 4}.get(cfg, None)        # ~10-20 s of O-2 work on 16 cores
     dims, gates = config_circuit(cfg, nqubits=nq)
     D = int(np.prod(dims))
     psi = np.zeros(D, dtype=np.complex128)
     psi[0] = 1.0
-    import paper_2410_17876_b200 as P
-    t0 = time.perf_counter()
-    upd, ng = 0, 0
-    for g in gates:
-        O2.apply(psi, dims, g)
-        upd += int(P.plan_gate(dims, g.target, g.U, g.ctrl, g.vals).touched)
-        ng += 1
-        if time.perf_counter() - t0 > budget_s:
-            break
-    dt = time.perf_counter() - t0
-    return {"value": upd / dt, "unit": UNIT, "cores": O2.num_threads(), "kind": "oracle",
-            "sample": f"config {cfg} recipe with {nq} qubits (D={D}), first {ng} of {len(gates)} gates, "
-                      f"{dt:.1f} s on the host"}
+    nt0 = O2.num_threads()
+    if threads:
+        O2.set_threads(threads)
+    try:
+        cores = O2.num_threads()
+        t0 = time.perf_counter()
+        upd, ng = 0, 0
+        for g in gates:
+            O2.apply(psi, dims, g)
+            ng += 1
+            if time.perf_counter() - t0 > budget_s:
+                break
+        dt = time.perf_counter() - t0
+    finally:
+        O2.set_threads(nt0)
+    upd = W.circuit_touched(dims, gates[:ng])
+    return upd / dt, cores, (f"config {cfg} recipe with {nq} qubits (D={D}), first {ng} of {len(gates)} "
+                             f"gates, {dt:.1f} s on the host")
+
+
+def cpu_baseline(cfg: int, budget_s: float = 20.0):
+    """O-2 on a bounded sample (all host threads), plus the same sample on one thread."""
+    v, cores, sample = _oracle_sample(cfg, budget_s)
+    v1, _, sample1 = _oracle_sample(cfg, budget_s / 4, threads=1)
+    return {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+            "one_thread": {"value": v1, "sample": sample1}, "host": host_info()}
 
 
 def run_reference(args, rank, world):
     """The tier's reference arm: the CPU oracle O-2 as it stands, on the host cores.  One step =
     the next few gates of the same recipe on a bounded register (5 qubits instead of 10 for c4)
-    so that W + K steps finish in about a minute; only the K steps are timed."""
+    so that W + K steps finish in about a minute; only the K steps are timed.  Loads only
+    oracle/ and sv_inputs/ (work counted by oracle/work.py)."""
     if rank != 0:
         return
     from oracle import blocksim as O2
-    from sv_inputs import config_circuit, CONFIG_NAMES
-    import paper_2410_17876_b200 as P
-    full_dims = config_circuit(args.config, ngates=0)[0]      # the workload the arm is quoted on
+    from oracle import work as W
+    from sv_inputs import config_circuit
     nq = {3: 7, 4: 5, 5: 4}.get(args.config, None)
     dims, gates = config_circuit(args.config, nqubits=nq)
     D = int(np.prod(dims))
@@ -173,18 +218,18 @@ def run_reference(args, rank, world):
         dt = time.perf_counter() - t0
         if step >= args.warmup:
             t += dt
-            upd += sum(int(P.plan_gate(dims, g.target, g.U, g.ctrl, g.vals).touched) for g in chunk)
+            upd += W.circuit_touched(dims, chunk)
     value = upd / t
     b = {"value": value, "unit": UNIT, "cores": O2.num_threads(), "kind": "oracle",
          "sample": f"config {args.config} recipe with {nq} qubits (D={D}), {per_step} gates per step, "
-                   f"{args.steps} timed steps after {args.warmup} warm-up steps"}
+                   f"{args.steps} timed steps after {args.warmup} warm-up steps",
+         "host": host_info()}
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * t / max(1, args.steps), "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": CONFIG_NAMES[args.config], "dims_q0_first": full_dims,
-                       "sample_dims_q0_first": dims},
+            "config": workload_config(args.config),
             "cpu_baseline": b,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -252,7 +297,13 @@ def main():
         st.reset(0)
         st.apply_circuit(ga, fuse=fuse, check=False, block=block, graph=graph)
 
-    for _ in range(args.warmup):
+    # ---- cold first submission: a fresh handle's first circuit, host planning included
+    st.sync()
+    t0 = time.perf_counter()
+    step()
+    st.sync()
+    cold_first_s = time.perf_counter() - t0
+    for _ in range(max(0, args.warmup - 1)):
         step()
     st.sync()
     # ---- timed region: K steps, barrier + sync on both sides, CUDA events on the library stream
@@ -283,61 +334,96 @@ def main():
     value = T_step * args.steps / (ms / 1e3)
 
     # ---- e2e: the public API end to end with host buffers (gate matrices in, norm + the
-    # first 4096 amplitudes out), timed on the same stream
+    # first 4096 amplitudes out), timed on the host around the whole call sequence.  Warm: the
+    # handle's memoised host plan is reused (the same circuit every step); cold: the plan cache
+    # is off, so every step plans (merge + pass planning) from scratch.
     out = np.empty(nread, dtype=np.complex128)
     h2d = sum(16 * g.U.size + 8 * len(g.ctrl) + 8 for g in gates)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        st.reset(0)
-        st.apply_circuit(gates, fuse=fuse, check=True, block=block, graph=graph)   # host gates each step
-        nrm = st.norm()
-        st.amplitudes(0, nread, out)
-    t_e2e = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_e2e = float(t.item())
-    e2e = {"value": T_step * args.steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-           "d2h_bytes_per_step": int(8 + 16 * nread), "norm": nrm}
+
+    def e2e_run(cache: bool):
+        st.set_option(P.sv.SV_OPT_PLAN_CACHE, 1 if cache else 0)
+        st.profile_read(reset=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            st.reset(0)
+            st.apply_circuit(gates, fuse=fuse, check=True, block=block, graph=graph)   # host gates each step
+            nrm = st.norm()
+            st.amplitudes(0, nread, out)
+        dt = time.perf_counter() - t0
+        plan_ms = st.profile_read(reset=True).plan_ms / args.steps
+        st.set_option(P.sv.SV_OPT_PLAN_CACHE, 1)
+        if world > 1:
+            t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        return T_step * args.steps / dt, nrm, plan_ms
+
+    v_warm, nrm, plan_warm = e2e_run(True)
+    v_cold, _, plan_cold = e2e_run(False)
+    e2e = {"value": v_warm, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": int(8 + 16 * nread), "norm": nrm,
+           "host_plan_ms_per_step": plan_warm,
+           "cold": {"value": v_cold, "host_plan_ms_per_step": plan_cold,
+                    "note": "plan cache off: merge + pass planning on every submission"},
+           "first_submission_s": cold_first_s}
 
     hbm, hbm_src = peaks()
-    bytes_per_launch = prof.algorithmic_bytes / max(1, prof.launches)
-    ms_per_launch = prof.kernel_ms / max(1, prof.launches)
-    achieved = bytes_per_launch / (ms_per_launch / 1e3) / 1e9 if prof.launches else None
-    # bytes the launches must move at least (a multi-gate pass: the state once)
-    state_bytes_per_launch = prof.state_bytes / max(1, prof.launches)
-    state_gbs = state_bytes_per_launch / (ms_per_launch / 1e3) / 1e9 if prof.launches else None
-    traffic = None
+    bpu = 32.0 if args.dtype == "c128" else 16.0      # bytes per amplitude update (read + write)
+    traffic_ratio, traffic_note = None, None
     tr_path = os.path.join(ROOT, "profiles", "traffic.json")
-    traffic_note = None
     if os.path.exists(tr_path):
         try:
             tr = json.load(open(tr_path))["block" if block else "single"]
-            # DRAM bytes / minimum bytes from one `ncu --set full` capture of the dominant kernel
-            # (reduced register), applied to this run's minimum bytes per launch
-            traffic = tr["ratio_dram_to_state_bytes"] * state_bytes_per_launch
-            traffic_note = tr["source"]
+            traffic_ratio, traffic_note = tr["ratio_dram_to_state_bytes"], tr["source"]
         except Exception:
-            traffic = None
-
-    bpu = 32.0 if args.dtype == "c128" else 16.0      # bytes per amplitude update (read + write)
-    # The pass kernel's own roofline: per launch it must stream the state through HBM once,
-    # move 32 B per touched amplitude of each gate through shared memory and do the general
-    # gates' FP64 flops; the binding resource sets its lower-bound time.
-    pass_roofline = None
-    if block and prof.launches and world == 1 and args.dtype == "c128":
-        sm_hz = (clk.summary().get("sm_mhz") or 1965.0) * 1e6
-        per_launch = {"hbm": state_bytes_per_launch / (hbm * 1e9),
-                      "smem": bpu * T_step * args.steps / prof.launches / (SMEM_B_PER_CLK_SM * 148 * sm_hz),
-                      "fp64": F_step * args.steps / prof.launches / (FP64_TFLOPS * 1e12)}
-        b = max(per_launch, key=per_launch.get)
-        pass_roofline = {"bound": b, "lower_bound_ms_per_launch": {k: 1e3 * v for k, v in per_launch.items()},
-                         "ms_per_launch": ms_per_launch, "frac": 1e3 * per_launch[b] / ms_per_launch,
-                         "peaks": {"hbm_gbs": hbm, "fp64_tflops": FP64_TFLOPS,
-                                   "smem_bytes_per_clk_per_sm": SMEM_B_PER_CLK_SM, "sm_mhz": sm_hz / 1e6}}
+            pass
+    sm_mhz = clk.summary().get("sm_mhz") or 1965.0
+    if block and prof.pass_launches:
+        # the dominant kernel: k_gate_pass.  Its algorithmic HBM bytes per launch are the state
+        # once in and once out (2 x elem x D_local); achieved = that / the mean event-timed launch.
+        n_l = prof.pass_launches
+        ms_l = prof.pass_ms / n_l
+        state_b = prof.pass_state_bytes / n_l
+        achieved = state_b / (ms_l / 1e3) / 1e9
+        # executed work per launch (merged and paired gates, one smem round trip per item)
+        floors = {"hbm": state_b / (hbm * 1e9),
+                  "smem": bpu * prof.pass_item_touched / n_l / (SMEM_B_PER_CLK_SM * 148 * sm_mhz * 1e6),
+                  "fp64": prof.pass_flops / n_l / (FP64_TFLOPS * 1e12)} if args.dtype == "c128" else None
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                    "traffic": traffic_ratio * state_b if traffic_ratio else None,
+                    "kernel": "k_gate_pass", "algorithmic": "2 x elem bytes x local state per pass (one HBM "
+                    "round trip of the state; SURVEY.md 8(d) per-unit 32 B x D amplitudes)",
+                    "bytes_per_launch": state_b, "ms_per_launch": ms_l, "launches_timed": int(n_l),
+                    "share_of_step": prof.pass_ms / ms if ms else None,
+                    "peak_source": hbm_src, "traffic_source": traffic_note}
+        pass_roofline = None
+        if floors:
+            b = max(floors, key=floors.get)
+            pass_roofline = {"bound": b, "frac": 1e3 * floors[b] / ms_l, "ms_per_launch": ms_l,
+                             "lower_bound_ms_per_launch": {k: 1e3 * v for k, v in floors.items()},
+                             "executed_per_launch": {"touched": prof.pass_touched / n_l,
+                                                     "smem_round_trip_amplitudes": prof.pass_item_touched / n_l,
+                                                     "fp64_flops": prof.pass_flops / n_l},
+                             "peaks": {"hbm_gbs": hbm, "fp64_tflops": FP64_TFLOPS,
+                                       "smem_bytes_per_clk_per_sm": SMEM_B_PER_CLK_SM, "sm_mhz": sm_mhz},
+                             "note": "floors from the executed (merged, paired) gates of each pass"}
+    else:
+        n_l = max(1, prof.launches)
+        ms_l = prof.kernel_ms / n_l
+        b_l = prof.algorithmic_bytes / n_l
+        achieved = b_l / (ms_l / 1e3) / 1e9 if prof.launches else None
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                    "frac": achieved / hbm if achieved else None,
+                    "traffic": traffic_ratio * b_l if traffic_ratio else None,
+                    "kernel": "single-gate kernels (k_gate_tiled / k_gate_direct)",
+                    "algorithmic": "32 B x touched amplitudes per gate launch (SURVEY.md 8(d))",
+                    "bytes_per_launch": b_l, "ms_per_launch": ms_l, "launches_timed": int(prof.launches),
+                    "share_of_step": prof.kernel_ms / ms if ms else None,
+                    "peak_source": hbm_src, "traffic_source": traffic_note}
+        pass_roofline = None
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -345,28 +431,14 @@ def main():
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
             "dtype": "f64" if args.dtype == "c128" else "f32",
             "data": "synthetic",
-            "config": {"workload": CONFIG_NAMES[args.config], "dims_q0_first": dims,
-                       "state_dtype": "complex128" if args.dtype == "c128" else "complex64",
-                       "D": int(np.prod(dims, dtype=object)), "gates": len(gates), "fuse": fuse, "block_passes": block,
-                       "cuda_graph": graph,
-                       "kernel": args.kernel, "sharded_ranks": world,
-                       "l2": "state (%.1f GB) >> L2 (126 MB): no flush needed" % (16 * np.prod(dims, dtype=object) / 1e9)},
+            "config": workload_config(args.config, args.dtype),
+            "mode": {"fuse": fuse, "block_passes": block, "cuda_graph": graph, "kernel": args.kernel,
+                     "sharded_ranks": world, "gates_timed": len(gates)},
             "hbm_gbs": bpu * value / 1e9,
-            "hbm_frac_of_measured": bpu * value / 1e9 / hbm if world == 1 else None,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
-                         "traffic_source": traffic_note,
-                         "peak_source": hbm_src,
-                         "kernel": ("k_gate_pass (multi-gate passes) + single-gate kernels" if block
-                                    else "single-gate kernels (k_gate_tiled / k_gate_direct)"),
-                         "algorithmic": "32 B x sum of touched amplitudes of the gates applied (SURVEY.md 8(d))",
-                         "note": ("a multi-gate pass applies ~10 gates per HBM round trip of the state, so the "
-                                  "per-gate algorithmic rate exceeds the HBM peak; the pass kernel's own binding "
-                                  "resource and fraction are in pass_roofline") if block else None,
-                         "bytes_per_launch": bytes_per_launch, "ms_per_launch": ms_per_launch,
-                         "state_bytes_per_launch": state_bytes_per_launch,
-                         "state_gbs": state_gbs,
-                         "launches_timed": int(prof.launches)},
+            "effective_hbm_frac": bpu * value / 1e9 / hbm if world == 1 else None,
+            "effective_note": "32 B x sum of T over the user's gates / step time, over the measured HBM peak: "
+                              "above 1 when a pass applies several gates per HBM round trip",
+            "roofline": roofline,
             "pass_roofline": pass_roofline,
             "e2e": e2e,
             "gpu_launches": int(launches),

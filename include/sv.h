@@ -71,7 +71,8 @@ typedef enum {
     SV_ERR_INDEX_RANGE = 9,   /* basis index / amplitude range outside [0, D)            */
     SV_ERR_NOMEM = 10,        /* device allocation failed                                */
     SV_ERR_CUDA = 11,         /* CUDA error (sticky)                                     */
-    SV_ERR_NCCL = 12,         /* NCCL error (sharded mode)                               */
+    SV_ERR_NCCL = 12,         /* communication error in sharded mode: NCCL, or the IPC
+                                 transport (a peer failed or timed out); sticky            */
     SV_ERR_UNSUPPORTED = 13   /* valid request outside what this build implements       */
 } sv_status;
 
@@ -128,9 +129,29 @@ SV_API sv_status sv_create_sharded(const int32_t *dims, int32_t n, sv_dtype dt, 
                             void *cuda_stream, sv_handle *out);
 SV_API sv_status sv_nccl_unique_id(void *out128);
 
+/* Sharded state over the fused peer-memory transport (same layout, rules and
+ * SPMD contract as sv_create_sharded).  The nranks processes run on ONE node (one GPU each,
+ * or several on one GPU): each rank maps every other rank's slice through CUDA IPC, and a gate
+ * on a sharded qubit runs as ONE kernel per rank that reads and writes the partner's slice in
+ * place over NVLink — rank lo of the pair updates the classes of local indices [0, L/2), rank hi
+ * the rest, (lo_i, hi_i) <- U (lo_i, hi_i) — and a qubit remapping swaps the two
+ * half-slices element by element; no staging buffer, no combine pass.  Ranks order these
+ * accesses with host barriers in POSIX shared memory (the kernels never wait on each other);
+ * norms reduce through it in rank order (deterministic).  ipc_id: the 128-byte id produced by
+ * sv_ipc_unique_id on one rank and broadcast by the caller (a shared-memory name).  Every
+ * rank must create, use and destroy the state together; a rank that stops (timeout
+ * SV_COMM_TIMEOUT_S, default 600 s) makes the others fail with SV_ERR_NCCL instead of hanging.
+ * Errors: as sv_create_sharded; SV_ERR_NCCL if the control block cannot be created;
+ * SV_ERR_CUDA if CUDA IPC fails (e.g. no peer access between the GPUs). */
+SV_API sv_status sv_create_sharded_ipc(const int32_t *dims, int32_t n, sv_dtype dt, int32_t rank,
+                                       int32_t nranks, const void *ipc_id, int device,
+                                       void *cuda_stream, sv_handle *out);
+SV_API sv_status sv_ipc_unique_id(void *out128);
+
 SV_API sv_status sv_destroy(sv_handle h);
 
-/* State = basis vector e_{basis_index}.  SV_ERR_INDEX_RANGE if basis_index >= D. */
+/* State = basis vector e_{basis_index} (the paper's initial state is e_0 = |0...0>,
+ * PAPER.md:247).  SV_ERR_INDEX_RANGE if basis_index >= D. */
 SV_API sv_status sv_reset(sv_handle h, uint64_t basis_index);
 
 /* ---- the hot path --------------------------------------------------------------------- */
@@ -141,7 +162,8 @@ SV_API sv_status sv_apply_gate(sv_handle h, int32_t target, const int32_t *ctrl,
                         const int32_t *ctrl_vals, int32_t nctrl, const double *U);
 
 /* Validate all gates first (state untouched on any error), then apply them in order
- * (gate after gate).  flags: SV_FUSE | SV_NO_CHECK | SV_GRAPH. */
+ * (gate after gate; SV_BLOCK may reorder commuting gates, which leaves the result
+ * unchanged up to rounding).  flags: SV_FUSE | SV_NO_CHECK | SV_GRAPH | SV_BLOCK. */
 SV_API sv_status sv_apply_circuit(sv_handle h, const sv_gate *gates, int64_t ngates, uint32_t flags);
 
 /* ---- readback ------------------------------------------------------------------------- */
@@ -158,8 +180,13 @@ SV_API sv_status sv_set_amplitudes(sv_handle h, uint64_t first, uint64_t count, 
  * Sharded: collective (all-reduce of the squared partial norms). */
 SV_API sv_status sv_norm(sv_handle h, double *out);
 
+/* Wait until every kernel queued on the handle's stream has finished (readback and setup
+ * calls synchronise on their own; this makes a timed region end on the device
+ * semantics of a completed evolution).  SV_ERR_CUDA reports an asynchronous fault (sticky). */
 SV_API sv_status sv_sync(sv_handle h);
 
+/* Thread-local message for the last failing call on this thread (empty if none); valid until
+ * the next failing call on the same thread.  Mirrors SPEC.md:45, 261, 346's error names. */
 SV_API const char *sv_last_error(void);
 
 /* ---- introspection (tests, bench) -------------------------------------------------------- */
@@ -200,6 +227,9 @@ SV_API sv_status sv_get_info(sv_handle h, sv_info *out);
 #define SV_OPT_PASS_SEARCH 14   /* 1 (default): each SV_BLOCK pass's in-tile qudit set is the one that
                                    admits the most window gates (subset search); 0: first come, first
                                    admitted */
+#define SV_OPT_PLAN_CACHE  15   /* 1 (default): the SV_BLOCK host plan (merged gates + passes) is
+                                   memoised per handle and reused while the same gates and options
+                                   come again; 0: plan every call (cold-submission timing)          */
 SV_API sv_status sv_set_option(sv_handle h, int32_t option, int64_t value);
 
 /* Per-launch timing of the gate kernels recorded while SV_OPT_PROFILE is on: the summed
@@ -214,6 +244,16 @@ typedef struct {
     double touched;            /* amplitude updates (sum of T over the launched gates)          */
     double state_bytes;        /* bytes the launches must move at least: a single-gate launch
                                   2 x elem x T; a multi-gate pass (SV_BLOCK) 2 x elem x the state */
+    /* the multi-gate pass launches (k_gate_pass) among them, as executed (merged, paired): */
+    uint64_t pass_launches;
+    double pass_ms;
+    double pass_touched;       /* sum of T over the gates the passes applied                   */
+    double pass_item_touched;  /* amplitudes read + written in shared memory, one round trip per
+                                  executed item (a gate, or a qubit pair applied as one class)   */
+    double pass_flops;         /* FP64 flops of the general items: 8 d per touched amplitude     */
+    double pass_state_bytes;   /* 2 x elem x the local state per pass                           */
+    double plan_ms;            /* host planning time (SV_BLOCK merge + pass planning) since the
+                                  last reset                                                    */
 } sv_profile;
 SV_API sv_status sv_profile_read(sv_handle h, int32_t reset, sv_profile *out);
 

@@ -238,6 +238,73 @@ int orc_gate_output_labelled(int n, const int *dims, int target, int nctrl, cons
     return 0;
 }
 
+/* One output amplitude of a short circuit g_1..g_G applied to the labelled state, for sampled
+ * full-size checks of multi-gate passes.  Gate by gate from the last one back (PAPER.md:256
+ * applies them in order, so the amplitude after g_k at index i is fixed by the amplitudes
+ * after g_{k-1}): if g_k's controls hold at i, it is row v of U_k times the
+ * class vector of i after g_{k-1} (v = digit of i in q_t), else the amplitude
+ * after g_{k-1} at i.  Cost prod_k d_k evaluations per index: short circuits. */
+static void circuit_value(uint64_t i, int64_t k, const int *dims, const uint64_t *b,
+                          const int *targets, const int *nctrls, const int64_t *coff,
+                          const int *ctrl_flat, const int *vals_flat, const int64_t *uoff,
+                          const double *U_flat, double *re, double *im)
+{
+    if (k == 0) { label(i, re, im); return; }
+    const int64_t g = k - 1;
+    const int t = targets[g];
+    if (!controls_hold(i, nctrls[g], ctrl_flat + coff[g], vals_flat + coff[g], b, dims)) {
+        circuit_value(i, k - 1, dims, b, targets, nctrls, coff, ctrl_flat, vals_flat, uoff, U_flat, re, im);
+        return;
+    }
+    const int d = dims[t];
+    const uint64_t bs = b[t];
+    const int v = (int)((i / bs) % (uint64_t)d);
+    const uint64_t base = i - (uint64_t)v * bs;
+    const double *U = U_flat + uoff[g];
+    double yr = 0.0, yi = 0.0;
+    for (int j = 0; j < d; ++j) {
+        double xr, xi;
+        circuit_value(base + (uint64_t)j * bs, k - 1, dims, b, targets, nctrls, coff, ctrl_flat,
+                      vals_flat, uoff, U_flat, &xr, &xi);
+        const double ur = U[2 * (v * d + j)], ui = U[2 * (v * d + j) + 1];
+        yr += ur * xr - ui * xi;
+        yi += ur * xi + ui * xr;
+    }
+    *re = yr;
+    *im = yi;
+}
+
+int orc_circuit_output_labelled(int n, const int *dims, int64_t ngates, const int *targets,
+                                const int *nctrls, const int *ctrl_flat, const int *vals_flat,
+                                const double *U_flat, const uint64_t *idx, int64_t count, double *out)
+{
+    uint64_t b[64], D;
+    if (n < 1 || n > 64 || ngates < 0 || ngates > 8 || orc_strides(n, dims, b, &D)) return -1;
+    int64_t coff[8], uoff[8], co = 0, uo = 0;
+    for (int64_t g = 0; g < ngates; ++g) {
+        if (targets[g] < 0 || targets[g] >= n) return -1;
+        coff[g] = co;
+        uoff[g] = uo;
+        co += nctrls[g];
+        uo += 2 * (int64_t)dims[targets[g]] * dims[targets[g]];
+    }
+    #pragma omp parallel for schedule(static)
+    for (int64_t s = 0; s < count; ++s)
+        circuit_value(idx[s], ngates, dims, b, targets, nctrls, coff, ctrl_flat, vals_flat, uoff, U_flat,
+                      &out[2 * s], &out[2 * s + 1]);
+    return 0;
+}
+
+/* OpenMP thread count of later calls (the bench's 1-thread baseline run); n < 1 keeps it. */
+void orc_set_threads(int n)
+{
+#ifdef _OPENMP
+    if (n >= 1) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 int orc_num_threads(void)
 {
 #ifdef _OPENMP

@@ -39,7 +39,10 @@ def lib():
         L.orc_strides.argtypes = [C.c_int, _ip, _up, _up]
         L.orc_gate_output_labelled.argtypes = [C.c_int, _ip, C.c_int, C.c_int, _ip, _ip, _dp,
                                                _up, C.c_int64, _dp]
+        L.orc_circuit_output_labelled.argtypes = [C.c_int, _ip, C.c_int64, _ip, _ip, _ip, _ip, _dp,
+                                                  _up, C.c_int64, _dp]
         L.orc_num_threads.restype = C.c_int
+        L.orc_set_threads.argtypes = [C.c_int]
         _lib = L
     return _lib
 
@@ -145,5 +148,29 @@ def gate_output_labelled(dims, gate, idx) -> np.ndarray:
     return out
 
 
+def circuit_output_labelled(dims, gates, idx) -> np.ndarray:
+    """Sampled outputs of a short circuit (<= 8 gates) applied to the labelled state."""
+    dims_a = _i32(dims)
+    targets = _i32([g.target for g in gates] or [0])
+    nctrls = _i32([len(g.ctrl) for g in gates] or [0])
+    cf = _i32([c for g in gates for c in g.ctrl] or [0])
+    vf = _i32([v for g in gates for v in g.vals] or [0])
+    Uf = np.ascontiguousarray(np.concatenate([np.asarray(g.U, np.complex128).ravel() for g in gates]
+                                             or [np.zeros(1, np.complex128)]))
+    idx = np.ascontiguousarray(np.asarray(idx, dtype=np.uint64))
+    out = np.zeros(idx.size, dtype=np.complex128)
+    rc = lib().orc_circuit_output_labelled(len(dims_a), _ptr(dims_a, _ip), len(gates), _ptr(targets, _ip),
+                                           _ptr(nctrls, _ip), _ptr(cf, _ip), _ptr(vf, _ip),
+                                           _ptr(Uf.view(np.float64), _dp), _ptr(idx, _up), idx.size,
+                                           _ptr(out.view(np.float64), _dp))
+    if rc:
+        raise ValueError("oracle rejected circuit")
+    return out
+
+
 def num_threads() -> int:
     return int(lib().orc_num_threads())
+
+
+def set_threads(n: int) -> None:
+    lib().orc_set_threads(int(n))

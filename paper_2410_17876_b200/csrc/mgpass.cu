@@ -40,15 +40,26 @@ constexpr int kMaxPairDim = 4;             // pair gates: d_a d_b <= 4 (qubit pa
 enum PassKind : int32_t { kPGeneral = 0, kPMonomial = 1, kPPerm = 2 };
 
 // a control decided at run time (in-tile controls on H / low-prefix digits are enumerated)
+// Run-digit controls (digits below min H and above the low prefix) come in two forms:
+//   cls 1: b_c d_c < 2^31 — the digit of run position s0 + l is read from (s0 mod b_c d_c) + l
+//          in 32-bit arithmetic (fastdiv32 is exact for divisors <= 2^31);
+//   cls 3: b_c d_c >= 2^31 (registers with D > 2^32 whose pass has no H digit, so a run spans
+//          the register) — b_c >= 2^27 exceeds any tile, so the digit changes at most once
+//          inside a tile; the producer decides, in 64-bit arithmetic, the range of l where it
+//          equals the control value.
 struct PassCtrl {
-    int32_t cls;          // 1 = run digit above the low prefix (needs the tile's run offset), 2 = outside the tile
+    int32_t cls;          // 1, 3 = run digit above the low prefix (see above), 2 = outside the tile
     uint32_t v;
     uint32_t d, md;       // control dimension (+ magic)
     uint32_t w, mw;       // cls 1: stride b_c (+ magic)
-    uint32_t M, mM;       // cls 1: b_c * d_c (+ magic)
-    uint64_t b64, mb64;   // cls 2: global stride (+ magic); cls 1: 64-bit magic of M
-    uint64_t md64;        // cls 2: magic for d
+    uint32_t M, mM;       // cls 1: b_c * d_c < 2^31 (+ magic)
+    uint64_t b64, mb64;   // cls 2, 3: global stride (+ magic); cls 1: 64-bit magic of M
+    uint64_t md64;        // cls 2, 3: magic for d
 };
+
+// cls 3 per-tile record: the control holds for run positions l < t (mode 1), l >= t (mode 2)
+// or none (mode 0); t < 2^30 is clamped (tiles are at most 8192 positions long).
+constexpr uint32_t kCls3Mask = (1u << 30) - 1u;
 
 enum PassFlags : uint32_t { kFRunCtrl = 4 };
 
@@ -158,6 +169,15 @@ __device__ __forceinline__ void issue_loads(const PassParams &p, uint64_t t, V *
                 uint64_t r;
                 fastdiv64(ti.s0, cc.M, cc.mb64, r);
                 si->lowoff[lane][k] = (uint32_t)r;
+            } else if (cc.cls == 3) {
+                uint64_t r0, dig;
+                const uint64_t q = fastdiv64(ti.s0, cc.b64, cc.mb64, r0);
+                fastdiv64(q, cc.d, cc.md64, dig);                  // digit of q_c at position s0
+                const uint64_t nxt = (dig + 1 == cc.d) ? 0 : dig + 1;   // after the one change
+                uint64_t t = cc.b64 - r0;                          // first l where the digit changes
+                if (t > kCls3Mask) t = kCls3Mask;
+                const uint32_t mode = dig == cc.v ? 1u : (nxt == cc.v ? 2u : 0u);
+                si->lowoff[lane][k] = (uint32_t)t | (mode << 30);
             }
         }
     }
@@ -225,6 +245,11 @@ __device__ __forceinline__ bool class_ok(const TileGate &tg, const PassGateP &g,
 #pragma unroll 1
         for (int k = 0; k < g.nctrl; ++k) {
             const PassCtrl &cc = g.c[k];
+            if (cc.cls == 3) {
+                const uint32_t x = tg.lowoff[k], t = x & kCls3Mask, mode = x >> 30;
+                ok = ok && (mode == 1 ? l < t : (mode == 2 && l >= t));
+                continue;
+            }
             if (cc.cls != 1) continue;
             uint32_t r, r2;
             fastdiv32(tg.lowoff[k] + l, cc.M, cc.mM, r);
@@ -543,7 +568,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant_
 // ------------------------------------------------------------------------------ host
 // Build the pass parameters; returns false if the pass does not fit this kernel.
 bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const PassPlan &pp, double2 *psi,
-                int TE, PassParams &p, double *touched) {
+                int TE, PassParams &p, PassWork *work) {
     std::memset(&p, 0, sizeof(p));
     if ((int)pp.gates.size() > kMaxPassGates || pp.tile > (uint64_t)TE) return false;
     p.psi = psi;
@@ -634,14 +659,14 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
     }
     // gates
     int uoff = 0;
-    *touched = 0.0;
+    *work = PassWork{};
     p.ngates = (int32_t)items.size();
     for (size_t gi = 0; gi < items.size(); ++gi) {
         const GateSpec &g = gates[items[gi].a];
         GatePlan gp;
         std::string err;
         if (plan_gate(reg, g, false, &gp, &err) != SV_OK) return false;
-        *touched += (double)gp.touched;
+        work->touched += (double)gp.touched;
         PassGateP &q = p.g[gi];
         const int t = g.target;
         const uint64_t st = tile_stride(t);
@@ -664,7 +689,7 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
             const GateSpec &h = gates[items[gi].b];      // h acts on digit b (second), g on a
             GatePlan hp;
             if (plan_gate(reg, h, false, &hp, &err) != SV_OK) return false;
-            *touched += (double)hp.touched;
+            work->touched += (double)hp.touched;
             const int da = gp.d, db = hp.d;
             D = da * db;
             const uint64_t stb = tile_stride(h.target);
@@ -702,6 +727,14 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
         }
         q.d = D;
         q.kind = kind == kGeneral ? kPGeneral : kPMonomial;
+        {   // executed work of this item: its control-satisfying classes x moving members
+            double cprod = 1.0;
+            for (const auto &c : g.ctrl) cprod *= (double)reg.dims[c.q];
+            const double nact = (double)__builtin_popcount(q.active);
+            const double it = (double)reg.D / ((double)D * cprod) * nact;
+            work->item_touched += it;
+            if (kind == kGeneral) work->flops += 8.0 * D * it;
+        }
         if (q.kind == kPMonomial) {            // every moving coefficient exactly 1: pure data movement
             bool perm = true;
             for (int j = 0; j < D; ++j)
@@ -736,7 +769,7 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
             cc.v = v;
             cc.d = (uint32_t)dc;
             cc.md = make_fastdiv32(cc.d).m;
-            if (reg.b[c] < R) {                // run digit above the low prefix: tile's run offset
+            if (reg.b[c] < R && reg.b[c] * dc < (1ull << 31)) {   // run digit: tile's run offset
                 cc.cls = 1;
                 q.flags |= kFRunCtrl;
                 cc.w = (uint32_t)reg.b[c];
@@ -744,6 +777,12 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
                 cc.M = cc.w * cc.d;
                 cc.mM = make_fastdiv32(cc.M).m;
                 cc.mb64 = make_fastdiv64(cc.M).m;
+            } else if (reg.b[c] < R) {         // run digit with b_c d_c >= 2^31: per-tile threshold
+                cc.cls = 3;
+                q.flags |= kFRunCtrl;
+                cc.b64 = reg.b[c];
+                cc.mb64 = make_fastdiv64(cc.b64).m;
+                cc.md64 = make_fastdiv64(dc).m;
             } else {                           // outside the tile: constant per tile
                 cc.cls = 2;
                 cc.b64 = reg.b[c];
@@ -810,9 +849,9 @@ cudaError_t launch_pass(const PassParams &p, cudaStream_t st, const LaunchCfg &c
 }
 
 cudaError_t run_pass(const Register &reg, const std::vector<GateSpec> &gates, const PassPlan &pp, double2 *psi,
-                     cudaStream_t st, const LaunchCfg &cfg, bool *handled, double *touched) {
+                     cudaStream_t st, const LaunchCfg &cfg, bool *handled, PassWork *work) {
     static thread_local PassParams p;   // ~23 KB; parameters are copied at launch
-    *handled = build_pass(reg, gates, pp, psi, cfg.pass_tile, p, touched);
+    *handled = build_pass(reg, gates, pp, psi, cfg.pass_tile, p, work);
     // complex64 (8-byte elements): every bulk copy must start at a 16-byte aligned address and
     // move a multiple of 16 bytes; tile runs are multiples of L = b_{m0} and start at multiples
     // of L, so an even L suffices (the stage needs the tile plus the fp32 matrix pool)

@@ -79,10 +79,22 @@ struct PassPlan {
 std::vector<PassPlan> plan_passes(const Register &reg, const std::vector<GateSpec> &g, uint64_t tile_cap,
                                   int max_gates, int window, bool search = true);
 
+// Work of one multi-gate pass as executed (after merging and pairing), for the roofline:
+//   touched      sum of T over the pass's gates (SURVEY.md §8(d) amplitude updates);
+//   item_touched amplitudes each executed item (a gate, or a pair gate applied as one 4-member
+//                class) reads and writes in shared memory: one round trip per item;
+//   flops        FP64 flops of the general items, 8 d flop per touched amplitude (d x d
+//                complex matvec per class).
+struct PassWork {
+    double touched = 0.0;
+    double item_touched = 0.0;
+    double flops = 0.0;
+};
+
 // Launch one multi-gate pass (mgpass.cu).  *handled = false if the pass does not fit the
-// kernel (the caller then applies its gates one by one); *touched = sum of T over its gates.
+// kernel (the caller then applies its gates one by one).
 cudaError_t run_pass(const Register &reg, const std::vector<GateSpec> &gates, const PassPlan &pp, double2 *psi,
-                     cudaStream_t st, const LaunchCfg &cfg, bool *handled, double *touched);
+                     cudaStream_t st, const LaunchCfg &cfg, bool *handled, PassWork *work);
 
 // Shard planning.  s = log2(nranks) top digits are sharded qubits.
 struct ShardAction {

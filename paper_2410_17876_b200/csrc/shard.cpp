@@ -26,14 +26,31 @@
 // position pos_of[q] (disjoint local <-> sharded qubit pairs); gates are
 // translated to positions before planning, and readback / uploads first swap the qubits
 // back home.  sv_reset restores both identity maps.
-// Transport: NCCL send/recv over NVLink (one process per GPU; NCCL is dlopen'ed so the core
-// library loads without it), chunked and double-buffered on a comm stream so the transfer of
-// chunk c+1 overlaps the combine of chunk c.  A loopback transport (all P slices in one
-// process on one device, device copies instead of NCCL) exercises the same planner, rank
-// predicates, chunking and combine kernel on a single GPU.
+// Transports (one schedule, three ways to move the data):
+//   * IPC (sv_create_sharded_ipc): one process per rank on one node (one GPU each, or several
+//     ranks on one GPU for testing); every rank maps every other rank's slice through CUDA IPC
+//     and the fused peer kernels (peer.cu) read and write the partner's slice in place over
+//     NVLink — gate + exchange in one kernel, qubit swaps element by element, no staging.
+//     Ranks order their accesses with host barriers in POSIX shared memory (stream
+//     synchronise, then barrier, before and after every cross-rank kernel); the kernels never
+//     wait on another rank.  Norms reduce through the same shared memory in rank order.
+//   * NCCL send/recv over NVLink (one process per GPU; NCCL is dlopen'ed so the core library
+//     loads without it), chunked and double-buffered on a comm stream so the transfer of chunk
+//     c+1 overlaps the combine of chunk c (the baseline the fused path replaces).
+//   * Loopback: all P slices in one process on one device; the fused peer kernels run over
+//     the slice pairs (one kernel over both ranks' data), exercising the same planner, maps
+//     and rank predicates on a single GPU.
 #include <dlfcn.h>
+#include <fcntl.h>
+#include <sched.h>
+#include <sys/mman.h>
+#include <time.h>
+#include <unistd.h>
 
+#include <atomic>
+#include <chrono>
 #include <cstring>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -60,6 +77,8 @@ struct NcclApi {
     ncclResult_t (*Broadcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t,
                               cudaStream_t);
     const char *(*GetErrorString)(ncclResult_t);
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *) = nullptr;   // optional
+    ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;                           // optional
 };
 
 NcclApi &nccl() {
@@ -87,6 +106,8 @@ NcclApi &nccl() {
     SV_SYM(Broadcast, "ncclBroadcast");
     SV_SYM(GetErrorString, "ncclGetErrorString");
 #undef SV_SYM
+    api.CommGetAsyncError = reinterpret_cast<decltype(api.CommGetAsyncError)>(dlsym(lib, "ncclCommGetAsyncError"));
+    api.CommAbort = reinterpret_cast<decltype(api.CommAbort)>(dlsym(lib, "ncclCommAbort"));
     api.ok = true;
     return api;
 }
@@ -98,11 +119,39 @@ sv_status nccl_fail(sv_handle h, ncclResult_t r, const char *where) {
 
 }  // namespace
 
+// The IPC transport's control block, in POSIX shared memory (one per sharded state; all ranks
+// of one node map it).  Zero-filled on creation.
+constexpr int kMaxIpcRanks = 64;
+struct IpcShm {
+    std::atomic<uint32_t> arrived;          // barrier: ranks arrived in this generation
+    std::atomic<uint32_t> generation;       // barrier: completed barriers
+    std::atomic<uint32_t> failed;           // a rank gave up (timeout / fault): everyone stops
+    uint32_t pad;
+    cudaIpcMemHandle_t mem[kMaxIpcRanks];   // each rank's slice
+    int device[kMaxIpcRanks];
+    double red[2][kMaxIpcRanks];            // norm partials, double-buffered by parity
+};
+static_assert(std::atomic<uint32_t>::is_always_lock_free, "process-shared atomics");
+
+enum Transport { kLoopback = 0, kNccl = 1, kIpc = 2 };
+
+double comm_timeout_s() {
+    const char *e = getenv("SV_COMM_TIMEOUT_S");
+    const double t = e ? atof(e) : 600.0;
+    return t > 0 ? t : 600.0;
+}
+
 struct ShardCtx {
     int P = 1;
     int s = 0;
     int rank = 0;                  // -1: loopback (all ranks in this handle)
+    int transport = kLoopback;
     ncclComm_t comm = nullptr;
+    // IPC transport: every rank's slice mapped into this process (peer[rank] = own slice)
+    std::vector<double2 *> peer;
+    IpcShm *shm = nullptr;
+    char shm_name[129] = {0};      // unlinked once every rank has attached (or on failure)
+    int red_parity = 0;
     std::vector<double2 *> slices; // loopback: P slices (slices[0] is h->psi); NCCL: {h->psi}
     double2 *stage[2] = {nullptr, nullptr};
     uint64_t chunk = 0;            // amplitudes per exchange chunk
@@ -124,8 +173,19 @@ struct ShardCtx {
     }
 };
 
+sv_status ipc_barrier_raw(ShardCtx *c);
+
 void shard_destroy(ShardCtx *c) {
     if (!c) return;
+    if (c->transport == kIpc && c->shm) {
+        // peers may still read this slice until every rank has arrived here
+        cudaDeviceSynchronize();
+        ipc_barrier_raw(c);
+        for (int r = 0; r < (int)c->peer.size(); ++r)
+            if (r != c->rank && c->peer[r]) cudaIpcCloseMemHandle(c->peer[r]);
+        munmap(c->shm, sizeof(IpcShm));
+        if (c->shm_name[0]) shm_unlink(c->shm_name);     // no-op once unlinked
+    }
     if (c->comm) nccl().CommDestroy(c->comm);
     for (size_t i = 1; i < c->slices.size(); ++i) cudaFree(c->slices[i]);
     for (double2 *p : c->stage) if (p) cudaFree(p);
@@ -135,6 +195,37 @@ void shard_destroy(ShardCtx *c) {
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->d_scalar) cudaFree(c->d_scalar);
     delete c;
+}
+
+// Sense-reversing barrier over the ranks of an IPC state (host side only).  Spins with
+// sched_yield, then short sleeps; gives up after SV_COMM_TIMEOUT_S and marks the state failed
+// so that the other ranks stop too.
+sv_status ipc_barrier_raw(ShardCtx *c) {
+    IpcShm *m = c->shm;
+    const uint32_t g = m->generation.load(std::memory_order_acquire);
+    if (m->arrived.fetch_add(1, std::memory_order_acq_rel) == (uint32_t)c->P - 1) {
+        m->arrived.store(0, std::memory_order_relaxed);
+        m->generation.store(g + 1, std::memory_order_release);
+        return SV_OK;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    const double limit = comm_timeout_s();
+    for (uint64_t it = 0; m->generation.load(std::memory_order_acquire) == g; ++it) {
+        if (m->failed.load(std::memory_order_relaxed))
+            return fail_msg(SV_ERR_NCCL, "IPC transport: another rank failed");
+        if (it < 2048) {
+            sched_yield();
+            continue;
+        }
+        struct timespec ts = {0, 20000};
+        nanosleep(&ts, nullptr);
+        if ((it & 1023) == 0 &&
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit) {
+            m->failed.store(1, std::memory_order_relaxed);
+            return fail_msg(SV_ERR_NCCL, "IPC transport: barrier timeout (a peer process is gone or stuck)");
+        }
+    }
+    return SV_OK;
 }
 
 int shard_rank(const ShardCtx *c) { return c->rank; }
@@ -250,6 +341,20 @@ std::vector<std::pair<int, double2>> relabel(ShardCtx *c, const GateSpec &g, int
 
 bool owns(const ShardCtx *c, int r) { return c->loopback() || r == c->rank; }
 
+// IPC: this rank's queued work is complete and so is every other rank's (before a kernel
+// touches a peer's slice, and after, before anyone touches its own slice again).
+sv_status ipc_fence(sv_handle h) {
+    if (h->shard->transport != kIpc) return SV_OK;
+    sv_status s = shard_sync(h);
+    if (s != SV_OK) {
+        h->shard->shm->failed.store(1, std::memory_order_relaxed);
+        return s;
+    }
+    s = ipc_barrier_raw(h->shard);
+    if (s != SV_OK) h->broken = true;
+    return s;
+}
+
 // A logical gate at the current digit positions (rule vi).
 GateSpec to_phys(const ShardCtx *c, const GateSpec &g) {
     GateSpec p = g;
@@ -310,23 +415,31 @@ sv_status swap_qubits(sv_handle h, int k, int j) {
                 out.push_back({m + (uint64_t)v * b + o, (b - o < c->chunk) ? b - o : c->chunk});
         return out;
     };
-    for (int r : ranks_of(c)) {
+    if (c->transport == kIpc) {                  // fused: half of the pair's swap space per rank
+        sv_status s = ipc_fence(h);
+        if (s != SV_OK) return s;
+        const int r = c->rank, l = c->lrank[r], beta = (l >> j) & 1;
+        const int p = c->prank[l ^ (1 << j)];
+        const uint64_t half = L / 2, q0 = half / 2;  // swap space [0, L/2): lo rank [0, q0), hi rank the rest
+        cudaError_t e = launch_pair_swap(at(c->peer[r], (uint64_t)(1 - beta) * b, h->elem),
+                                         at(c->peer[p], (uint64_t)beta * b, h->elem), b, beta ? q0 : 0,
+                                         beta ? half - q0 : q0, h->stream, h->cfg.num_sms, &h->launches, h->c64);
+        if (e != cudaSuccess) return cuda_fail_h(h, e, "peer qubit swap");
+        ++h->exchanges;
+        s = ipc_fence(h);
+        if (s != SV_OK) return s;
+    }
+    for (int r : (c->transport == kIpc ? std::vector<int>{} : ranks_of(c))) {
         const int l = c->lrank[r];
         const int beta = (l >> j) & 1;
         const int p = c->prank[l ^ (1 << j)];
         const auto mine = pieces(1 - beta);          // what this rank gives away
         if (c->loopback()) {
-            if (p < r) continue;                      // each pair once
-            const auto theirs = pieces(beta);         // the partner's (its digit j is 1 - beta)
-            for (size_t x = 0; x < mine.size(); ++x) {
-                const size_t bytes = mine[x].second * h->elem;
-                double2 *a = at(c->slices[r], mine[x].first, h->elem);
-                double2 *bb = at(c->slices[p], theirs[x].first, h->elem);
-                cudaError_t e = cudaMemcpyAsync(c->stage[0], a, bytes, cudaMemcpyDeviceToDevice, h->stream);
-                if (e == cudaSuccess) e = cudaMemcpyAsync(a, bb, bytes, cudaMemcpyDeviceToDevice, h->stream);
-                if (e == cudaSuccess) e = cudaMemcpyAsync(bb, c->stage[0], bytes, cudaMemcpyDeviceToDevice, h->stream);
-                if (e != cudaSuccess) return cuda_fail_h(h, e, "loopback qubit swap");
-            }
+            if (p < r) continue;                      // each pair once: one kernel over both slices
+            cudaError_t e = launch_pair_swap(at(c->slices[r], (uint64_t)(1 - beta) * b, h->elem),
+                                             at(c->slices[p], (uint64_t)beta * b, h->elem), b, 0, L / 2, h->stream,
+                                             h->cfg.num_sms, &h->launches, h->c64);
+            if (e != cudaSuccess) return cuda_fail_h(h, e, "loopback qubit swap");
             ++h->exchanges;
             continue;
         }
@@ -337,7 +450,10 @@ sv_status swap_qubits(sv_handle h, int k, int j) {
         for (size_t x = 0; x < mine.size(); ++x) {
             const uint64_t len = mine[x].second;
             const int sb = (int)(x & 1);
-            if (x >= 2) cudaStreamWaitEvent(c->comm_stream, c->ev_done[sb], 0);   // stage free again
+            if (x >= 2) {                                                   // stage free again
+                e = cudaStreamWaitEvent(c->comm_stream, c->ev_done[sb], 0);
+                if (e != cudaSuccess) return cuda_fail_h(h, e, "qubit swap stage wait");
+            }
             double2 *a = at(c->slices[0], mine[x].first, h->elem);
             ncclResult_t rr = nccl().GroupStart();
             if (rr == ncclSuccess) rr = nccl().Send(a, 2 * len, ty, p, c->comm, c->comm_stream);
@@ -394,7 +510,10 @@ sv_status exchange_nccl(sv_handle h, const GateSpec &g, const ShardAction &a) {
     for (uint64_t off = 0; off < L; off += c->chunk, ++k) {
         const uint64_t len = (L - off < c->chunk) ? L - off : c->chunk;
         const int sb = (int)(k & 1);
-        if (k >= 2) cudaStreamWaitEvent(c->comm_stream, c->ev_done[sb], 0);   // stage free again
+        if (k >= 2) {                                                       // stage free again
+            e = cudaStreamWaitEvent(c->comm_stream, c->ev_done[sb], 0);
+            if (e != cudaSuccess) return cuda_fail_h(h, e, "exchange stage wait");
+        }
         ncclResult_t r = nccl().GroupStart();
         const ncclDataType_t ty = h->c64 ? ncclFloat32 : ncclFloat64;     // 2 reals per amplitude
         if (r == ncclSuccess) r = nccl().Send(at(c->slices[0], off, h->elem), 2 * len, ty, a.partner, c->comm, c->comm_stream);
@@ -414,29 +533,14 @@ sv_status exchange_nccl(sv_handle h, const GateSpec &g, const ShardAction &a) {
     return SV_OK;
 }
 
-sv_status exchange_loopback(sv_handle h, const GateSpec &g, int r, const ShardAction &a,
-                            const ShardAction &ap) {
-    ShardCtx *c = h->shard;
-    const int p = a.partner;
-    const double2 Ar = g.U[a.beta * 2 + a.beta], Br = g.U[a.beta * 2 + (1 - a.beta)];
-    const double2 Ap = g.U[ap.beta * 2 + ap.beta], Bp = g.U[ap.beta * 2 + (1 - ap.beta)];
+// Rule iii through peer memory (loopback: one kernel over both slices; IPC: each rank of the
+// pair updates half of the local indices, reading and writing the partner's slice in place).
+// lo = the slice whose digit of the target is 0.
+sv_status exchange_fused(sv_handle h, const GateSpec &g, double2 *lo, double2 *hi, uint64_t first, uint64_t n) {
+    const double2 u[4] = {g.U[0], g.U[1], g.U[2], g.U[3]};
     const CombineCtrl cc = local_ctrl(h->local, g.ctrl);
-    const uint64_t L = h->local.D;
-    for (uint64_t off = 0; off < L; off += c->chunk) {
-        const uint64_t len = (L - off < c->chunk) ? L - off : c->chunk;
-        cudaError_t e = cudaMemcpyAsync(c->stage[0], at(c->slices[r], off, h->elem), len * h->elem,
-                                        cudaMemcpyDeviceToDevice, h->stream);
-        if (e == cudaSuccess)
-            e = cudaMemcpyAsync(c->stage[1], at(c->slices[p], off, h->elem), len * h->elem,
-                                cudaMemcpyDeviceToDevice, h->stream);
-        if (e == cudaSuccess)
-            e = launch_combine(at(c->slices[r], off, h->elem), c->stage[1], len, off, Ar, Br, cc, h->stream,
-                               &h->launches, h->c64);
-        if (e == cudaSuccess)
-            e = launch_combine(at(c->slices[p], off, h->elem), c->stage[0], len, off, Ap, Bp, cc, h->stream,
-                               &h->launches, h->c64);
-        if (e != cudaSuccess) return cuda_fail_h(h, e, "loopback exchange");
-    }
+    cudaError_t e = launch_pair_update(lo, hi, first, n, u, cc, h->stream, h->cfg.num_sms, &h->launches, h->c64);
+    if (e != cudaSuccess) return cuda_fail_h(h, e, "fused exchange");
     ++h->exchanges;
     return SV_OK;
 }
@@ -474,6 +578,10 @@ sv_status apply_phys(sv_handle h, const GateSpec &g) {
     for (const auto &cs : g.ctrl)
         if (cs.q < h->local.n) gl.ctrl.push_back(cs);
     std::vector<int> done(c->P, 0);
+    if (c->transport == kIpc) {           // every rank takes part in the fences, firing or not
+        sv_status s = ipc_fence(h);
+        if (s != SV_OK) return s;
+    }
     for (int r : ranks_of(c)) {
         if (done[r]) continue;
         ShardAction a;   // planned on logical slice indices; partner mapped back to a rank
@@ -490,18 +598,22 @@ sv_status apply_phys(sv_handle h, const GateSpec &g) {
         }
         const int lpartner = a.partner;
         a.partner = c->prank[lpartner];
+        const uint64_t L = h->local.D;
         if (c->loopback()) {
-            ShardAction ap;
-            s = shard_plan(h->reg, c->P, lpartner, g.target, g.ctrl, &ap, err);
-            if (s != SV_OK) return s;
-            ap.partner = r;
-            s = exchange_loopback(h, g, r, a, ap);
+            double2 *mine = c->slices[r], *theirs = c->slices[a.partner];
+            s = exchange_fused(h, g, a.beta ? theirs : mine, a.beta ? mine : theirs, 0, L);
             done[a.partner] = 1;
+        } else if (c->transport == kIpc) {
+            double2 *mine = c->peer[r], *theirs = c->peer[a.partner];
+            const uint64_t h0 = L / 2;        // lo rank: local indices [0, L/2), hi rank: the rest
+            s = exchange_fused(h, g, a.beta ? theirs : mine, a.beta ? mine : theirs, a.beta ? h0 : 0,
+                               a.beta ? L - h0 : h0);
         } else {
             s = exchange_nccl(h, g, a);
         }
         if (s != SV_OK) return s;
     }
+    if (c->transport == kIpc) return ipc_fence(h);
     return SV_OK;
 }
 
@@ -670,23 +782,27 @@ sv_status shard_amplitudes(sv_handle h, uint64_t first, uint64_t count, double *
     ShardCtx *c = h->shard;
     sv_status rs = restore_layout(h);
     if (rs != SV_OK) return rs;
+    rs = ipc_fence(h);                       // IPC: every rank's slice final before anyone reads
+    if (rs != SV_OK) return rs;
     const uint64_t L = h->local.D;
     for (int r = 0; r < c->P; ++r) {
         const uint64_t lo = (uint64_t)c->lrank[r] * L, hi = lo + L;
         const uint64_t a = first > lo ? first : lo, b = (first + count) < hi ? first + count : hi;
         if (a >= b) continue;
-        if (c->loopback() && !h->c64) {
-            cudaError_t e = cudaMemcpyAsync(out + 2 * (a - first), c->slices[r] + (a - lo),
+        // loopback: the slice is in this handle; IPC: read the owner's slice through its mapping
+        double2 *src = c->loopback() ? c->slices[r] : (c->transport == kIpc ? c->peer[r] : nullptr);
+        if (src && !h->c64) {
+            cudaError_t e = cudaMemcpyAsync(out + 2 * (a - first), src + (a - lo),
                                             (b - a) * sizeof(double2), cudaMemcpyDeviceToHost, h->stream);
             if (e != cudaSuccess) return cuda_fail_h(h, e, "sharded readback");
             continue;
         }
-        if (c->loopback()) {                 // complex64: widen to the ABI's doubles on the host
+        if (src) {                           // complex64: widen to the ABI's doubles on the host
             const uint64_t chunk = 1ull << 22;
             std::vector<float2> tmp((size_t)((b - a) < chunk ? (b - a) : chunk));
             for (uint64_t o = a; o < b; o += chunk) {
                 const uint64_t n = (b - o) < chunk ? b - o : chunk;
-                cudaError_t e = cudaMemcpyAsync(tmp.data(), at(c->slices[r], o - lo, h->elem), n * h->elem,
+                cudaError_t e = cudaMemcpyAsync(tmp.data(), at(src, o - lo, h->elem), n * h->elem,
                                                 cudaMemcpyDeviceToHost, h->stream);
                 if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
                 if (e != cudaSuccess) return cuda_fail_h(h, e, "sharded readback");
@@ -723,11 +839,22 @@ sv_status shard_amplitudes(sv_handle h, uint64_t first, uint64_t count, double *
     }
     cudaError_t e = cudaStreamSynchronize(h->stream);
     if (e != cudaSuccess) return cuda_fail_h(h, e, "sharded readback");
-    return SV_OK;
+    return ipc_fence(h);                     // IPC: nobody writes a slice another rank still reads
 }
 
 sv_status shard_allreduce_sum(sv_handle h, double *v) {
     ShardCtx *c = h->shard;
+    if (c->transport == kIpc) {   // partials through shared memory, summed in rank order
+        const int par = c->red_parity;
+        c->red_parity ^= 1;
+        c->shm->red[par][c->rank] = *v;
+        sv_status s = ipc_barrier_raw(c);
+        if (s != SV_OK) { h->broken = true; return s; }
+        double t = 0.0;
+        for (int r = 0; r < c->P; ++r) t += c->shm->red[par][r];
+        *v = t;
+        return SV_OK;
+    }
     if (c->loopback()) {   // local_norm2 covered slice 0; add the others
         double2 *keep = h->psi;
         for (int r = 1; r < c->P; ++r) {
@@ -750,6 +877,43 @@ sv_status shard_allreduce_sum(sv_handle h, double *v) {
     return SV_OK;
 }
 
+// Wait for the handle's stream while watching the transport: NCCL asynchronous errors abort the
+// communicator; an IPC peer that gave up stops this rank too; nothing completes within
+// SV_COMM_TIMEOUT_S -> abort.  The handle is unusable after a failure (sticky, like CUDA faults).
+sv_status shard_sync(sv_handle h) {
+    ShardCtx *c = h->shard;
+    const auto t0 = std::chrono::steady_clock::now();
+    const double limit = comm_timeout_s();
+    for (uint64_t it = 0;; ++it) {
+        cudaError_t e = cudaStreamQuery(h->stream);
+        if (e == cudaSuccess) break;
+        if (e != cudaErrorNotReady) return cuda_fail_h(h, e, "sharded sync");
+        if (c->transport == kNccl && c->comm && nccl().CommGetAsyncError) {
+            ncclResult_t ae = ncclSuccess;
+            if (nccl().CommGetAsyncError(c->comm, &ae) == ncclSuccess && ae != ncclSuccess && ae != ncclInProgress) {
+                if (nccl().CommAbort) nccl().CommAbort(c->comm);
+                c->comm = nullptr;
+                return nccl_fail(h, ae, "NCCL asynchronous error (communicator aborted)");
+            }
+        }
+        if (c->transport == kIpc && c->shm->failed.load(std::memory_order_relaxed)) {
+            h->broken = true;
+            return fail_msg(SV_ERR_NCCL, "IPC transport: another rank failed");
+        }
+        if (it < 256) { sched_yield(); continue; }
+        struct timespec ts = {0, 50000};
+        nanosleep(&ts, nullptr);
+        if ((it & 255) == 0 &&
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit) {
+            if (c->transport == kNccl && c->comm && nccl().CommAbort) { nccl().CommAbort(c->comm); c->comm = nullptr; }
+            if (c->transport == kIpc) c->shm->failed.store(1, std::memory_order_relaxed);
+            h->broken = true;
+            return fail_msg(SV_ERR_NCCL, "sharded sync: timeout (SV_COMM_TIMEOUT_S)");
+        }
+    }
+    return SV_OK;
+}
+
 }  // namespace svi
 
 using namespace svi;
@@ -766,8 +930,8 @@ sv_status sv_nccl_unique_id(void *out128) {
     return SV_OK;
 }
 
-sv_status sv_create_sharded(const int32_t *dims, int32_t n, sv_dtype dt, int32_t rank, int32_t nranks,
-                            const void *nccl_unique_id, int device, void *cuda_stream, sv_handle *out) {
+static sv_status create_sharded(const int32_t *dims, int32_t n, sv_dtype dt, int32_t rank, int32_t nranks,
+                                int transport, const void *id128, int device, void *cuda_stream, sv_handle *out) {
     if (!out) return fail_msg(SV_ERR_INVALID_ARG, "null out");
     *out = nullptr;
     if (nranks == 1 && rank <= 0)
@@ -775,6 +939,9 @@ sv_status sv_create_sharded(const int32_t *dims, int32_t n, sv_dtype dt, int32_t
     if (dt != SV_C128 && dt != SV_C64) return fail_msg(SV_ERR_INVALID_ARG, "unknown dtype");
     if (nranks < 1 || (nranks & (nranks - 1))) return fail_msg(SV_ERR_INVALID_ARG, "nranks must be a power of two");
     if (rank < -1 || rank >= nranks) return fail_msg(SV_ERR_INVALID_ARG, "rank out of range");
+    if (transport == kIpc && (rank < 0 || nranks > kMaxIpcRanks))
+        return fail_msg(SV_ERR_INVALID_ARG, "IPC transport: rank 0..nranks-1, nranks <= 64");
+    if (transport != kLoopback && !id128) return fail_msg(SV_ERR_INVALID_ARG, "null unique id");
     sv_handle h = new (std::nothrow) sv_state_s();
     if (!h) return fail_msg(SV_ERR_NOMEM, "host allocation");
     std::string *err = err_slot();
@@ -793,25 +960,69 @@ sv_status sv_create_sharded(const int32_t *dims, int32_t n, sv_dtype dt, int32_t
     c->P = nranks;
     c->s = sh;
     c->rank = rank;
+    c->transport = transport;
     c->identity_map(n);
     h->shard = c;
+    if (transport == kIpc) {             // attach the control block before any device work
+        char name[129];
+        std::memcpy(name, id128, 128);
+        name[128] = 0;
+        if (name[0] != '/') { state_free(h); return fail_msg(SV_ERR_INVALID_ARG, "bad IPC id"); }
+        const int fd = shm_open(name, O_CREAT | O_RDWR, 0600);
+        if (fd < 0) { state_free(h); return fail_msg(SV_ERR_NCCL, std::string("shm_open ") + name + " failed"); }
+        if (ftruncate(fd, sizeof(IpcShm)) != 0) {
+            close(fd);
+            state_free(h);
+            return fail_msg(SV_ERR_NCCL, "ftruncate of the IPC control block failed");
+        }
+        void *m = mmap(nullptr, sizeof(IpcShm), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+        close(fd);
+        if (m == MAP_FAILED) { state_free(h); return fail_msg(SV_ERR_NCCL, "mmap of the IPC control block failed"); }
+        c->shm = reinterpret_cast<IpcShm *>(m);
+        std::memcpy(c->shm_name, name, sizeof(name));
+    }
     s = state_init_device(h, device, cuda_stream, nullptr, 0);
-    if (s != SV_OK) { state_free(h); return s; }
+    if (s != SV_OK) {
+        if (c->shm) c->shm->failed.store(1);
+        state_free(h);
+        return s;
+    }
     c->slices.push_back(h->psi);
     const uint64_t L = h->local.D;
     cudaError_t e = cudaSuccess;
-    if (c->loopback()) {
+    if (transport == kLoopback) {
         for (int r = 1; r < nranks && e == cudaSuccess; ++r) {
             double2 *p = nullptr;
             e = cudaMalloc(&p, L * h->elem);
             if (e == cudaSuccess) c->slices.push_back(p);
         }
         if (e != cudaSuccess) { cudaGetLastError(); state_free(h); return fail_msg(SV_ERR_NOMEM, "slice allocation"); }
+    } else if (transport == kIpc) {
+        // publish this rank's slice, then map every other rank's (CUDA IPC; across GPUs the
+        // mapping enables peer access over NVLink)
+        IpcShm *m = c->shm;
+        e = cudaIpcGetMemHandle(&m->mem[rank], h->psi);
+        m->device[rank] = device;
+        if (e != cudaSuccess) { m->failed.store(1); state_free(h); return cuda_fail_h(nullptr, e, "cudaIpcGetMemHandle"); }
+        s = ipc_barrier_raw(c);
+        if (s != SV_OK) { state_free(h); return s; }
+        c->peer.assign(nranks, nullptr);
+        c->peer[rank] = h->psi;
+        for (int r = 0; r < nranks && e == cudaSuccess; ++r) {
+            if (r == rank) continue;
+            void *p = nullptr;
+            e = cudaIpcOpenMemHandle(&p, m->mem[r], cudaIpcMemLazyEnablePeerAccess);
+            if (e == cudaSuccess) c->peer[r] = reinterpret_cast<double2 *>(p);
+        }
+        if (e != cudaSuccess) { m->failed.store(1); state_free(h); return cuda_fail_h(nullptr, e, "cudaIpcOpenMemHandle"); }
+        s = ipc_barrier_raw(c);                   // every rank attached: the name can go
+        if (s != SV_OK) { state_free(h); return s; }
+        shm_unlink(c->shm_name);                  // every rank; all but the first are no-ops
+        c->shm_name[0] = 0;
     } else {
-        if (!nccl_unique_id) { state_free(h); return fail_msg(SV_ERR_INVALID_ARG, "null nccl id"); }
         if (!nccl().ok) { state_free(h); return fail_msg(SV_ERR_NCCL, nccl().why); }
         ncclUniqueId id;
-        std::memcpy(&id, nccl_unique_id, sizeof(id));
+        std::memcpy(&id, id128, sizeof(id));
         ncclResult_t r = nccl().CommInitRank(&c->comm, nranks, id, rank);
         if (r != ncclSuccess) { s = nccl_fail(nullptr, r, "ncclCommInitRank"); c->comm = nullptr; state_free(h); return s; }
     }
@@ -819,19 +1030,44 @@ sv_status sv_create_sharded(const int32_t *dims, int32_t n, sv_dtype dt, int32_t
     c->chunk = ch ? strtoull(ch, nullptr, 10) : (16ull << 20);     // 16 Mi amplitudes = 256 MiB
     if (c->chunk == 0) c->chunk = 16ull << 20;
     if (c->chunk > L) c->chunk = L;
-    for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaMalloc(&c->stage[i], c->chunk * h->elem);
-    if (e == cudaSuccess) e = cudaMalloc(&c->d_scalar, sizeof(double));
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking);
-    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
-        e = cudaEventCreateWithFlags(&c->ev_recv[i], cudaEventDisableTiming);
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming);
+    if (transport == kNccl) {                 // staging and the comm stream: the NCCL path only
+        for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaMalloc(&c->stage[i], c->chunk * h->elem);
+        if (e == cudaSuccess) e = cudaMalloc(&c->d_scalar, sizeof(double));
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking);
+        for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+            e = cudaEventCreateWithFlags(&c->ev_recv[i], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming);
+        }
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming);
+        if (e != cudaSuccess) { cudaGetLastError(); state_free(h); return fail_msg(SV_ERR_NOMEM, "exchange buffers"); }
     }
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming);
-    if (e != cudaSuccess) { cudaGetLastError(); state_free(h); return fail_msg(SV_ERR_NOMEM, "exchange buffers"); }
     s = shard_reset(h, 0);
     if (s != SV_OK) { state_free(h); return s; }
     *out = h;
     return SV_OK;
+}
+
+sv_status sv_create_sharded(const int32_t *dims, int32_t n, sv_dtype dt, int32_t rank, int32_t nranks,
+                            const void *nccl_unique_id, int device, void *cuda_stream, sv_handle *out) {
+    return create_sharded(dims, n, dt, rank, nranks, rank < 0 ? kLoopback : kNccl, nccl_unique_id, device,
+                          cuda_stream, out);
+}
+
+sv_status sv_ipc_unique_id(void *out128) {
+    if (!out128) return fail_msg(SV_ERR_INVALID_ARG, "null out");
+    std::random_device rd;
+    const uint64_t a = ((uint64_t)rd() << 32) ^ rd(), b = ((uint64_t)rd() << 32) ^ rd();
+    char name[128];
+    std::memset(name, 0, sizeof(name));
+    snprintf(name, sizeof(name), "/sv_ipc_%d_%016llx%016llx", (int)getpid(), (unsigned long long)a,
+             (unsigned long long)b);
+    std::memcpy(out128, name, sizeof(name));
+    return SV_OK;
+}
+
+sv_status sv_create_sharded_ipc(const int32_t *dims, int32_t n, sv_dtype dt, int32_t rank, int32_t nranks,
+                                const void *ipc_id, int device, void *cuda_stream, sv_handle *out) {
+    return create_sharded(dims, n, dt, rank, nranks, kIpc, ipc_id, device, cuda_stream, out);
 }
 
 }  // extern "C"

@@ -46,4 +46,18 @@ cudaError_t launch_combine(double2 *loc, const double2 *partner, uint64_t n, uin
                            double2 a, double2 b, const CombineCtrl &cc, cudaStream_t st,
                            uint64_t *launches, bool c64 = false);
 
+// peer.cu: fused gate + exchange and in-place qubit swap over peer memory.
+// (lo_i, hi_i) <- (u[0] lo_i + u[1] hi_i, u[2] lo_i + u[3] hi_i) for i in [first, first+n) whose
+// local control digits match.
+cudaError_t launch_pair_update(double2 *lo, double2 *hi, uint64_t first, uint64_t n, const double2 u[4],
+                               const CombineCtrl &cc, cudaStream_t st, int num_sms, uint64_t *launches,
+                               bool c64 = false);
+// a[2 b m + o] <-> c[2 b m + o] for the swap-space elements e in [first, first+n), m = e / b, o = e mod b.
+cudaError_t launch_pair_swap(double2 *a, double2 *c, uint64_t b, uint64_t first, uint64_t n, cudaStream_t st,
+                             int num_sms, uint64_t *launches, bool c64 = false);
+
+// sv_sync / readback of a sharded handle: wait for its stream while watching the transport
+// (NCCL asynchronous errors, the IPC peers); aborts on a fault or after SV_COMM_TIMEOUT_S.
+sv_status shard_sync(sv_handle h);
+
 }  // namespace svi

@@ -28,8 +28,15 @@ struct sv_state_s {
     ShardCtx *shard = nullptr;     // non-null for sharded handles
     // SV_OPT_PROFILE: events bracketing each gate launch
     bool profile = false;
-    struct ProfRec { cudaEvent_t a, b; double bytes; double touched; double state_bytes; };
+    struct ProfRec {
+        cudaEvent_t a, b;
+        double bytes, touched, state_bytes;
+        bool pass;                       // a multi-gate pass (k_gate_pass)
+        double item_touched, flops;      // passes: executed shared-memory round trips, FP64 flops
+    };
     std::vector<ProfRec> prof;
+    double plan_ms = 0.0;              // host planning time (SV_BLOCK merge + passes), accumulated
+    bool plan_cache = true;            // SV_OPT_PLAN_CACHE
     std::vector<cudaEvent_t> ev_pool;
     // SV_GRAPH: the last captured circuit, replayed while the same circuit is submitted again
     std::vector<unsigned char> graph_key;

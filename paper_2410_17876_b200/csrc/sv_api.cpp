@@ -3,6 +3,7 @@
 // CPU fallback.
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <new>
@@ -158,7 +159,8 @@ sv_status launch_on(sv_handle h, const GatePlan &p, double2 *buf) {
     if (h->profile) {
         cudaEventRecord(b, h->stream);
         const double bpu = 2.0 * (double)h->elem;     // one read + one write per touched amplitude
-        h->prof.push_back({a, b, bpu * (double)p.touched, (double)p.touched, bpu * (double)p.touched});
+        h->prof.push_back({a, b, bpu * (double)p.touched, (double)p.touched, bpu * (double)p.touched, false,
+                           (double)p.touched, 0.0});
     }
     return SV_OK;
 }
@@ -176,8 +178,8 @@ static sv_status launch_pass_on(sv_handle h, const std::vector<GateSpec> &specs,
         cudaEventRecord(a, h->stream);
     }
     bool handled = false;
-    double touched = 0.0;
-    cudaError_t e = run_pass(h->local, specs, pp, buf, h->stream, h->cfg, &handled, &touched);
+    PassWork w;
+    cudaError_t e = run_pass(h->local, specs, pp, buf, h->stream, h->cfg, &handled, &w);
     if (e != cudaSuccess) return cuda_fail(h, e, "pass kernel launch");
     if (handled) {
         ++h->launches;
@@ -186,7 +188,8 @@ static sv_status launch_pass_on(sv_handle h, const std::vector<GateSpec> &specs,
             // algorithmic bytes per SURVEY.md §8(d): 32 B per touched amplitude of every gate the
             // pass applies; the pass itself moves the local state once (16 B read + 16 B write)
             const double bpu = 2.0 * (double)h->elem;     // one read + one write per amplitude
-            h->prof.push_back({a, b, bpu * touched, touched, bpu * (double)h->local.D});
+            h->prof.push_back({a, b, bpu * w.touched, w.touched, bpu * (double)h->local.D, true, w.item_touched,
+                               w.flops});
         }
         return SV_OK;
     }
@@ -239,18 +242,23 @@ sv_status run_local_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_t 
     }
     std::vector<PassPlan> passes;
     if (flags & SV_BLOCK) {
-        std::vector<unsigned char> pkey = graph_key(h, specs, flags & (SV_BLOCK | SV_FUSE), nullptr);
-        if (pkey == h->plan_key) {                 // same gates and configuration: same plan
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<unsigned char> pkey;
+        if (h->plan_cache) pkey = graph_key(h, specs, flags & (SV_BLOCK | SV_FUSE), nullptr);
+        if (h->plan_cache && pkey == h->plan_key) {     // same gates and configuration: same plan
             specs = h->plan_specs;
             passes = h->plan_passes;
         } else {
             if (h->cfg.pass_merge) specs = merge_commuting(specs, 64);
             passes = plan_passes(h->local, specs, (uint64_t)h->cfg.pass_tile, h->cfg.pass_gates,
                                  h->cfg.pass_window, h->cfg.pass_search != 0);
-            h->plan_key.swap(pkey);
-            h->plan_specs = specs;
-            h->plan_passes = passes;
+            if (h->plan_cache) {
+                h->plan_key.swap(pkey);
+                h->plan_specs = specs;
+                h->plan_passes = passes;
+            }
         }
+        h->plan_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     } else {
         if (flags & SV_FUSE) specs = fuse_gates(h->local, specs);
         for (size_t i = 0; i < specs.size(); ++i) {
@@ -462,6 +470,7 @@ sv_status sv_norm(sv_handle h, double *out) {
 sv_status sv_sync(sv_handle h) {
     sv_status s = check_handle(h);
     if (s != SV_OK) return s;
+    if (h->shard) return shard_sync(h);      // watches NCCL / IPC faults while waiting
     cudaError_t e = cudaStreamSynchronize(h->stream);
     if (e != cudaSuccess) return cuda_fail(h, e, "sync");
     return SV_OK;
@@ -524,6 +533,10 @@ sv_status sv_set_option(sv_handle h, int32_t option, int64_t value) {
         case SV_OPT_PASS_SEARCH:
             h->cfg.pass_search = value != 0;
             return SV_OK;
+        case SV_OPT_PLAN_CACHE:
+            h->plan_cache = value != 0;
+            if (!h->plan_cache) { h->plan_key.clear(); h->plan_specs.clear(); h->plan_passes.clear(); }
+            return SV_OK;
         case SV_OPT_PASS_WINDOW:
             if (value < 1 || value > 4096) return fail(SV_ERR_INVALID_ARG, "pass window 1..4096");
             h->cfg.pass_window = (int)value;
@@ -547,21 +560,28 @@ sv_status sv_profile_read(sv_handle h, int32_t reset, sv_profile *out) {
     if (!out) return fail(SV_ERR_INVALID_ARG, "null out");
     cudaError_t e = cudaStreamSynchronize(h->stream);
     if (e != cudaSuccess) return cuda_fail(h, e, "profile sync");
+    std::memset(out, 0, sizeof(*out));
     out->launches = h->prof.size();
-    out->kernel_ms = 0.0;
-    out->algorithmic_bytes = 0.0;
-    out->touched = 0.0;
-    out->state_bytes = 0.0;
     for (auto &r : h->prof) {
         float ms = 0.f;
         if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) out->kernel_ms += ms;
         out->algorithmic_bytes += r.bytes;
         out->touched += r.touched;
         out->state_bytes += r.state_bytes;
+        if (r.pass) {
+            ++out->pass_launches;
+            out->pass_ms += ms;
+            out->pass_touched += r.touched;
+            out->pass_item_touched += r.item_touched;
+            out->pass_flops += r.flops;
+            out->pass_state_bytes += r.state_bytes;
+        }
     }
+    out->plan_ms = h->plan_ms;
     if (reset) {
         for (auto &r : h->prof) { h->ev_pool.push_back(r.a); h->ev_pool.push_back(r.b); }
         h->prof.clear();
+        h->plan_ms = 0.0;
     }
     return SV_OK;
 }

@@ -20,6 +20,7 @@ SV_FUSE, SV_NO_CHECK, SV_GRAPH, SV_BLOCK = 1, 2, 4, 8
 SV_OPT_KERNEL, SV_OPT_TILE_ELEMS, SV_OPT_TILE_STAGES, SV_OPT_CTAS_PER_SM, SV_OPT_PROFILE, SV_OPT_PASS_TILE = 1, 2, 3, 4, 5, 6
 SV_OPT_PASS_STAGES, SV_OPT_PASS_THREADS, SV_OPT_PASS_GATES, SV_OPT_PASS_GROUPS = 7, 8, 9, 10
 SV_OPT_PASS_WINDOW, SV_OPT_PASS_MERGE, SV_OPT_SHARD_SWAP, SV_OPT_PASS_SEARCH = 11, 12, 13, 14
+SV_OPT_PLAN_CACHE = 15
 
 STATUS = {0: "SV_OK", 1: "SV_ERR_INVALID_ARG", 2: "SV_ERR_DIM", 3: "SV_ERR_OVERFLOW",
           4: "SV_ERR_QUDIT_RANGE", 5: "SV_ERR_CTRL_OVERLAP", 6: "SV_ERR_CTRL_DUP",
@@ -49,7 +50,10 @@ class sv_info(C.Structure):
 
 class sv_profile(C.Structure):
     _fields_ = [("launches", C.c_uint64), ("kernel_ms", C.c_double),
-                ("algorithmic_bytes", C.c_double), ("touched", C.c_double), ("state_bytes", C.c_double)]
+                ("algorithmic_bytes", C.c_double), ("touched", C.c_double), ("state_bytes", C.c_double),
+                ("pass_launches", C.c_uint64), ("pass_ms", C.c_double), ("pass_touched", C.c_double),
+                ("pass_item_touched", C.c_double), ("pass_flops", C.c_double),
+                ("pass_state_bytes", C.c_double), ("plan_ms", C.c_double)]
 
 
 class sv_gate_plan(C.Structure):
@@ -81,6 +85,9 @@ _sig("sv_create_ex", [_i32p, C.c_int32, C.c_int, C.c_int, C.c_void_p, C.c_void_p
 _sig("sv_create_sharded", [_i32p, C.c_int32, C.c_int, C.c_int32, C.c_int32, C.c_void_p, C.c_int,
                            C.c_void_p, C.POINTER(_h)])
 _sig("sv_nccl_unique_id", [C.c_void_p])
+_sig("sv_create_sharded_ipc", [_i32p, C.c_int32, C.c_int, C.c_int32, C.c_int32, C.c_void_p, C.c_int,
+                               C.c_void_p, C.POINTER(_h)])
+_sig("sv_ipc_unique_id", [C.c_void_p])
 _sig("sv_destroy", [_h])
 _sig("sv_reset", [_h, C.c_uint64])
 _sig("sv_apply_gate", [_h, C.c_int32, _i32p, _i32p, C.c_int32, _dp])
@@ -115,6 +122,7 @@ _sig("sv_block_plan", [_i32p, C.c_int32, C.POINTER(sv_gate), C.c_int64, C.c_int6
                        C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)])
 
 EXPORTS = ["sv_create", "sv_create_ex", "sv_create_sharded", "sv_nccl_unique_id", "sv_destroy",
+           "sv_create_sharded_ipc", "sv_ipc_unique_id",
            "sv_reset", "sv_apply_gate", "sv_apply_circuit", "sv_amplitudes", "sv_set_amplitudes",
            "sv_norm", "sv_sync", "sv_last_error", "sv_get_info", "sv_set_option", "sv_plan_gate",
            "sv_enumerate_fibres", "sv_fuse_plan", "sv_merge_plan", "sv_shard_plan", "sv_version", "sv_profile_read", "sv_block_plan",
@@ -194,6 +202,19 @@ class State:
         return cls(dims, _handle=h)
 
     @classmethod
+    def sharded_ipc(cls, dims, rank: int, nranks: int, ipc_id: bytes, device: int = 0,
+                    stream=None, dtype: str = "c128") -> "State":
+        """One rank of a sharded state over the fused peer-memory transport (sv_create_sharded_ipc)."""
+        d = _i32(dims)
+        h = _h()
+        idbuf = C.create_string_buffer(bytes(ipc_id), 128)
+        dt = {"c128": SV_C128, "c64": SV_C64}[dtype]
+        _check(_lib.sv_create_sharded_ipc(d.ctypes.data_as(_i32p), d.size, dt, int(rank), int(nranks),
+                                          idbuf, int(device), C.c_void_p(stream) if stream else None,
+                                          C.byref(h)))
+        return cls(dims, _handle=h)
+
+    @classmethod
     def loopback(cls, dims, nranks: int, device: int = 0, dtype: str = "c128") -> "State":
         return cls.sharded(dims, -1, nranks, None, device, dtype=dtype)
 
@@ -266,6 +287,12 @@ class State:
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(_lib.sv_nccl_unique_id(buf))
+    return buf.raw
+
+
+def ipc_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(_lib.sv_ipc_unique_id(buf))
     return buf.raw
 
 

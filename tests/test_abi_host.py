@@ -302,6 +302,21 @@ def test_bench_reference_arm_line():
     assert d["impl"] == "reference" and d["value"] > 0 and d["steps"] == 1
     assert d["config"]["dims_q0_first"] == [5, 5, 4, 4, 4, 4] + [3] * 6 + [2] * 10
     assert d["cpu_baseline"]["kind"] == "oracle" and d["e2e"]["h2d_bytes_per_step"] == 0
+    assert d["cpu_baseline"]["host"]["nproc"] >= 1
+
+
+def test_bench_reference_arm_does_not_load_the_product():
+    """The oracle arms count work with oracle/work.py: the reference-arm process maps the
+    oracle's library and never the product's libsv.so (VERDICT r1 weak #6)."""
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, runpy; sys.argv=['bench.py','--impl','reference','--steps','1','--warmup','1'];"
+            "runpy.run_path('bench.py', run_name='__main__');"
+            "maps=open('/proc/self/maps').read(); print('LIBSV' if 'libsv.so' in maps else 'NOLIBSV');"
+            "print('PKG' if 'paper_2410_17876_b200' in sys.modules else 'NOPKG')")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "NOLIBSV" in out.stdout and "NOPKG" in out.stdout, out.stdout[-500:]
 
 
 def test_block_planner_order_is_equivalent():
@@ -344,3 +359,24 @@ def test_bench_reference_arm_under_torchrun():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+
+
+def test_oracle_work_count_matches_planner_and_closed_forms():
+    """The metric's work count T has two independent implementations: the
+    product planner (sv_plan_gate, used by bench.py's GPU arm) and oracle/work.py (used by the
+    oracle arms, which must not load the product).  Pinned by closed forms, then equal on every
+    gate of every config circuit."""
+    from oracle import work as W
+    dims = [5, 4, 3, 2, 2]
+    D = int(np.prod(dims))
+    assert W.touched(dims, Gate(2, (), (), haar_unitary(3, np.random.default_rng(1)))) == D
+    assert W.touched(dims, Gate(1, (), (), shift_x(4, 1))) == D                   # X_d: every member
+    assert W.touched(dims, Gate(0, (), (), clock_z(5))) == D * 4 // 5             # Z_d: j = 0 fixed
+    assert W.touched(dims, Gate(4, (), (), t_gate())) == D // 2                    # T: |0> fixed
+    assert W.touched(dims, Gate(2, (3,), (1,), shift_x(3, 1))) == D // 2           # CINC: D / d_c
+    assert W.touched(dims, Gate(0, (1, 3), (3, 0), haar_unitary(5, np.random.default_rng(2)))) == D // 8
+    assert W.touched(dims, Gate(3, (), (), np.eye(2))) == 0
+    for cfg in (1, 2, 3, 4, 5):
+        cd, gates = config_circuit(cfg, ngates=None if cfg != 2 else 600)
+        for g in gates:
+            assert W.touched(cd, g) == int(P.plan_gate(cd, g.target, g.U, g.ctrl, g.vals).touched), (cfg, g)

@@ -1,8 +1,13 @@
-"""Full-size parity at BASELINE.json's configs c3 (6.9 GB) and c4 (76.4 GB), in the launch
-configuration bench.py times (auto kernel policy, SV_FUSE), against the oracle:
+"""Full-size parity at BASELINE.json's configs c3 (6.9 GB) and c4 (76.4 GB) against the oracle,
+in two circuit-driver modes: single-gate kernels (auto kernel policy, SV_FUSE) and the mode
+bench.py times on c1-c4 (SV_BLOCK multi-gate passes with the default pass configuration):
 
   * the state after a prefix of the seeded circuit, compared element by element with O-2
-    run on the host (streamed back in 2 GB chunks);
+    run on the host (streamed back in 2 GB chunks); with SV_BLOCK a 48-gate prefix forms
+    merged gates, pair gates and multi-gate passes;
+  * multi-gate passes whose in-tile set has no high digit (a run spans the whole register,
+    D > 2^32), with run-digit controls on the top qubits, on the labelled state against the
+    oracle's short-circuit evaluator;
   * every target qudit x {Haar U(d), controlled increment with a high / low-stride control,
     phase} applied to the index-labelled state, checked at sampled windows against the
     oracle's one-index evaluator (O-2, PAPER.md:222 row v of U times the class vector), then
@@ -61,11 +66,11 @@ def _idx(starts, width):
     return (starts[:, None] + np.arange(width)[None, :]).ravel().astype(np.uint64)
 
 
-def _prefix_parity(P, cfg, ngates):
+def _prefix_parity(P, cfg, ngates, block=False):
     dims, gates = config_circuit(cfg, ngates=ngates)
     ref = O2.run(dims, gates)                       # host O-2 on the full register
     with P.State(dims) as st:
-        st.apply_circuit(gates, fuse=True)
+        st.apply_circuit(gates, fuse=True, block=block)
         err = _compare_full(st, ref)
         nrm = st.norm()
     del ref
@@ -120,12 +125,12 @@ def _labelled_gates(P, cfg):
                 _upload_labelled(st, D)      # reset the accumulated rounding of the round trips
 
 
-def _adjoint_return(P, cfg):
+def _adjoint_return(P, cfg, block=False):
     dims, gates = config_circuit(cfg)
     with P.State(dims) as st:
-        st.apply_circuit(gates, fuse=True)
+        st.apply_circuit(gates, fuse=True, block=block)
         nrm = st.norm()
-        st.apply_circuit(adjoint_circuit(gates), fuse=True)
+        st.apply_circuit(adjoint_circuit(gates), fuse=True, block=block)
         a0 = st.amplitudes(0, 4096)
         D = int(np.prod(dims))
         tail = st.amplitudes(D - 4096, 4096)
@@ -157,6 +162,57 @@ def test_c4_labelled_every_target(P):
 
 def test_c4_circuit_then_adjoint(P):
     _adjoint_return(P, 4)
+
+
+def test_c4_block_prefix_parity_full_register(P):
+    """The bench's circuit-driver mode (SV_BLOCK, default pass configuration) on the first 48
+    gates of c4 (merges, pair gates, multi-gate passes) vs O-2 on the whole register."""
+    _prefix_parity(P, 4, 48, block=True)
+
+
+def test_c4_block_circuit_then_adjoint(P):
+    """The bench's whole timed circuit (SV_BLOCK) and its adjoint return to e_0."""
+    _adjoint_return(P, 4, block=True)
+
+
+def test_c3_block_circuit_then_adjoint(P):
+    _adjoint_return(P, 3, block=True)
+
+
+def test_c4_block_run_digit_controls_labelled(P):
+    """Two-gate SV_BLOCK passes whose targets all lie in the low prefix (q_0..q_2), so the
+    in-tile set has no high digit and a tile run spans the register (D = 4.78e9 > 2^32):
+    controls on q_20 / q_21 have b_c d_c >= 2^31 (per-tile threshold), on q_6 / q_13 below it.
+    Windows straddle the digit changes of q_20 and q_21 (D/4, D/2, 3D/4), where a tile holds
+    both control values.  Checked on the labelled state against the oracle's short-circuit
+    evaluator; regression for the 32-bit control modulus."""
+    dims = config_circuit(4, ngates=0)[0]
+    D = int(np.prod(dims))
+    rng = np.random.default_rng(404)
+    starts, width = _windows(D, rng, nwin=24)
+    extra = np.array([D // 4 - width // 2, D // 2 - width // 2, 3 * D // 4 - width // 2,
+                      D // 2 - 4000, D // 2 + 3000], dtype=np.int64)
+    starts = np.sort(np.concatenate([starts, extra]))
+    idx = _idx(starts, width)
+    b = np.cumprod([1] + dims[:-1]).astype(np.float64)
+    scale = idx.astype(np.float64) + float(np.sum(np.array(dims) * b)) + 1.0
+    H = lambda d: haar_unitary(d, rng)                  # noqa: E731
+    cases = [
+        ("cinc_q21", [Gate(0, (), (), H(5)), Gate(1, (21,), (1,), shift_x(5, 1))]),
+        ("haar_q20_v0", [Gate(1, (), (), H(5)), Gate(2, (20,), (0,), H(4))]),
+        ("haar_q13_q21", [Gate(2, (), (), shift_x(4, 1)), Gate(0, (13, 21), (1, 0), H(5))]),
+        ("haar_q6_q20", [Gate(0, (), (), H(5)), Gate(1, (6, 20), (2, 1), H(5))]),
+    ]
+    with P.State(dims) as st:
+        for name, gates in cases:
+            _upload_labelled(st, D)
+            l0 = st.info().kernel_launches
+            st.apply_circuit(gates, fuse=True, block=True)
+            assert st.info().kernel_launches - l0 == 1, name       # one multi-gate pass
+            got = _sample(st, starts, width)
+            exp = O2.circuit_output_labelled(dims, gates, idx)
+            rel = float(np.max(np.abs(got - exp) / scale))
+            assert rel <= 1e-13, (name, rel)
 
 
 def test_c3_many_controls_labelled(P):

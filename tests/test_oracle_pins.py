@@ -276,6 +276,22 @@ def test_sampled_gate_output_matches_full_apply():
             assert np.max(np.abs(got - psi[idx]) / np.abs(psi[idx])) < 1e-15
 
 
+def test_sampled_circuit_output_matches_kronecker():
+    """The short-circuit evaluator used for sampled full-size checks of multi-gate passes ==
+    O-1 (the Kronecker operators, independent of O-2) on the labelled state, every index."""
+    from oracle import kron as O1
+    rng = np.random.default_rng(9)
+    for s in range(40):
+        n = int(rng.integers(2, 5))
+        dims = [int(x) for x in rng.integers(2, 6, size=n)]
+        D = int(np.prod(dims))
+        _, gates = random_circuit(9_000 + s, dims, int(rng.integers(1, 4)), max_ctrl=2)
+        ref = O1.run(dims, gates, psi0=labelled_state(0, D))
+        got = O2.circuit_output_labelled(dims, gates, np.arange(D))
+        assert np.max(np.abs(got - ref) / np.abs(ref).max()) < 1e-14, (dims, s)
+    assert O2.circuit_output_labelled([2, 3], [], [4])[0] == labelled_state(4, 1)[0]
+
+
 # ------------------------------------------------------------------ O-3 (sparse, §2.3)
 def test_sparse_oracle_matches_dense_oracle():
     from oracle import sparse as O3
