@@ -235,12 +235,47 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def pairwise_peak(P, ipc_id, rank, world, dev, dtype, allreduce_max, lgl=27, reps=5):
+    """In-run NVLink reference for the multi-GPU roofline: the fused exchange kernel alone (H on
+    the top sharded qubit with qubit remapping off) on a probe state of 2^lgl amplitudes per
+    rank; GB/s per direction per rank = bytes that cross this rank's NVLink ports each way / the
+    kernel's event-timed duration, best of `reps`, the slowest rank.  On one GPU (ranks sharing
+    cuda:0) this measures HBM, not NVLink, and is labelled so."""
+    s = max(1, (world - 1).bit_length())
+    dims = [2] * (lgl + s)
+    st = P.State.sharded_ipc(dims, rank, world, ipc_id, device=dev, dtype=dtype)
+    try:
+        st.set_option(P.sv.SV_OPT_SHARD_SWAP, 0)
+        from sv_inputs import Gate, hadamard
+        gate = [Gate(len(dims) - 1, (), (), hadamard())]
+        st.apply_circuit(gate)
+        st.sync()
+        best = 0.0
+        for _ in range(reps):
+            st.set_option(P.sv.SV_OPT_PROFILE, 1)
+            st.profile_read(reset=True)
+            st.apply_circuit(gate)
+            pr = st.profile_read(reset=True)
+            st.set_option(P.sv.SV_OPT_PROFILE, 0)
+            if pr.comm_launches and pr.comm_ms > 0:
+                best = max(best, pr.comm_nvlink_bytes / (pr.comm_ms / 1e3) / 1e9)
+    finally:
+        st.close()
+    worst = -allreduce_max(-best)
+    return {"gbs_per_direction": worst, "kernel": "k_pair_update (fused exchange)",
+            "probe_amplitudes_per_rank": 2 ** lgl}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--config", type=int, default=None,
+                    help="BASELINE config (default: 4 for N <= 4 GPUs; 5, the 391 GB 8-GPU config, for N = 8)")
+    ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
+                    help="N > 1: fused peer-memory kernels over CUDA IPC (default) or NCCL send/recv + combine")
+    ap.add_argument("--nqubits", type=int, default=None, help="shrink the register (functional checks only)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 direct, 2 tiled")
     ap.add_argument("--no-fuse", action="store_true")
@@ -257,6 +292,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.config is None:
+        args.config = 5 if world >= 8 else 4
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -264,30 +301,61 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2410_17876_b200 as P
-    from sv_inputs import config_circuit, CONFIG_NAMES
+    from sv_inputs import config_circuit
 
-    torch.cuda.set_device(local_rank)
+    # one process per GPU; with fewer GPUs than ranks (a functional run of the multi-process
+    # path on one GPU: the IPC transport's kernels never wait on another rank) all ranks share
+    # cuda:0 and the bootstrap group runs over gloo
+    ngpu = torch.cuda.device_count()
+    dev = local_rank if ngpu >= world else 0
+    torch.cuda.set_device(dev)
+    backend = "nccl" if ngpu >= world else "gloo"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    dims, gates = config_circuit(args.config, ngates=args.ngates)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
+
+    def allreduce_max(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allreduce_sum(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    dims, gates = config_circuit(args.config, ngates=args.ngates, nqubits=args.nqubits)
     # circuit-driver mode per workload (measured, profiles/r01/passbench_*): multi-gate passes
-    # (SV_BLOCK) on c1-c4, plus a cached CUDA graph for the launch-bound c1/c2; sharded runs
-    # run the same passes on each slice between the pairwise exchanges of sharded targets.
+    # (SV_BLOCK) on c1-c5, plus a cached CUDA graph for the launch-bound c1/c2; sharded runs
+    # run the same passes on each slice between the cross-rank steps of gates on sharded qubits.
     fuse = not args.no_fuse
-    block = args.block or (args.config in (1, 2, 3, 4) and not args.no_block)
-    graph = args.graph or (args.config in (1, 2) and not args.no_graph)
+    block = args.block or (args.config in (1, 2, 3, 4, 5) and not args.no_block)
+    graph = args.graph or (args.config in (1, 2) and not args.no_graph and world == 1)
     T_step, F_step = circuit_work(dims, gates)               # global amplitude updates, flops / step
     D_total = int(np.prod(dims, dtype=object))
     nread = min(4096, D_total)
 
+    nvl_peak = None
     if world > 1:
-        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            idt.copy_(torch.frombuffer(bytearray(P.nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(idt, 0)
-        st = P.State.sharded(dims, rank, world, bytes(idt.cpu().numpy()), device=local_rank, dtype=args.dtype)
+        if args.transport == "ipc":
+            obj = [P.sv.ipc_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, 0)
+            nvl_peak = pairwise_peak(P, obj[0], rank, world, dev, args.dtype, allreduce_max)
+            obj = [P.sv.ipc_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, 0)
+            st = P.State.sharded_ipc(dims, rank, world, obj[0], device=dev, dtype=args.dtype)
+        else:
+            obj = [P.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, 0)
+            st = P.State.sharded(dims, rank, world, obj[0], device=dev, dtype=args.dtype)
     else:
-        st = P.State(dims, device=local_rank, dtype=args.dtype)
+        st = P.State(dims, device=dev, dtype=args.dtype)
     st.set_option(P.sv.SV_OPT_KERNEL, args.kernel)
     ga = P.sv._GateArray(gates)
     info = st.info()
@@ -314,7 +382,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(local_rank) as clk:
+    with Clocks(dev) as clk:
         e0.record(ext)
         for _ in range(args.steps):
             step()
@@ -327,10 +395,8 @@ def main():
     prof = st.profile_read(reset=True)
     st.set_option(P.sv.SV_OPT_PROFILE, 0)
     launches = st.info().kernel_launches - launches0
-    if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms_rank = ms
+    ms = allreduce_max(ms)
     value = T_step * args.steps / (ms / 1e3)
 
     # ---- e2e: the public API end to end with host buffers (gate matrices in, norm + the
@@ -355,10 +421,7 @@ def main():
         dt = time.perf_counter() - t0
         plan_ms = st.profile_read(reset=True).plan_ms / args.steps
         st.set_option(P.sv.SV_OPT_PLAN_CACHE, 1)
-        if world > 1:
-            t = torch.tensor([dt], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t.item())
+        dt = allreduce_max(dt)
         return T_step * args.steps / dt, nrm, plan_ms
 
     v_warm, nrm, plan_warm = e2e_run(True)
@@ -424,6 +487,28 @@ def main():
                     "share_of_step": prof.kernel_ms / ms if ms else None,
                     "peak_source": hbm_src, "traffic_source": traffic_note}
         pass_roofline = None
+    multi = None
+    if world > 1:
+        # SURVEY.md 8(d) multi-GPU roofline: per rank, the HBM time of its passes and single-gate
+        # launches plus, for the cross-rank kernels, the slower of their HBM and NVLink times;
+        # the slowest rank's floor over the slowest rank's measured time
+        bw_nvl = (nvl_peak or {}).get("gbs_per_direction") or 770.0
+        gate_bytes = max(0.0, prof.algorithmic_bytes - bpu * prof.pass_touched - prof.comm_hbm_bytes)
+        floor_s = ((prof.pass_state_bytes + gate_bytes) / (hbm * 1e9) +
+                   max(prof.comm_hbm_bytes / (hbm * 1e9), prof.comm_nvlink_bytes / (bw_nvl * 1e9)))
+        floor_max = allreduce_max(floor_s)
+        nvl_step = prof.comm_nvlink_bytes / args.steps
+        multi = {"transport": args.transport if world > 1 else None,
+                 "nvlink_bytes_per_step_per_rank": nvl_step,
+                 "nvlink_bytes_per_step_max_rank": allreduce_max(nvl_step),
+                 "cross_rank_kernels_per_step": prof.comm_launches / args.steps,
+                 "cross_rank_ms_per_step": prof.comm_ms / args.steps,
+                 "pairwise_peak": nvl_peak,
+                 "bw_nvlink_gbs_used": bw_nvl,
+                 "bw_nvlink_source": "in-run pairwise probe" if nvl_peak else "B200_PROFILING.md peer copy 770 GB/s",
+                 "ranks_share_one_gpu": ngpu < world,
+                 "roofline_floor_ms_per_step": 1e3 * floor_max / args.steps,
+                 "roofline_frac": floor_max / (ms / 1e3)}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -440,6 +525,7 @@ def main():
                               "above 1 when a pass applies several gates per HBM round trip",
             "roofline": roofline,
             "pass_roofline": pass_roofline,
+            "multi_gpu": multi,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),

@@ -254,6 +254,12 @@ typedef struct {
     double pass_state_bytes;   /* 2 x elem x the local state per pass                           */
     double plan_ms;            /* host planning time (SV_BLOCK merge + pass planning) since the
                                   last reset                                                    */
+    /* sharded handles: the cross-rank kernels (fused exchanges, qubit swaps): */
+    uint64_t comm_launches;
+    double comm_ms;
+    double comm_hbm_bytes;     /* bytes they move through this rank's HBM                       */
+    double comm_nvlink_bytes;  /* bytes per direction over this rank's NVLink ports (IPC
+                                  transport; 0 for loopback slices on one device)               */
 } sv_profile;
 SV_API sv_status sv_profile_read(sv_handle h, int32_t reset, sv_profile *out);
 

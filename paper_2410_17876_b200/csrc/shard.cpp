@@ -421,10 +421,15 @@ sv_status swap_qubits(sv_handle h, int k, int j) {
         const int r = c->rank, l = c->lrank[r], beta = (l >> j) & 1;
         const int p = c->prank[l ^ (1 << j)];
         const uint64_t half = L / 2, q0 = half / 2;  // swap space [0, L/2): lo rank [0, q0), hi rank the rest
+        const uint64_t n = beta ? half - q0 : q0;
+        void *tok;
+        prof_begin(h, &tok);
         cudaError_t e = launch_pair_swap(at(c->peer[r], (uint64_t)(1 - beta) * b, h->elem),
                                          at(c->peer[p], (uint64_t)beta * b, h->elem), b, beta ? q0 : 0,
-                                         beta ? half - q0 : q0, h->stream, h->cfg.num_sms, &h->launches, h->c64);
+                                         n, h->stream, h->cfg.num_sms, &h->launches, h->c64);
         if (e != cudaSuccess) return cuda_fail_h(h, e, "peer qubit swap");
+        // this rank's half slice in and out of HBM; n elements cross each way twice (own + partner's)
+        prof_end(h, tok, (double)h->elem * (double)L, 2.0 * (double)h->elem * (double)n, 0.0);
         ++h->exchanges;
         s = ipc_fence(h);
         if (s != SV_OK) return s;
@@ -436,10 +441,13 @@ sv_status swap_qubits(sv_handle h, int k, int j) {
         const auto mine = pieces(1 - beta);          // what this rank gives away
         if (c->loopback()) {
             if (p < r) continue;                      // each pair once: one kernel over both slices
+            void *tok;
+            prof_begin(h, &tok);
             cudaError_t e = launch_pair_swap(at(c->slices[r], (uint64_t)(1 - beta) * b, h->elem),
                                              at(c->slices[p], (uint64_t)beta * b, h->elem), b, 0, L / 2, h->stream,
                                              h->cfg.num_sms, &h->launches, h->c64);
             if (e != cudaSuccess) return cuda_fail_h(h, e, "loopback qubit swap");
+            prof_end(h, tok, 2.0 * (double)h->elem * (double)L, 0.0, 0.0);
             ++h->exchanges;
             continue;
         }
@@ -539,8 +547,15 @@ sv_status exchange_nccl(sv_handle h, const GateSpec &g, const ShardAction &a) {
 sv_status exchange_fused(sv_handle h, const GateSpec &g, double2 *lo, double2 *hi, uint64_t first, uint64_t n) {
     const double2 u[4] = {g.U[0], g.U[1], g.U[2], g.U[3]};
     const CombineCtrl cc = local_ctrl(h->local, g.ctrl);
+    void *tok;
+    prof_begin(h, &tok);
     cudaError_t e = launch_pair_update(lo, hi, first, n, u, cc, h->stream, h->cfg.num_sms, &h->launches, h->c64);
     if (e != cudaSuccess) return cuda_fail_h(h, e, "fused exchange");
+    // IPC: this rank's slice is read and written once (half by each rank of the pair); n index
+    // pairs cross NVLink both ways.  Loopback: both slices on this device, nothing crosses.
+    const double el = (double)h->elem, L = (double)h->local.D;
+    if (h->shard->transport == kIpc) prof_end(h, tok, 2.0 * el * L, 2.0 * el * (double)n, 2.0 * (double)n);
+    else prof_end(h, tok, 4.0 * el * (double)n, 0.0, 2.0 * (double)n);
     ++h->exchanges;
     return SV_OK;
 }

@@ -20,6 +20,8 @@ sv_status local_norm2(sv_handle h, double *out);
 sv_status local_apply(sv_handle h, const GatePlan &p);
 sv_status launch_on(sv_handle h, const GatePlan &p, double2 *buf);
 sv_status run_local_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_t flags, double2 *buf);
+void prof_begin(sv_handle h, void **tok);
+void prof_end(sv_handle h, void *tok, double hbm_bytes, double nvlink_bytes, double touched);
 
 // implemented in shard.cpp
 void shard_destroy(ShardCtx *c);

@@ -28,11 +28,13 @@ struct sv_state_s {
     ShardCtx *shard = nullptr;     // non-null for sharded handles
     // SV_OPT_PROFILE: events bracketing each gate launch
     bool profile = false;
+    enum ProfKind { kProfGate = 0, kProfPass = 1, kProfComm = 2 };
     struct ProfRec {
         cudaEvent_t a, b;
         double bytes, touched, state_bytes;
-        bool pass;                       // a multi-gate pass (k_gate_pass)
+        int kind;                        // ProfKind: single-gate kernel, multi-gate pass, cross-rank kernel
         double item_touched, flops;      // passes: executed shared-memory round trips, FP64 flops
+        double nvl_bytes;                // cross-rank kernels: bytes per direction over NVLink
     };
     std::vector<ProfRec> prof;
     double plan_ms = 0.0;              // host planning time (SV_BLOCK merge + passes), accumulated

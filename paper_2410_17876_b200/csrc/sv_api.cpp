@@ -159,13 +159,29 @@ sv_status launch_on(sv_handle h, const GatePlan &p, double2 *buf) {
     if (h->profile) {
         cudaEventRecord(b, h->stream);
         const double bpu = 2.0 * (double)h->elem;     // one read + one write per touched amplitude
-        h->prof.push_back({a, b, bpu * (double)p.touched, (double)p.touched, bpu * (double)p.touched, false,
-                           (double)p.touched, 0.0});
+        h->prof.push_back({a, b, bpu * (double)p.touched, (double)p.touched, bpu * (double)p.touched,
+                           sv_state_s::kProfGate, (double)p.touched, 0.0, 0.0});
     }
     return SV_OK;
 }
 
 sv_status local_apply(sv_handle h, const GatePlan &p) { return launch_on(h, p, h->psi); }
+
+// SV_OPT_PROFILE brackets for the cross-rank kernels (shard.cpp): hbm = bytes this rank's HBM
+// moves, nvl = bytes per direction over this rank's NVLink ports.
+void prof_begin(sv_handle h, void **tok) {
+    *tok = nullptr;
+    if (!h->profile) return;
+    cudaEvent_t a = pool_event(h);
+    cudaEventRecord(a, h->stream);
+    *tok = a;
+}
+void prof_end(sv_handle h, void *tok, double hbm, double nvl, double touched) {
+    if (!h->profile || !tok) return;
+    cudaEvent_t b = pool_event(h);
+    cudaEventRecord(b, h->stream);
+    h->prof.push_back({(cudaEvent_t)tok, b, hbm, touched, hbm, sv_state_s::kProfComm, 0.0, 0.0, nvl});
+}
 
 // One multi-gate pass (mgpass.cu); falls back to its gates one by one if the pass kernel
 // cannot take it.
@@ -188,8 +204,8 @@ static sv_status launch_pass_on(sv_handle h, const std::vector<GateSpec> &specs,
             // algorithmic bytes per SURVEY.md §8(d): 32 B per touched amplitude of every gate the
             // pass applies; the pass itself moves the local state once (16 B read + 16 B write)
             const double bpu = 2.0 * (double)h->elem;     // one read + one write per amplitude
-            h->prof.push_back({a, b, bpu * w.touched, w.touched, bpu * (double)h->local.D, true, w.item_touched,
-                               w.flops});
+            h->prof.push_back({a, b, bpu * w.touched, w.touched, bpu * (double)h->local.D, sv_state_s::kProfPass,
+                               w.item_touched, w.flops, 0.0});
         }
         return SV_OK;
     }
@@ -568,7 +584,13 @@ sv_status sv_profile_read(sv_handle h, int32_t reset, sv_profile *out) {
         out->algorithmic_bytes += r.bytes;
         out->touched += r.touched;
         out->state_bytes += r.state_bytes;
-        if (r.pass) {
+        if (r.kind == sv_state_s::kProfComm) {
+            ++out->comm_launches;
+            out->comm_ms += ms;
+            out->comm_hbm_bytes += r.bytes;
+            out->comm_nvlink_bytes += r.nvl_bytes;
+        }
+        if (r.kind == sv_state_s::kProfPass) {
             ++out->pass_launches;
             out->pass_ms += ms;
             out->pass_touched += r.touched;

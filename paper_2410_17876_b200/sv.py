@@ -53,7 +53,9 @@ class sv_profile(C.Structure):
                 ("algorithmic_bytes", C.c_double), ("touched", C.c_double), ("state_bytes", C.c_double),
                 ("pass_launches", C.c_uint64), ("pass_ms", C.c_double), ("pass_touched", C.c_double),
                 ("pass_item_touched", C.c_double), ("pass_flops", C.c_double),
-                ("pass_state_bytes", C.c_double), ("plan_ms", C.c_double)]
+                ("pass_state_bytes", C.c_double), ("plan_ms", C.c_double),
+                ("comm_launches", C.c_uint64), ("comm_ms", C.c_double), ("comm_hbm_bytes", C.c_double),
+                ("comm_nvlink_bytes", C.c_double)]
 
 
 class sv_gate_plan(C.Structure):

@@ -22,7 +22,8 @@ def main():
     import paper_2410_17876_b200 as P
     dims, gates = job["dims"], job["gates"]
     res = {}
-    st = P.State.sharded_ipc(dims, rank, job["nranks"], job["ipc_id"], device=0, dtype=job.get("dtype", "c128"))
+    dev = rank if job.get("device_per_rank") else 0
+    st = P.State.sharded_ipc(dims, rank, job["nranks"], job["ipc_id"], device=dev, dtype=job.get("dtype", "c128"))
     try:
         st.set_option(P.sv.SV_OPT_SHARD_SWAP, job.get("swap", 1))
         if job.get("psi0") is not None:
@@ -34,7 +35,14 @@ def main():
         else:
             st.apply_circuit(gates, fuse=mode == "fuse", block=mode == "block")
         res["norm"] = st.norm()                    # collective: partials in rank order
-        res["psi"] = st.amplitudes()               # collective: reads every slice
+        if job.get("adjoint"):                     # full-size: circuit + adjoint back to e_0
+            st.apply_circuit(job["adjoint"], fuse=mode == "fuse", block=mode == "block")
+            D = st.info().D
+            res["norm2"] = st.norm()
+            res["head"] = st.amplitudes(0, 4096)
+            res["tail"] = st.amplitudes(D - 4096, 4096)
+        else:
+            res["psi"] = st.amplitudes()           # collective: reads every slice
         res["exchanges"] = int(st.info().exchanges)
         if job.get("extra"):
             st.apply_circuit(job["extra"], block=True)

@@ -203,9 +203,10 @@ def test_c4_block_run_digit_controls_labelled(P):
         ("haar_q13_q21", [Gate(2, (), (), shift_x(4, 1)), Gate(0, (13, 21), (1, 0), H(5))]),
         ("haar_q6_q20", [Gate(0, (), (), H(5)), Gate(1, (6, 20), (2, 1), H(5))]),
     ]
+    exp_lab = np.concatenate([labelled_state(int(s0), width) for s0 in starts])
     with P.State(dims) as st:
+        _upload_labelled(st, D)                     # once: each case is undone by its adjoint
         for name, gates in cases:
-            _upload_labelled(st, D)
             l0 = st.info().kernel_launches
             st.apply_circuit(gates, fuse=True, block=True)
             assert st.info().kernel_launches - l0 == 1, name       # one multi-gate pass
@@ -213,6 +214,9 @@ def test_c4_block_run_digit_controls_labelled(P):
             exp = O2.circuit_output_labelled(dims, gates, idx)
             rel = float(np.max(np.abs(got - exp) / scale))
             assert rel <= 1e-13, (name, rel)
+            st.apply_circuit(adjoint_circuit(gates), fuse=True, block=True)
+            back = _sample(st, starts, width)
+            assert float(np.max(np.abs(back - exp_lab) / scale)) <= 1e-13, name
 
 
 def test_c3_many_controls_labelled(P):

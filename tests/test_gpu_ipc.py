@@ -21,7 +21,7 @@ pytestmark = pytest.mark.gpu
 
 from oracle import blocksim as O2  # noqa: E402
 from sv_inputs import (Gate, hadamard, haar_unitary, shift_x, fourier, t_gate, random_circuit,  # noqa: E402
-                       random_state, labelled_state)
+                       random_state, labelled_state, config_circuit, adjoint_circuit)
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 WORKER = os.path.join(ROOT, "tests", "_ipc_worker.py")
@@ -132,3 +132,34 @@ def test_ipc_rank_failure_is_reported_not_hung(P):
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120,
                          env=dict(os.environ, SV_COMM_TIMEOUT_S="3"))
     assert "ERR SV_ERR_NCCL" in out.stdout, (out.stdout, out.stderr[-2000:])
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_ipc_c5_recipe_reduced_register(P, nranks):
+    """BASELINE config 5's recipe (6 qutrits + qubits, 200 gates, 20 % on the 3 top qubits,
+    CNOTs controlled on sharded qubits) on a register reduced to 14 qubits (D = 1.2e7), sharded
+    over P processes: vs O-2 on the whole register (SURVEY.md §8(c) fallback for c5)."""
+    dims, gates = config_circuit(5, nqubits=14)
+    ref = O2.run(dims, gates)
+    for swap in (1, 0):
+        res = _run(P, {"dims": dims, "gates": gates, "psi0": None, "swap": swap, "mode": "block"}, nranks,
+                   timeout=600)
+        assert np.max(np.abs(res["psi"] - ref)) <= 1e-10, swap
+        assert abs(res["norm"] - 1.0) <= 1e-10
+
+
+def test_ipc_c5_full_size_adjoint_return(P):
+    """The full 391 GB config 5 on 8 GPUs (48.9 GB per rank; 4 GPUs: 97.8 GB): the circuit and its
+    adjoint return to e_0 within 1e-10 (SURVEY.md §8(c) fallback when the host cannot hold O-2's
+    copy).  Needs >= 4 GPUs (skipped on the one-GPU box)."""
+    import torch
+    ng = torch.cuda.device_count()
+    if ng < 4:
+        pytest.skip("needs 4 or 8 GPUs")
+    nranks = 8 if ng >= 8 else 4
+    dims, gates = config_circuit(5)
+    res = _run(P, {"dims": dims, "gates": gates, "psi0": None, "swap": 1, "mode": "block",
+                   "adjoint": adjoint_circuit(gates), "device_per_rank": True}, nranks, timeout=3000)
+    assert abs(res["norm"] - 1.0) <= 1e-10 and abs(res["norm2"] - 1.0) <= 1e-10
+    assert abs(res["head"][0] - 1.0) <= 1e-10
+    assert np.max(np.abs(res["head"][1:])) <= 1e-10 and np.max(np.abs(res["tail"])) <= 1e-10

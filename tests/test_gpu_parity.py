@@ -455,6 +455,23 @@ def test_loopback_sharded_matches_single_state(P, nranks):
         del os.environ["SV_EXCHANGE_CHUNK"]
 
 
+@pytest.mark.parametrize("nranks", [2, 4, 8])
+def test_loopback_c5_recipe_reduced_register(P, nranks):
+    """BASELINE config 5's recipe on a register reduced to 13 qubits, sharded P ways on one device
+    (loopback: the fused exchange / swap kernels over slice pairs), both remap settings, vs O-2."""
+    dims, gates = config_circuit(5, nqubits=13)
+    ref = O2.run(dims, gates)
+    for swap in (1, 0):
+        with P.State.loopback(dims, nranks) as st:
+            st.set_option(P.sv.SV_OPT_SHARD_SWAP, swap)
+            st.apply_circuit(gates, fuse=True, block=True)
+            got = st.amplitudes()
+            nrm = st.norm()
+            assert st.info().exchanges > 0
+        assert np.max(np.abs(got - ref)) <= 1e-10, swap
+        assert abs(nrm - 1.0) <= 1e-10
+
+
 # (compute threads, consumer groups, stages) of the pass kernel
 PASS_CFGS = [(256, 1, 2), (384, 1, 2), (512, 1, 2), (384, 2, 2), (256, 2, 3), (384, 2, 3), (512, 2, 3), (512, 4, 4)]
 
