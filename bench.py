@@ -139,15 +139,16 @@ def host_info():
     return info
 
 
-def workload_config(cfg: int, dtype: str = "c128"):
+def workload_config(cfg: int, dtype: str = "c128", nqubits=None):
     """The workload both arms are quoted on (identical dicts; implementation options go under
-    the line's "mode")."""
+    the line's "mode").  nqubits: a reduced register (functional runs), named as such."""
     from sv_inputs import config_circuit, CONFIG_NAMES
-    dims = config_circuit(cfg, ngates=0)[0]
+    dims = config_circuit(cfg, ngates=0, nqubits=nqubits)[0]
     D = int(np.prod(dims, dtype=object))
     ngates = len(config_circuit(cfg)[1])
     elem = 16 if dtype == "c128" else 8
-    return {"workload": CONFIG_NAMES[cfg], "dims_q0_first": dims,
+    return {"workload": CONFIG_NAMES[cfg] + ("" if nqubits is None else f"_reduced_{nqubits}qubits"),
+            "dims_q0_first": dims,
             "state_dtype": "complex128" if dtype == "c128" else "complex64", "D": D, "gates": ngates,
             "initial_state": "e_0", "l2": "state (%.1f GB) >> L2 (126 MB): no flush needed" % (elem * D / 1e9)}
 
@@ -516,7 +517,7 @@ def main():
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
             "dtype": "f64" if args.dtype == "c128" else "f32",
             "data": "synthetic",
-            "config": workload_config(args.config, args.dtype),
+            "config": workload_config(args.config, args.dtype, args.nqubits),
             "mode": {"fuse": fuse, "block_passes": block, "cuda_graph": graph, "kernel": args.kernel,
                      "sharded_ranks": world, "gates_timed": len(gates)},
             "hbm_gbs": bpu * value / 1e9,

@@ -227,6 +227,11 @@ SV_API sv_status sv_get_info(sv_handle h, sv_info *out);
 #define SV_OPT_PASS_SEARCH 14   /* 1 (default): each SV_BLOCK pass's in-tile qudit set is the one that
                                    admits the most window gates (subset search); 0: first come, first
                                    admitted */
+#define SV_OPT_PASS_KERNEL 16   /* SV_BLOCK pass kernel: 0 (default) = register-blocked stages
+                                   (k_gate_stage: consecutive gates on a pair of in-tile digits applied
+                                   to register blocks, one shared-memory round trip per stage) when the
+                                   pass fits them (targets d <= 5), else the per-gate kernel; 1 = per-gate
+                                   kernel (k_gate_pass) only; 2 = stages only                       */
 #define SV_OPT_PLAN_CACHE  15   /* 1 (default): the SV_BLOCK host plan (merged gates + passes) is
                                    memoised per handle and reused while the same gates and options
                                    come again; 0: plan every call (cold-submission timing)          */
@@ -316,6 +321,13 @@ SV_API sv_status sv_merge_plan(const int32_t *dims, int32_t n, const sv_gate *ga
 SV_API sv_status sv_block_plan(const int32_t *dims, int32_t n, const sv_gate *gates, int64_t ngates,
                                int64_t tile_cap, int64_t *out_order, int64_t *out_pass,
                                int64_t *out_tile, int64_t *out_npasses);
+/* As sv_block_plan with the planner's knobs: at most max_gates (1..32) gates per pass, `window`
+ * gates scanned ahead, search != 0 = the in-tile set search (the SV_BLOCK defaults are 32, 256, 1;
+ * sv_block_plan uses 24, 64, 0). */
+SV_API sv_status sv_block_plan_ex(const int32_t *dims, int32_t n, const sv_gate *gates, int64_t ngates,
+                                  int64_t tile_cap, int32_t max_gates, int32_t window, int32_t search,
+                                  int64_t *out_order, int64_t *out_pass, int64_t *out_tile,
+                                  int64_t *out_npasses);
 
 /* Host-only (sharded planning): what rank `rank` of `nranks` does for a
  * gate.  *action: 0 = local apply, 1 = skip (a sharded control is unmet on this rank),

@@ -21,6 +21,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "sv_internal.h"
@@ -34,6 +36,7 @@ constexpr int kPoolC = 768;
 constexpr int kMaxPassCtrl = 4;
 constexpr int kMaxIns = 2 + kMaxPassCtrl;   // inserted in-tile digits: the target(s) + pinned controls
 constexpr int kMaxPairDim = 4;             // pair gates: d_a d_b <= 4 (qubit pairs)
+constexpr int kGDesc = 12;                 // words of a gate's shared-memory descriptor
 
 // in-pass gate kinds: general y = U x (§2.3), monomial y_{sigma(j)} = c_j x_j (§2.1-2.2),
 // and the pure permutation (every moving coefficient exactly 1: no arithmetic at all)
@@ -95,6 +98,58 @@ struct PassParams {
 
 static_assert(sizeof(PassParams) <= 32764, "kernel parameter space (32 KB on sm_100)");
 
+// ---- register-blocked stages (k_gate_stage).  The pass's gates are grouped, in pass order, into
+// stages: maximal runs of consecutive gates whose targets lie in one pair of in-tile digits {a, b}
+// with d_a d_b <= kStageAmps (a single target is paired with a passive digit).  A thread loads a
+// whole d_a x d_b block of the tile into registers (every digit but a and b fixed), applies all
+// the stage's gates there — each gate's classes are the block's rows or columns
+// — and stores the block once: one shared-memory round trip and one group barrier per stage
+// instead of per gate.
+constexpr int kStageAmps = 12;
+constexpr int kPoolS = 800;                 // 32 gates of d <= 5
+enum StageKind : int32_t { kSGeneral = 0, kSDiag = 1, kSShift = 2 };
+
+struct StageGate {
+    int32_t nctrl;                          // controls decided per tile (producer): cls 2 out of
+    PassCtrl c[kMaxPassCtrl];               //   the tile, cls 1 / 3 run digits
+    int32_t axis;                           // target: 0 = the stage's digit a, 1 = digit b
+    int32_t kind;                           // StageKind
+    int32_t shift;                          // kSShift: y_{(j + shift) mod d} = x_j
+    int32_t uoff;                           // kSGeneral: row-major d x d; kSDiag: d entries
+    int32_t octrl;                          // control on the stage's other digit: value, or -1
+    int32_t nic;                            // controls on in-tile digits outside the stage:
+    uint32_t ic_s[kMaxPassCtrl], ic_m[kMaxPassCtrl], ic_d[kMaxPassCtrl], ic_dm[kMaxPassCtrl],
+             ic_v[kMaxPassCtrl];            //   digit (e / s) mod d == v (s, d + magics)
+    uint32_t runck;                         // 1: c[] holds a run-digit control
+};
+
+struct StageRec {
+    int32_t da, db;                         // dims of digit a (lower tile stride) and b
+    int32_t g0, ng;                         // its gates
+    uint32_t sa, sb;                        // tile strides
+    uint32_t nblk;                          // blocks per full tile = M LT / (da db)
+    uint32_t s0, m0, sd0;                   // block id -> tile offset: insert digit a (stride, magic,
+    uint32_t s1, m1, sd1;                   //   stride*dim), then digit b
+};
+
+struct StageParams {
+    double2 *psi;
+    int32_t nrem;
+    RemovedRun rem[kMaxRem];
+    uint64_t ntiles, R, tpr, tpr_m;
+    uint32_t LT, mLT;
+    uint32_t L, mL;
+    int32_t M;
+    int32_t ngates;
+    int32_t nstages;
+    int32_t upool;
+    uint64_t moff[kMaxMembers];
+    StageRec st[kMaxPassGates];
+    StageGate g[kMaxPassGates];
+    double2 U[kPoolS];
+};
+static_assert(sizeof(StageParams) <= 32764, "kernel parameter space (32 KB on sm_100)");
+
 namespace {
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -130,7 +185,8 @@ struct TileInfo {
     uint32_t len;     // valid run elements per member
 };
 
-__device__ __forceinline__ TileInfo tile_info(const PassParams &p, uint64_t t) {
+template <typename PP>
+__device__ __forceinline__ TileInfo tile_info(const PP &p, uint64_t t) {
     TileInfo ti;
     uint64_t sub;
     const uint64_t run = fastdiv64(t, p.tpr, p.tpr_m, sub);
@@ -150,14 +206,16 @@ struct StageInfo {
     uint32_t lowoff[kMaxPassGates][kMaxPassCtrl];    // (s0 mod b_c d_c) for run-digit controls
 };
 
-template <typename V>
-__device__ __forceinline__ void issue_loads(const PassParams &p, uint64_t t, V *buf, uint64_t *bar,
+// PP: PassParams or StageParams (same geometry fields; g[i].nctrl / g[i].c[] = the controls
+// decided per tile)
+template <typename V, typename PP>
+__device__ __forceinline__ void issue_loads(const PP &p, uint64_t t, V *buf, uint64_t *bar,
                                             StageInfo *si, int lane) {
     const TileInfo ti = tile_info(p, t);
     // lane g decides gate g for this tile
     bool fire = true;
     if (lane < p.ngates) {
-        const PassGateP &g = p.g[lane];
+        const auto &g = p.g[lane];
         for (int k = 0; k < g.nctrl; ++k) {
             const PassCtrl &cc = g.c[k];
             if (cc.cls == 2) {
@@ -230,6 +288,8 @@ __device__ __forceinline__ uint32_t class_e0(uint32_t c, const PassGateP &g, con
 // What one gate needs to decide its classes inside the current tile.
 struct TileGate {
     uint32_t LT, mLT, len, flags;
+    uint32_t nins, active;      // hot gate fields, read from the shared-memory descriptor
+    Ins1 first;                 // the first digit insertion of the class index
     const uint32_t *lowoff;     // shared memory: run offsets of the run-digit controls
     const uint32_t *moff;       // shared memory: tile offset of class member j (j st, or the
                                 //   two-digit offset of a pair gate)
@@ -309,30 +369,44 @@ __device__ __forceinline__ void sts2(uint32_t a, float2 v) {
 
 // One general gate (y = U x per class) on one tile, K classes per thread
 // iteration.  All K*D gathers are issued before the matvecs; buf and U are restrict-qualified
-// so the matrix reads may be scheduled across the stores of earlier rows.
-template <int D, int K, int NT, typename V>
+// so the matrix reads may be scheduled across the stores of earlier rows.  Branch-free: a class
+// that does not exist or fire (CHECK) computes on harmless inputs and stores to the lane's trash
+// slot, so the K classes' FMA chains stay in one basic block and interleave (with a branch per
+// store, ptxas ran the classes' dependent DFMA chains one after another).
+template <int D, int K, int NT, bool CHECK, typename V>
 __device__ __forceinline__ void gate_tile_general(const TileGate &tg, const PassGateP &g, V *__restrict__ buf,
                                                   const V *__restrict__ U, uint32_t cbeg, uint32_t cend,
-                                                  uint32_t ncls, bool needck, int tid) {
+                                                  uint32_t ncls, bool needck, int tid, uint32_t trash) {
     // member offsets, read once from shared memory (the stores below may alias that table as
     // far as the compiler knows, so it keeps them in registers)
     uint32_t mo[D];
 #pragma unroll
     for (int j = 0; j < D; ++j) mo[j] = tg.moff[j] * (uint32_t)sizeof(V);
     const uint32_t sb = smem_u32(buf);
-    const Ins1 first = ins_at(g, 0);
-    const bool more = g.nins > 1;
+    const Ins1 first = tg.first;
+    const bool more = tg.nins > 1;
 #pragma unroll 1
     for (uint32_t c0 = cbeg + (uint32_t)tid; c0 < cend; c0 += (uint32_t)(NT * K)) {
         uint32_t e[K];
         bool ok[K];
-        class_batch<K, NT>(tg, g, first, more, c0, ncls, needck, e, ok);
+        if (CHECK) {
+            class_batch<K, NT>(tg, g, first, more, c0, ncls, needck, e, ok);
+        } else {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                e[k] = class_e0(c0 + (uint32_t)(k * NT), g, first, more);
+                ok[k] = true;
+            }
+        }
         const V *__restrict__ Ui = U + opaque_zero(c0);
+        uint32_t a[K];
         V x[K][D];
 #pragma unroll
-        for (int k = 0; k < K; ++k)
+        for (int k = 0; k < K; ++k) {
+            a[k] = sb + e[k] * (uint32_t)sizeof(V);
 #pragma unroll
-            for (int j = 0; j < D; ++j) x[k][j] = lds2<V>(sb + e[k] * (uint32_t)sizeof(V) + mo[j]);
+            for (int j = 0; j < D; ++j) x[k][j] = lds2<V>(a[k] + mo[j]);
+        }
 #pragma unroll
         for (int i = 0; i < D; ++i) {
             V acc[K];
@@ -345,8 +419,7 @@ __device__ __forceinline__ void gate_tile_general(const TileGate &tg, const Pass
                 for (int k = 0; k < K; ++k) cfma(acc[k], u, x[k][j]);
             }
 #pragma unroll
-            for (int k = 0; k < K; ++k)
-                if (ok[k]) sts2(sb + e[k] * (uint32_t)sizeof(V) + mo[i], acc[k]);
+            for (int k = 0; k < K; ++k) sts2(CHECK ? (ok[k] ? a[k] + mo[i] : trash) : a[k] + mo[i], acc[k]);
         }
     }
 }
@@ -354,14 +427,14 @@ __device__ __forceinline__ void gate_tile_general(const TileGate &tg, const Pass
 // One monomial gate (phase / permutation, y_{sigma(j)} = c_j x_j) on one
 // tile; PERM: every moving coefficient is exactly 1, so the gate only moves data.  Only the
 // members that move or scale are read and written (select-form predicated gathers: a branch
-// per member makes ptxas spill the array).
-template <int D, int K, int NT, bool PERM, typename V>
+// per member makes ptxas spill the array); skipped classes store to the trash slot.
+template <int D, int K, int NT, bool PERM, bool CHECK, typename V>
 __device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const PassGateP &g, V *__restrict__ buf,
                                                    const V *__restrict__ U, uint32_t cbeg, uint32_t cend,
-                                                   uint32_t ncls, bool needck, int tid) {
-    const uint32_t act = g.active;
-    const Ins1 first = ins_at(g, 0);
-    const bool more = g.nins > 1;
+                                                   uint32_t ncls, bool needck, int tid, uint32_t trash) {
+    const uint32_t act = tg.active;
+    const Ins1 first = tg.first;
+    const bool more = tg.nins > 1;
     // destination offsets sigma(j) * st, read once from shared memory: the stores below may
     // alias that table as far as the compiler knows, so it keeps them in registers instead of
     // re-reading the parameter bank inside the loop
@@ -376,14 +449,25 @@ __device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const Pas
     for (uint32_t c0 = cbeg + (uint32_t)tid; c0 < cend; c0 += (uint32_t)(NT * K)) {
         uint32_t e[K];
         bool ok[K];
-        class_batch<K, NT>(tg, g, first, more, c0, ncls, needck, e, ok);
+        if (CHECK) {
+            class_batch<K, NT>(tg, g, first, more, c0, ncls, needck, e, ok);
+        } else {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                e[k] = class_e0(c0 + (uint32_t)(k * NT), g, first, more);
+                ok[k] = true;
+            }
+        }
+        uint32_t a[K];
         V x[K][D];
+#pragma unroll
+        for (int k = 0; k < K; ++k) a[k] = sb + e[k] * (uint32_t)sizeof(V);
 #pragma unroll
         for (int j = 0; j < D; ++j) {
             const bool aj = (act >> j) & 1;
 #pragma unroll
             for (int k = 0; k < K; ++k)
-                x[k][j] = aj ? lds2<V>(sb + e[k] * (uint32_t)sizeof(V) + mo[j]) : cz<V>();
+                x[k][j] = aj ? lds2<V>(a[k] + mo[j]) : cz<V>();
         }
 #pragma unroll
         for (int j = 0; j < D; ++j)
@@ -391,12 +475,12 @@ __device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const Pas
                 if (PERM) {
 #pragma unroll
                     for (int k = 0; k < K; ++k)
-                        if (ok[k]) sts2(sb + e[k] * (uint32_t)sizeof(V) + so[j], x[k][j]);
+                        sts2(CHECK ? (ok[k] ? a[k] + so[j] : trash) : a[k] + so[j], x[k][j]);
                 } else {
                     const V u = U[j];
 #pragma unroll
                     for (int k = 0; k < K; ++k)
-                        if (ok[k]) sts2(sb + e[k] * (uint32_t)sizeof(V) + so[j], cmul(u, x[k][j]));
+                        sts2(CHECK ? (ok[k] ? a[k] + so[j] : trash) : a[k] + so[j], cmul(u, x[k][j]));
                 }
             }
     }
@@ -439,21 +523,25 @@ template <int NT> struct PassK<5, NT> { static constexpr int value = NT >= 384 ?
 // NT = compute threads of the CTA (sets the register budget), NTG = threads of one consumer
 // group (the class stride)
 template <int D, int NT, int NTG, typename V>
-__device__ __forceinline__ void apply_gate_tile(const TileGate &tg, const PassGateP &g, V *buf,
-                                                const V *U, uint32_t ncls, bool needck, int tid) {
+__device__ __forceinline__ void apply_gate_tile(const TileGate &tg, const PassGateP &g, int kind, V *buf,
+                                                const V *U, uint32_t ncls, bool needck, int tid, uint32_t trash) {
     constexpr int K = PassK<D, NT>::value;
-    // full batches of K classes per thread, then the remainder one class per thread (no idle
-    // batch slots in the tail)
+    // full batches of K classes per thread (no predicates at all without checks), then the
+    // remainder one class per thread (a predicated K-batch for the remainder was measured slower:
+    // its idle slots cost more than the interleaving gains, profiles/r02/ab)
     const uint32_t full = ncls / (uint32_t)(NTG * K) * (uint32_t)(NTG * K);
-    if (g.kind == kPGeneral) {
-        gate_tile_general<D, K, NTG, V>(tg, g, buf, U, 0, full, ncls, needck, tid);
-        gate_tile_general<D, 1, NTG, V>(tg, g, buf, U, full, ncls, ncls, needck, tid);
-    } else if (g.kind == kPPerm) {
-        gate_tile_monomial<D, K, NTG, true, V>(tg, g, buf, U, 0, full, ncls, needck, tid);
-        gate_tile_monomial<D, 1, NTG, true, V>(tg, g, buf, U, full, ncls, ncls, needck, tid);
+    if (kind == kPGeneral) {
+        if (needck) gate_tile_general<D, K, NTG, true, V>(tg, g, buf, U, 0, full, ncls, true, tid, trash);
+        else gate_tile_general<D, K, NTG, false, V>(tg, g, buf, U, 0, full, ncls, false, tid, trash);
+        gate_tile_general<D, 1, NTG, true, V>(tg, g, buf, U, full, ncls, ncls, needck, tid, trash);
+    } else if (kind == kPPerm) {
+        if (needck) gate_tile_monomial<D, K, NTG, true, true, V>(tg, g, buf, U, 0, full, ncls, true, tid, trash);
+        else gate_tile_monomial<D, K, NTG, true, false, V>(tg, g, buf, U, 0, full, ncls, false, tid, trash);
+        gate_tile_monomial<D, 1, NTG, true, true, V>(tg, g, buf, U, full, ncls, ncls, needck, tid, trash);
     } else {
-        gate_tile_monomial<D, K, NTG, false, V>(tg, g, buf, U, 0, full, ncls, needck, tid);
-        gate_tile_monomial<D, 1, NTG, false, V>(tg, g, buf, U, full, ncls, ncls, needck, tid);
+        if (needck) gate_tile_monomial<D, K, NTG, false, true, V>(tg, g, buf, U, 0, full, ncls, true, tid, trash);
+        else gate_tile_monomial<D, K, NTG, false, false, V>(tg, g, buf, U, 0, full, ncls, false, tid, trash);
+        gate_tile_monomial<D, 1, NTG, false, true, V>(tg, g, buf, U, full, ncls, ncls, needck, tid, trash);
     }
 }
 
@@ -467,31 +555,47 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Warp-specialised: warps 0..NT/32-1 compute, warp NT/32 is the producer (TMA loads, stage
-// records, TMA stores).  full[s] completes when a tile's bytes have landed; done[s] when the
-// compute warps have finished it (after fence.proxy.async, so the bulk store sees their writes).
-// The compute warps form G consumer groups of NT/G threads; group g takes the CTA's tiles
-// g, g+G, ... (ping-pong), so one group's barrier waits overlap the other groups' work.
+// Warp-specialised: warps 0..NT/32-1 compute, warp NT/32 loads (stage records, TMA loads),
+// warp NT/32+1 stores (TMA stores).  full[s] completes when a tile's bytes have landed; done[s]
+// when the compute warps have finished it (after fence.proxy.async, so the bulk store sees their
+// writes); empty[s] when the store warp's bulk store has read the stage.  With one warp doing
+// both, every load waited for the previous store's smem read (wait_group.read covers all of the
+// thread's groups), serialising the stages; split, a stage is reloaded as soon as its own store
+// has been read.  The compute warps form G consumer groups of NT/G threads; group g takes the
+// CTA's tiles g, g+G, ... (ping-pong), so one group's barrier waits overlap the other groups' work.
+constexpr int kPassExtra = 64;     // the load warp and the store warp
 template <int NT, int G, typename V>
-__global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant__ PassParams p, int S, int TE) {
+__global__ void __launch_bounds__(NT + kPassExtra, 1) k_gate_pass(const __grid_constant__ PassParams p, int S, int TE) {
     constexpr int NTG = NT / G;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     V *bufs = reinterpret_cast<V *>(smem_raw);
     V *Us = bufs + (size_t)S * TE;                             // the pass's matrices (in V's precision)
     uint32_t *moffs = reinterpret_cast<uint32_t *>(Us + p.upool);   // per gate: member offsets
     uint32_t *soffs = moffs + kMaxPassGates * kMaxDim;               // per gate: sigma-member offsets
-    StageInfo *sinfo = reinterpret_cast<StageInfo *>(soffs + kMaxPassGates * kMaxDim);
+    uint32_t *gdesc = soffs + kMaxPassGates * kMaxDim;               // per gate: hot fields (kGDesc words)
+    StageInfo *sinfo = reinterpret_cast<StageInfo *>(gdesc + kMaxPassGates * kGDesc);
     uint64_t *full = reinterpret_cast<uint64_t *>(sinfo + S);
     uint64_t *done = full + S;
+    uint64_t *empty = done + S;
+    // per-lane slots that absorb the stores of classes a thread computes but must not write
+    const uint32_t trash_base = (smem_u32(empty + S) + 15u) & ~15u;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t trash = trash_base + (uint32_t)lane * 16u;
     if (tid == 0) {
-        for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&done[s], 1); }
+        for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&done[s], 1); mbar_init(&empty[s], 1); }
         fence_mbar_init();
     }
-    for (int k = tid; k < p.upool; k += NT + 32) Us[k] = to_v<V>(p.U[k]);
-    for (int k = tid; k < p.ngates * kMaxDim; k += NT + 32) {
+    for (int k = tid; k < p.upool; k += NT + kPassExtra) Us[k] = to_v<V>(p.U[k]);
+    for (int k = tid; k < p.ngates * kMaxDim; k += NT + kPassExtra) {
         moffs[k] = (&p.moff_t[0][0])[k];
         soffs[k] = (&p.soff_t[0][0])[k];
+    }
+    if (tid < p.ngates) {      // the fields every gate of every tile needs, one 48-byte record
+        const PassGateP &g = p.g[tid];
+        uint32_t *d = gdesc + tid * kGDesc;
+        d[0] = (uint32_t)g.d; d[1] = (uint32_t)g.kind; d[2] = g.ncls; d[3] = g.flags;
+        d[4] = (uint32_t)g.nins; d[5] = (uint32_t)g.uoff; d[6] = g.active; d[7] = g.ins_s[0];
+        d[8] = g.ins_m[0]; d[9] = g.ins_sd[0]; d[10] = g.ins_ps[0]; d[11] = 0;
     }
     __syncthreads();
     const uint64_t first = blockIdx.x, step = gridDim.x;
@@ -499,23 +603,27 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant_
     const uint64_t my = (p.ntiles - first + step - 1) / step;
 
     if (warp == NT / 32) {
-        // ---------------- producer warp
-        for (uint64_t i = 0; i < my + (uint64_t)S; ++i) {
+        // ---------------- load warp: tile i into stage i mod S once the store of tile i-S has read it
+        for (uint64_t i = 0; i < my; ++i) {
             const int s = (int)(i % (uint64_t)S);
-            if (i >= (uint64_t)S) {                   // drain tile i-S from stage s
-                const uint64_t j = i - (uint64_t)S;
-                if (j >= my) continue;
-                mbar_wait(&done[s], (uint32_t)((j / (uint64_t)S) & 1));
-                const StageInfo &si = sinfo[s];
-                for (int m = lane; m < p.M; m += 32)
-                    bulk_store(reinterpret_cast<V *>(p.psi) + si.ti.gbase + p.moff[m],
-                               bufs + (size_t)s * TE + (size_t)m * p.LT, si.ti.len * (uint32_t)sizeof(V));
-                bulk_commit();
-                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                __syncwarp();
-            }
-            if (i < my)
-                issue_loads(p, first + i * step, bufs + (size_t)s * TE, &full[s], &sinfo[s], lane);
+            if (i >= (uint64_t)S) mbar_wait(&empty[s], (uint32_t)(((i - (uint64_t)S) / (uint64_t)S) & 1));
+            issue_loads(p, first + i * step, bufs + (size_t)s * TE, &full[s], &sinfo[s], lane);
+        }
+        return;
+    }
+    if (warp == NT / 32 + 1) {
+        // ---------------- store warp: tile j back to HBM once computed; frees the stage when read
+        for (uint64_t j = 0; j < my; ++j) {
+            const int s = (int)(j % (uint64_t)S);
+            mbar_wait(&done[s], (uint32_t)((j / (uint64_t)S) & 1));
+            const StageInfo &si = sinfo[s];
+            for (int m = lane; m < p.M; m += 32)
+                bulk_store(reinterpret_cast<V *>(p.psi) + si.ti.gbase + p.moff[m],
+                           bufs + (size_t)s * TE + (size_t)m * p.LT, si.ti.len * (uint32_t)sizeof(V));
+            bulk_commit();
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
+            if (lane == 0 && j + (uint64_t)S < my) mbar_arrive(&empty[s]);
         }
         bulk_wait_all();
         return;
@@ -537,25 +645,33 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant_
         const StageInfo &si = sinfo[s];
         const uint32_t len = si.ti.len;
         const uint32_t fire = si.fire;
+        const uint32_t LT = p.LT, mLT = p.mLT;
         for (int gi = 0; gi < p.ngates; ++gi) {
             if (!((fire >> gi) & 1)) continue;          // out-of-tile control unmet: uniform skip
-            const PassGateP &g = p.g[gi];
+            const PassGateP &g = p.g[gi];               // cold fields only (controls, more insertions)
+            const uint4 h0 = *reinterpret_cast<const uint4 *>(gdesc + gi * kGDesc);       // d, kind, ncls, flags
+            const uint4 h1 = *reinterpret_cast<const uint4 *>(gdesc + gi * kGDesc + 4);   // nins, uoff, active, s
+            const uint4 h2 = *reinterpret_cast<const uint4 *>(gdesc + gi * kGDesc + 8);   // m, sd, ps
             TileGate tg;
-            tg.LT = p.LT;
-            tg.mLT = p.mLT;
+            tg.LT = LT;
+            tg.mLT = mLT;
             tg.len = len;
-            tg.flags = g.flags;
+            tg.flags = h0.w;
+            tg.nins = h1.x;
+            tg.active = h1.z;
+            tg.first = Ins1{h1.w, h2.x, h2.y, h2.z};
             tg.lowoff = si.lowoff[gi];
-            tg.moff = &p.moff_t[gi][0];          // parameter bank (uniform across the CTA)
-            tg.soff = &p.soff_t[gi][0];
-            const bool needck = g.flags != 0 || len < p.LT;
-            const V *U = Us + g.uoff;
-            switch (g.d) {
-                case 2: apply_gate_tile<2, NT, NTG, V>(tg, g, buf, U, g.ncls, needck, gtid); break;
-                case 3: apply_gate_tile<3, NT, NTG, V>(tg, g, buf, U, g.ncls, needck, gtid); break;
-                case 4: apply_gate_tile<4, NT, NTG, V>(tg, g, buf, U, g.ncls, needck, gtid); break;
-                case 5: apply_gate_tile<5, NT, NTG, V>(tg, g, buf, U, g.ncls, needck, gtid); break;
-                default: gate_tile_generic<V>(tg, g, buf, U, g.ncls, needck, gtid, NTG); break;
+            tg.moff = moffs + gi * kMaxDim;
+            tg.soff = soffs + gi * kMaxDim;
+            const bool needck = h0.w != 0 || len < LT;
+            const V *U = Us + h1.y;
+            const uint32_t ncls = h0.z;
+            switch (h0.x) {
+                case 2: apply_gate_tile<2, NT, NTG, V>(tg, g, (int)h0.y, buf, U, ncls, needck, gtid, trash); break;
+                case 3: apply_gate_tile<3, NT, NTG, V>(tg, g, (int)h0.y, buf, U, ncls, needck, gtid, trash); break;
+                case 4: apply_gate_tile<4, NT, NTG, V>(tg, g, (int)h0.y, buf, U, ncls, needck, gtid, trash); break;
+                case 5: apply_gate_tile<5, NT, NTG, V>(tg, g, (int)h0.y, buf, U, ncls, needck, gtid, trash); break;
+                default: gate_tile_generic<V>(tg, g, buf, U, ncls, needck, gtid, NTG); break;
             }
             compute_barrier(1 + grp, NTG);
         }
@@ -565,12 +681,257 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gate_pass(const __grid_constant_
     }
 }
 
+// ------------------------------------------------------------------ register-blocked stages
+namespace {
+
+// element (j along the gate's digit, k along the stage's other digit) of a d_a x d_b block
+template <int AX, int DA, int DB> struct BlockAx;
+template <int DA, int DB> struct BlockAx<0, DA, DB> {
+    static constexpr int D = DA, N = DB;
+    template <typename V> __device__ __forceinline__ static V &at(V (&x)[DA][DB], int j, int k) { return x[j][k]; }
+};
+template <int DA, int DB> struct BlockAx<1, DA, DB> {
+    static constexpr int D = DB, N = DA;
+    template <typename V> __device__ __forceinline__ static V &at(V (&x)[DA][DB], int j, int k) { return x[k][j]; }
+};
+
+// One gate of a stage on every class of one block (the block's columns for a gate on digit a,
+// its rows for digit b): y = U x, y_j = c_j x_j (§2.1), or a cyclic shift (§2.2).
+// A control on the stage's other digit selects one class.  Branch-free over the
+// classes (every class is computed, the control selects which results are kept), so the
+// classes' FMA chains share one basic block and interleave.
+template <int AX, int DA, int DB, typename V>
+__device__ __forceinline__ void block_gate(V (&x)[DA][DB], const StageGate &g, const V *__restrict__ Us) {
+    using A = BlockAx<AX, DA, DB>;
+    constexpr int D = A::D, N = A::N;
+    const int oc = g.octrl;
+    const V *__restrict__ U = Us + g.uoff;
+    bool keep[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) keep[k] = oc < 0 || oc == k;
+    if (g.kind == kSGeneral) {
+        V y[N][D];
+        if constexpr (D == 2) {            // 2 x 2: the matrix in registers, reused by every class
+            V u[D * D];
+#pragma unroll
+            for (int t = 0; t < D * D; ++t) u[t] = U[t];
+#pragma unroll
+            for (int k = 0; k < N; ++k)
+#pragma unroll
+                for (int i = 0; i < D; ++i) {
+                    y[k][i] = cz<V>();
+#pragma unroll
+                    for (int j = 0; j < D; ++j) cfma(y[k][i], u[i * D + j], A::at(x, j, k));
+                }
+        } else {                           // matrix entries streamed from shared memory (broadcast)
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+                // an offset the compiler cannot prove zero: re-read U per class instead of holding
+                // all d^2 entries in registers across the block's classes
+                const V *__restrict__ Uk = U + opaque_zero((uint32_t)k);
+#pragma unroll
+                for (int i = 0; i < D; ++i) {
+                    y[k][i] = cz<V>();
+#pragma unroll
+                    for (int j = 0; j < D; ++j) cfma(y[k][i], Uk[i * D + j], A::at(x, j, k));
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+#pragma unroll
+            for (int i = 0; i < D; ++i) A::at(x, i, k) = keep[k] ? y[k][i] : A::at(x, i, k);
+    } else if (g.kind == kSDiag) {
+        V c[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) c[j] = U[j];
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                const V t = cmul(c[j], A::at(x, j, k));
+                A::at(x, j, k) = keep[k] ? t : A::at(x, j, k);
+            }
+    } else {                               // kSShift: data movement only (selects)
+        const int s = g.shift;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            V t[D];
+#pragma unroll
+            for (int j = 0; j < D; ++j) t[j] = A::at(x, j, k);
+#pragma unroll
+            for (int i = 0; i < D; ++i) {  // y_i = x_{(i - s) mod d}
+                V v = t[i];
+#pragma unroll
+                for (int ss = 1; ss < D; ++ss) v = s == ss ? t[(i - ss + D) % D] : v;
+                A::at(x, i, k) = keep[k] ? v : t[i];
+            }
+        }
+    }
+}
+
+// run-digit controls of a gate (cls 1 / 3) at run position l of the tile
+__device__ __forceinline__ bool run_ctrl_ok(const StageGate &g, const uint32_t *lowoff, uint32_t l) {
+    bool ok = true;
+#pragma unroll 1
+    for (int k = 0; k < g.nctrl; ++k) {
+        const PassCtrl &cc = g.c[k];
+        if (cc.cls == 3) {
+            const uint32_t x = lowoff[k], t = x & kCls3Mask, mode = x >> 30;
+            ok = ok && (mode == 1 ? l < t : (mode == 2 && l >= t));
+        } else if (cc.cls == 1) {
+            uint32_t r, r2;
+            fastdiv32(lowoff[k] + l, cc.M, cc.mM, r);
+            const uint32_t q = fastdiv32(r, cc.w, cc.mw, r2);
+            fastdiv32(q, cc.d, cc.md, r2);
+            ok = ok && (r2 == cc.v);
+        }
+    }
+    return ok;
+}
+
+// One stage on one tile: every block (cb = thread, thread + NTG, ...) loaded once, all the
+// stage's gates applied in registers, stored once.
+template <int DA, int DB, typename V>
+__device__ __forceinline__ void run_stage(const StageParams &p, const StageRec &sr, const StageInfo &si,
+                                          V *buf, const V *__restrict__ Us, uint32_t gtid, uint32_t ntg) {
+    const uint32_t sbase = smem_u32(buf);
+    const Ins1 ia{sr.s0, sr.m0, sr.sd0, 0u}, ib{sr.s1, sr.m1, sr.sd1, 0u};
+    const uint32_t oa = sr.sa * (uint32_t)sizeof(V), ob = sr.sb * (uint32_t)sizeof(V);
+    const uint32_t len = si.ti.len, LT = p.LT, mLT = p.mLT;
+    const bool ragged = len < LT;
+    const uint32_t fire = si.fire;
+    const int g0 = sr.g0, g1 = sr.g0 + sr.ng;
+#pragma unroll 1
+    for (uint32_t cb = gtid; cb < sr.nblk; cb += ntg) {
+        uint32_t e = insert1(cb, ia);
+        if (DB > 1) e = insert1(e, ib);
+        uint32_t l;
+        tdiv(e, LT, mLT, l);
+        if (ragged && l >= len) continue;
+        const uint32_t base = sbase + e * (uint32_t)sizeof(V);
+        V x[DA][DB];
+#pragma unroll
+        for (int ja = 0; ja < DA; ++ja)
+#pragma unroll
+            for (int jb = 0; jb < DB; ++jb) x[ja][jb] = lds2<V>(base + ja * oa + jb * ob);
+#pragma unroll 1
+        for (int gi = g0; gi < g1; ++gi) {
+            if (!((fire >> gi) & 1)) continue;          // out-of-tile control unmet
+            const StageGate &g = p.g[gi];
+            bool ok = true;
+#pragma unroll 1
+            for (int k = 0; k < g.nic; ++k) {           // in-tile controls outside the stage
+                uint32_t r, r2;
+                const uint32_t q = tdiv(e, g.ic_s[k], g.ic_m[k], r);
+                tdiv(q, g.ic_d[k], g.ic_dm[k], r2);
+                ok = ok && (r2 == g.ic_v[k]);
+            }
+            if (g.runck) ok = ok && run_ctrl_ok(g, si.lowoff[gi], l);
+            if (!ok) continue;
+            if (g.axis == 0) block_gate<0, DA, DB, V>(x, g, Us);
+            else block_gate<1, DA, DB, V>(x, g, Us);
+        }
+#pragma unroll
+        for (int ja = 0; ja < DA; ++ja)
+#pragma unroll
+            for (int jb = 0; jb < DB; ++jb) sts2(base + ja * oa + jb * ob, x[ja][jb]);
+    }
+}
+
+}  // namespace
+
+// The register-blocked pass kernel: the same warp roles, ring and tile geometry as k_gate_pass;
+// the compute groups run the pass's stages one after another on each tile, a group barrier
+// between stages (a stage's blocks overlap the previous stage's).
+template <int NT, int G, typename V>
+__global__ void __launch_bounds__(NT + kPassExtra, 1) k_gate_stage(const __grid_constant__ StageParams p, int S, int TE) {
+    constexpr int NTG = NT / G;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    V *bufs = reinterpret_cast<V *>(smem_raw);
+    V *Us = bufs + (size_t)S * TE;
+    StageInfo *sinfo = reinterpret_cast<StageInfo *>(Us + kPoolS);
+    uint64_t *full = reinterpret_cast<uint64_t *>(sinfo + S);
+    uint64_t *done = full + S;
+    uint64_t *empty = done + S;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&done[s], 1); mbar_init(&empty[s], 1); }
+        fence_mbar_init();
+    }
+    for (int k = tid; k < p.upool; k += NT + kPassExtra) Us[k] = to_v<V>(p.U[k]);
+    __syncthreads();
+    const uint64_t first = blockIdx.x, step = gridDim.x;
+    if (first >= p.ntiles) return;
+    const uint64_t my = (p.ntiles - first + step - 1) / step;
+
+    if (warp == NT / 32) {
+        for (uint64_t i = 0; i < my; ++i) {
+            const int s = (int)(i % (uint64_t)S);
+            if (i >= (uint64_t)S) mbar_wait(&empty[s], (uint32_t)(((i - (uint64_t)S) / (uint64_t)S) & 1));
+            issue_loads(p, first + i * step, bufs + (size_t)s * TE, &full[s], &sinfo[s], lane);
+        }
+        return;
+    }
+    if (warp == NT / 32 + 1) {
+        for (uint64_t j = 0; j < my; ++j) {
+            const int s = (int)(j % (uint64_t)S);
+            mbar_wait(&done[s], (uint32_t)((j / (uint64_t)S) & 1));
+            const StageInfo &si = sinfo[s];
+            for (int m = lane; m < p.M; m += 32)
+                bulk_store(reinterpret_cast<V *>(p.psi) + si.ti.gbase + p.moff[m],
+                           bufs + (size_t)s * TE + (size_t)m * p.LT, si.ti.len * (uint32_t)sizeof(V));
+            bulk_commit();
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
+            if (lane == 0 && j + (uint64_t)S < my) mbar_arrive(&empty[s]);
+        }
+        bulk_wait_all();
+        return;
+    }
+
+    const int grp = tid / NTG, gtid = tid % NTG;
+    for (uint64_t i = (uint64_t)grp; i < my; i += (uint64_t)G) {
+        const int s = (int)(i % (uint64_t)S);
+        V *buf = bufs + (size_t)s * TE;
+        if (G > 1 && i >= (uint64_t)S) mbar_wait(&done[s], (uint32_t)(((i - (uint64_t)S) / (uint64_t)S) & 1));
+        mbar_wait(&full[s], (uint32_t)((i / (uint64_t)S) & 1));
+        const StageInfo &si = sinfo[s];
+        for (int st = 0; st < p.nstages; ++st) {
+            if (st > 0) compute_barrier(1 + grp, NTG);
+            const StageRec &sr = p.st[st];
+            const int key = sr.da * 8 + sr.db;
+            switch (key) {
+                case 2 * 8 + 2: run_stage<2, 2, V>(p, sr, si, buf, Us, gtid, NTG); break;
+                case 2 * 8 + 3: run_stage<2, 3, V>(p, sr, si, buf, Us, gtid, NTG); break;
+                case 3 * 8 + 2: run_stage<3, 2, V>(p, sr, si, buf, Us, gtid, NTG); break;
+                case 2 * 8 + 4: run_stage<2, 4, V>(p, sr, si, buf, Us, gtid, NTG); break;
+                case 4 * 8 + 2: run_stage<4, 2, V>(p, sr, si, buf, Us, gtid, NTG); break;
+                case 2 * 8 + 5: run_stage<2, 5, V>(p, sr, si, buf, Us, gtid, NTG); break;
+                case 5 * 8 + 2: run_stage<5, 2, V>(p, sr, si, buf, Us, gtid, NTG); break;
+                case 3 * 8 + 3: run_stage<3, 3, V>(p, sr, si, buf, Us, gtid, NTG); break;
+                case 3 * 8 + 4: run_stage<3, 4, V>(p, sr, si, buf, Us, gtid, NTG); break;
+                case 4 * 8 + 3: run_stage<4, 3, V>(p, sr, si, buf, Us, gtid, NTG); break;
+                case 2 * 8 + 1: run_stage<2, 1, V>(p, sr, si, buf, Us, gtid, NTG); break;
+                case 3 * 8 + 1: run_stage<3, 1, V>(p, sr, si, buf, Us, gtid, NTG); break;
+                case 4 * 8 + 1: run_stage<4, 1, V>(p, sr, si, buf, Us, gtid, NTG); break;
+                default: run_stage<5, 1, V>(p, sr, si, buf, Us, gtid, NTG); break;
+            }
+        }
+        fence_proxy_async();
+        compute_barrier(1 + grp, NTG);
+        if (gtid == 0) mbar_arrive(&done[s]);
+    }
+}
+
 // ------------------------------------------------------------------------------ host
-// Build the pass parameters; returns false if the pass does not fit this kernel.
-bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const PassPlan &pp, double2 *psi,
-                int TE, PassParams &p, PassWork *work) {
-    std::memset(&p, 0, sizeof(p));
-    if ((int)pp.gates.size() > kMaxPassGates || pp.tile > (uint64_t)TE) return false;
+// Tile geometry of a pass (shared by the per-gate and the register-blocked kernels): members
+// (combinations of the H digits) with their global offsets, the removed H digits of the tile
+// enumeration, the run R below min H and its split into tiles of LT run elements.  W[h] = member
+// radix weight of H digit h.  Returns false if the pass does not fit.
+template <class PP>
+static bool pass_geometry(const Register &reg, const PassPlan &pp, double2 *psi, int TE, PP &p,
+                          std::vector<uint64_t> &W, uint64_t &R_out, uint64_t &LT_out) {
     p.psi = psi;
     const int m0 = pp.m0;
     const uint64_t L = (m0 < reg.n) ? reg.b[m0] : reg.D;
@@ -580,7 +941,7 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
     for (int h : pp.H) M *= (uint64_t)reg.dims[h];
     if (M > (uint64_t)kMaxMembers) return false;
     // member radix weights and global offsets (H ascending)
-    std::vector<uint64_t> W(reg.n, 0);
+    W.assign(reg.n, 0);
     {
         uint64_t w = 1;
         for (int h : pp.H) { W[h] = w; w *= (uint64_t)reg.dims[h]; }
@@ -622,6 +983,50 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
     p.tpr_m = make_fastdiv64(p.tpr).m;
     const uint64_t nruns = reg.D / (M * R);
     p.ntiles = nruns * p.tpr;
+    R_out = R;
+    LT_out = LT;
+    return true;
+}
+
+// A control decided per tile (not on an in-tile digit): a run digit below min H (cls 1, or cls 3
+// when b_c d_c >= 2^31) or a digit outside the tile (cls 2).  Returns true for a run digit.
+static bool fill_tile_ctrl(PassCtrl &cc, const Register &reg, int c, uint32_t v, uint64_t R) {
+    const uint64_t dc = (uint64_t)reg.dims[c];
+    cc.v = v;
+    cc.d = (uint32_t)dc;
+    cc.md = make_fastdiv32(cc.d).m;
+    if (reg.b[c] < R && reg.b[c] * dc < (1ull << 31)) {   // run digit: tile's run offset
+        cc.cls = 1;
+        cc.w = (uint32_t)reg.b[c];
+        cc.mw = make_fastdiv32(cc.w).m;
+        cc.M = cc.w * cc.d;
+        cc.mM = make_fastdiv32(cc.M).m;
+        cc.mb64 = make_fastdiv64(cc.M).m;
+        return true;
+    }
+    if (reg.b[c] < R) {                                    // b_c d_c >= 2^31: per-tile threshold
+        cc.cls = 3;
+        cc.b64 = reg.b[c];
+        cc.mb64 = make_fastdiv64(cc.b64).m;
+        cc.md64 = make_fastdiv64(dc).m;
+        return true;
+    }
+    cc.cls = 2;                                            // outside the tile: constant per tile
+    cc.b64 = reg.b[c];
+    cc.mb64 = make_fastdiv64(cc.b64).m;
+    cc.md64 = make_fastdiv64(cc.d).m;
+    return false;
+}
+
+// Build the pass parameters; returns false if the pass does not fit this kernel.
+bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const PassPlan &pp, double2 *psi,
+                int TE, PassParams &p, PassWork *work) {
+    std::memset(&p, 0, sizeof(p));
+    if ((int)pp.gates.size() > kMaxPassGates || pp.tile > (uint64_t)TE) return false;
+    std::vector<uint64_t> W;
+    uint64_t R = 0, LT = 0;
+    if (!pass_geometry(reg, pp, psi, TE, p, W, R, LT)) return false;
+    const int m0 = pp.m0;
     auto in_tile = [&](int q) {
         return q < m0 || std::find(pp.H.begin(), pp.H.end(), q) != pp.H.end();
     };
@@ -765,30 +1170,7 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
                 cls_div *= dc;
                 continue;
             }
-            PassCtrl &cc = q.c[nc++];
-            cc.v = v;
-            cc.d = (uint32_t)dc;
-            cc.md = make_fastdiv32(cc.d).m;
-            if (reg.b[c] < R && reg.b[c] * dc < (1ull << 31)) {   // run digit: tile's run offset
-                cc.cls = 1;
-                q.flags |= kFRunCtrl;
-                cc.w = (uint32_t)reg.b[c];
-                cc.mw = make_fastdiv32(cc.w).m;
-                cc.M = cc.w * cc.d;
-                cc.mM = make_fastdiv32(cc.M).m;
-                cc.mb64 = make_fastdiv64(cc.M).m;
-            } else if (reg.b[c] < R) {         // run digit with b_c d_c >= 2^31: per-tile threshold
-                cc.cls = 3;
-                q.flags |= kFRunCtrl;
-                cc.b64 = reg.b[c];
-                cc.mb64 = make_fastdiv64(cc.b64).m;
-                cc.md64 = make_fastdiv64(dc).m;
-            } else {                           // outside the tile: constant per tile
-                cc.cls = 2;
-                cc.b64 = reg.b[c];
-                cc.mb64 = make_fastdiv64(cc.b64).m;
-                cc.md64 = make_fastdiv64(cc.d).m;
-            }
+            if (fill_tile_ctrl(q.c[nc++], reg, c, v, R)) q.flags |= kFRunCtrl;
         }
         q.nctrl = nc;
         if ((int)ins.size() > kMaxIns) return false;
@@ -800,7 +1182,7 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
             q.ins_sd[i] = (uint32_t)(ins[i].s * ins[i].d);
             q.ins_ps[i] = (uint32_t)(ins[i].s * ins[i].pin);
         }
-        q.ncls = (uint32_t)((uint64_t)M * LT / cls_div);
+        q.ncls = (uint32_t)((uint64_t)p.M * LT / cls_div);
     }
     return p.ntiles > 0;
 }
@@ -811,7 +1193,8 @@ cudaError_t launch_pass_t(const PassParams &p, cudaStream_t st, const LaunchCfg 
     // size for the largest matrix pool so the attribute and the occupancy are set once per config
     const size_t smem = (size_t)S * TE * sizeof(V) + (size_t)kPoolC * sizeof(V) +
                         (size_t)2 * kMaxPassGates * kMaxDim * sizeof(uint32_t) +
-                        (size_t)S * sizeof(StageInfo) + (size_t)2 * S * sizeof(uint64_t);
+                        (size_t)kMaxPassGates * kGDesc * sizeof(uint32_t) +
+                        (size_t)S * sizeof(StageInfo) + (size_t)3 * S * sizeof(uint64_t) + 16 + 32 * 16;
     static LaunchAttr attr;
     const int dv = current_device_slot();
     if (attr.configured[dv] < smem) {
@@ -821,13 +1204,13 @@ cudaError_t launch_pass_t(const PassParams &p, cudaStream_t st, const LaunchCfg 
     }
     if (attr.occ_for[dv] != smem) {   // resident CTAs per SM at this smem size (persistent grid)
         int o = 1;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_gate_pass<NT, G, V>, NT + 32, smem) != cudaSuccess || o < 1) o = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_gate_pass<NT, G, V>, NT + kPassExtra, smem) != cudaSuccess || o < 1) o = 1;
         attr.occ[dv] = o;
         attr.occ_for[dv] = smem;
     }
     const uint64_t cap = (uint64_t)cfg.num_sms * (uint64_t)attr.occ[dv];
     const unsigned grid = (unsigned)(p.ntiles < cap ? p.ntiles : cap);
-    k_gate_pass<NT, G, V><<<grid, NT + 32, smem, st>>>(p, S, TE);
+    k_gate_pass<NT, G, V><<<grid, NT + kPassExtra, smem, st>>>(p, S, TE);
     return cudaGetLastError();
 }
 
@@ -848,8 +1231,193 @@ cudaError_t launch_pass(const PassParams &p, cudaStream_t st, const LaunchCfg &c
     return launch_pass_t<256, 1, double2>(p, st, cfg);
 }
 
+// ---- register-blocked stages: host side
+// Group the pass's gates (in pass order) into stages and fill the stage kernel's parameters.
+// Returns false (the caller then uses k_gate_pass) if a target digit has d > 5, a gate has more
+// than kMaxPassCtrl controls, or the matrix pool overflows.
+bool build_stage_pass(const Register &reg, const std::vector<GateSpec> &gates, const PassPlan &pp, double2 *psi,
+                      int TE, StageParams &p, PassWork *work) {
+    std::memset(&p, 0, sizeof(p));
+    if ((int)pp.gates.size() > kMaxPassGates || pp.tile > (uint64_t)TE) return false;
+    std::vector<uint64_t> W;
+    uint64_t R = 0, LT = 0;
+    if (!pass_geometry(reg, pp, psi, TE, p, W, R, LT)) return false;
+    const int m0 = pp.m0;
+    auto in_tile = [&](int q) { return q < m0 || std::find(pp.H.begin(), pp.H.end(), q) != pp.H.end(); };
+    auto tile_stride = [&](int q) -> uint64_t { return q < m0 ? reg.b[q] : W[q] * LT; };
+    for (int i : pp.gates) {
+        const GateSpec &g = gates[i];
+        if (g.span != 1 || !in_tile(g.target) || g.d > 5 || (int)g.ctrl.size() > kMaxPassCtrl) return false;
+    }
+    std::vector<int> tiled;                      // in-tile digits: passive partners for 1-digit stages
+    for (int q = 0; q < reg.n; ++q)
+        if (in_tile(q)) tiled.push_back(q);
+    // stages: maximal runs of consecutive gates whose targets fit one digit pair
+    struct St { int a, b; std::vector<int> g; };
+    std::vector<St> stages;
+    for (int i : pp.gates) {
+        const int t = gates[i].target;
+        if (!stages.empty()) {
+            St &c = stages.back();
+            if (t == c.a || t == c.b) { c.g.push_back(i); continue; }
+            if (c.b < 0 && reg.dims[c.a] * reg.dims[t] <= kStageAmps) { c.b = t; c.g.push_back(i); continue; }
+        }
+        stages.push_back({t, -1, {i}});
+    }
+    if ((int)stages.size() > kMaxPassGates) return false;
+    *work = PassWork{};
+    int ng = 0, uoff = 0;
+    const double Dloc = (double)reg.D;
+    for (size_t si = 0; si < stages.size(); ++si) {
+        St &S = stages[si];
+        if (S.b < 0) {                           // passive partner: the smallest in-tile dim that fits
+            int best = -1;
+            for (int q : tiled)
+                if (q != S.a && reg.dims[S.a] * reg.dims[q] <= kStageAmps &&
+                    (best < 0 || reg.dims[q] < reg.dims[best] || (reg.dims[q] == reg.dims[best] && q > best)))
+                    best = q;
+            S.b = best;                          // may stay -1 (a one-digit tile): d_b = 1
+        }
+        if (S.b >= 0 && tile_stride(S.b) < tile_stride(S.a)) std::swap(S.a, S.b);   // a = lower stride
+        StageRec &r = p.st[si];
+        r.da = reg.dims[S.a];
+        r.db = S.b >= 0 ? reg.dims[S.b] : 1;
+        r.sa = (uint32_t)tile_stride(S.a);
+        r.sb = S.b >= 0 ? (uint32_t)tile_stride(S.b) : 0u;
+        r.nblk = (uint32_t)((uint64_t)p.M * LT / (uint64_t)(r.da * r.db));
+        r.s0 = r.sa;
+        r.m0 = make_fastdiv32(r.s0).m;
+        r.sd0 = r.sa * (uint32_t)r.da;
+        r.s1 = S.b >= 0 ? r.sb : 1u;
+        r.m1 = S.b >= 0 ? make_fastdiv32(r.s1).m : 0u;
+        r.sd1 = S.b >= 0 ? r.sb * (uint32_t)r.db : 1u;
+        r.g0 = ng;
+        r.ng = (int32_t)S.g.size();
+        work->item_touched += Dloc;              // the stage's one shared-memory round trip
+        for (int gi : S.g) {
+            const GateSpec &g = gates[gi];
+            GatePlan gp;
+            std::string err;
+            if (plan_gate(reg, g, false, &gp, &err) != SV_OK) return false;
+            work->touched += (double)gp.touched;
+            StageGate &q = p.g[ng++];
+            q.axis = g.target == S.a ? 0 : 1;
+            q.octrl = -1;
+            const int d = g.d;
+            // kind: diagonal (§2.1), pure cyclic shift X_{+s} (§2.2), else the general rule (§2.3)
+            bool diag = true, shift = true;
+            int sh = -1;
+            for (int i = 0; i < d; ++i)
+                for (int j = 0; j < d; ++j) {
+                    const double2 u = g.U[(size_t)i * d + j];
+                    const bool nz = u.x != 0.0 || u.y != 0.0;
+                    if (i != j && nz) diag = false;
+                    if (nz) {
+                        const int k = ((i - j) % d + d) % d;
+                        if (!(u.x == 1.0 && u.y == 0.0) || (sh >= 0 && k != sh)) shift = false;
+                        sh = k;
+                    }
+                }
+            if (sh <= 0) shift = false;
+            double cprod = 1.0;
+            for (const auto &c : g.ctrl) cprod *= (double)reg.dims[c.q];
+            const int need = shift ? 0 : (diag ? d : d * d);
+            if (uoff + need > kPoolS) return false;
+            q.uoff = uoff;
+            if (shift) {
+                q.kind = kSShift;
+                q.shift = sh;
+            } else if (diag) {
+                q.kind = kSDiag;
+                for (int j = 0; j < d; ++j) p.U[uoff + j] = g.U[(size_t)j * d + j];
+            } else {
+                q.kind = kSGeneral;
+                for (int k = 0; k < d * d; ++k) p.U[uoff + k] = g.U[k];
+                work->flops += 8.0 * d * (Dloc / cprod);
+            }
+            uoff += need;
+            for (const auto &c : g.ctrl) {
+                const uint32_t v = (uint32_t)c.v;
+                if (c.q == S.a || c.q == S.b) { q.octrl = (int32_t)v; continue; }
+                if (in_tile(c.q)) {
+                    const int k = q.nic++;
+                    q.ic_s[k] = (uint32_t)tile_stride(c.q);
+                    q.ic_m[k] = make_fastdiv32(q.ic_s[k]).m;
+                    q.ic_d[k] = (uint32_t)reg.dims[c.q];
+                    q.ic_dm[k] = make_fastdiv32(q.ic_d[k]).m;
+                    q.ic_v[k] = v;
+                    continue;
+                }
+                if (fill_tile_ctrl(q.c[q.nctrl++], reg, c.q, v, R)) q.runck = 1;
+            }
+        }
+    }
+    p.nstages = (int32_t)stages.size();
+    p.ngates = ng;
+    p.upool = uoff;
+    return p.ntiles > 0;
+}
+
+template <int NT, int G, typename V>
+cudaError_t launch_stage_t(const StageParams &p, cudaStream_t st, const LaunchCfg &cfg) {
+    const int S = cfg.pass_stages, TE = cfg.pass_tile;
+    const size_t smem = (size_t)S * TE * sizeof(V) + (size_t)kPoolS * sizeof(V) + (size_t)S * sizeof(StageInfo) +
+                        (size_t)3 * S * sizeof(uint64_t);
+    static LaunchAttr attr;
+    const int dv = current_device_slot();
+    if (attr.configured[dv] < smem) {
+        cudaError_t e = cudaFuncSetAttribute(k_gate_stage<NT, G, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr.configured[dv] = smem;
+    }
+    if (attr.occ_for[dv] != smem) {
+        int o = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_gate_stage<NT, G, V>, NT + kPassExtra, smem) != cudaSuccess || o < 1) o = 1;
+        attr.occ[dv] = o;
+        attr.occ_for[dv] = smem;
+    }
+    const uint64_t cap = (uint64_t)cfg.num_sms * (uint64_t)attr.occ[dv];
+    const unsigned grid = (unsigned)(p.ntiles < cap ? p.ntiles : cap);
+    k_gate_stage<NT, G, V><<<grid, NT + kPassExtra, smem, st>>>(p, S, TE);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess && getenv("SV_DEBUG_LAUNCH")) {
+        cudaFuncAttributes fa;
+        cudaFuncGetAttributes(&fa, k_gate_stage<NT, G, V>);
+        fprintf(stderr, "k_gate_stage<%d,%d> launch %s: grid %u block %d smem %zu | regs %d maxThreads %d static smem %zu "
+                        "maxDyn %d local %zu\n", NT, G, cudaGetErrorString(e), grid, NT + kPassExtra, smem, fa.numRegs,
+                fa.maxThreadsPerBlock, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, fa.localSizeBytes);
+    }
+    return e;
+}
+
+cudaError_t launch_stage(const StageParams &p, cudaStream_t st, const LaunchCfg &cfg) {
+    if (cfg.c64) return launch_stage_t<512, 2, float2>(p, st, cfg);
+    int G = cfg.pass_groups;
+    while (G > 1 && cfg.pass_stages < G) G /= 2;
+    if (cfg.pass_threads >= 512) {
+        if (G >= 2) return launch_stage_t<512, 2, double2>(p, st, cfg);
+        return launch_stage_t<512, 1, double2>(p, st, cfg);
+    }
+    if (cfg.pass_threads >= 384) {
+        if (G >= 2) return launch_stage_t<384, 2, double2>(p, st, cfg);
+        return launch_stage_t<384, 1, double2>(p, st, cfg);
+    }
+    if (G >= 2) return launch_stage_t<256, 2, double2>(p, st, cfg);
+    return launch_stage_t<256, 1, double2>(p, st, cfg);
+}
+
 cudaError_t run_pass(const Register &reg, const std::vector<GateSpec> &gates, const PassPlan &pp, double2 *psi,
                      cudaStream_t st, const LaunchCfg &cfg, bool *handled, PassWork *work) {
+    // register-blocked stages (k_gate_stage) unless disabled or the pass does not fit them
+    if (cfg.pass_kernel != 1) {
+        static thread_local StageParams sp;   // ~27 KB; parameters are copied at launch
+        if (build_stage_pass(reg, gates, pp, psi, cfg.pass_tile, sp, work) &&
+            !(cfg.c64 && (sp.L % 2 != 0 || sp.LT % 2 != 0))) {
+            *handled = true;
+            return launch_stage(sp, st, cfg);
+        }
+        if (cfg.pass_kernel == 2) { *handled = false; return cudaSuccess; }
+    }
     static thread_local PassParams p;   // ~23 KB; parameters are copied at launch
     *handled = build_pass(reg, gates, pp, psi, cfg.pass_tile, p, work);
     // complex64 (8-byte elements): every bulk copy must start at a 16-byte aligned address and

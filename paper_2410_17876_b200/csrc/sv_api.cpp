@@ -69,6 +69,7 @@ void default_cfg(LaunchCfg &c, int device) {
     c.pass_groups = 2;         // two consumer groups ping-pong over tiles
     c.shard_swap = 1;          // qubit remapping for gates on sharded qubits
     c.pass_search = 1;         // in-tile set chosen by subset search (c4 29 -> 22 passes)
+    c.pass_kernel = 0;         // register-blocked stages (k_gate_stage) when the pass fits them
 }
 
 }  // namespace
@@ -549,6 +550,10 @@ sv_status sv_set_option(sv_handle h, int32_t option, int64_t value) {
         case SV_OPT_PASS_SEARCH:
             h->cfg.pass_search = value != 0;
             return SV_OK;
+        case SV_OPT_PASS_KERNEL:
+            if (value < 0 || value > 2) return fail(SV_ERR_INVALID_ARG, "pass kernel 0..2");
+            h->cfg.pass_kernel = (int)value;
+            return SV_OK;
         case SV_OPT_PLAN_CACHE:
             h->plan_cache = value != 0;
             if (!h->plan_cache) { h->plan_key.clear(); h->plan_specs.clear(); h->plan_passes.clear(); }
@@ -711,6 +716,14 @@ sv_status sv_merge_plan(const int32_t *dims, int32_t n, const sv_gate *gates, in
 sv_status sv_block_plan(const int32_t *dims, int32_t n, const sv_gate *gates, int64_t ngates,
                         int64_t tile_cap, int64_t *out_order, int64_t *out_pass, int64_t *out_tile,
                         int64_t *out_npasses) {
+    return sv_block_plan_ex(dims, n, gates, ngates, tile_cap, 24, 64, 0, out_order, out_pass, out_tile,
+                            out_npasses);
+}
+
+sv_status sv_block_plan_ex(const int32_t *dims, int32_t n, const sv_gate *gates, int64_t ngates,
+                           int64_t tile_cap, int32_t max_gates, int32_t window, int32_t search,
+                           int64_t *out_order, int64_t *out_pass, int64_t *out_tile, int64_t *out_npasses) {
+    if (max_gates < 1 || max_gates > 32 || window < 1) return fail(SV_ERR_INVALID_ARG, "max_gates 1..32, window >= 1");
     Register reg;
     sv_status s = make_register(dims, n, &reg, &g_err);
     if (s != SV_OK) return s;
@@ -723,7 +736,7 @@ sv_status sv_block_plan(const int32_t *dims, int32_t n, const sv_gate *gates, in
         if (s != SV_OK) return s;
         specs.push_back(make_spec(reg, g.target, g.ctrl, g.ctrl_vals, g.nctrl, g.U));
     }
-    std::vector<PassPlan> passes = plan_passes(reg, specs, (uint64_t)tile_cap, 24, 64);
+    std::vector<PassPlan> passes = plan_passes(reg, specs, (uint64_t)tile_cap, max_gates, window, search != 0);
     int64_t k = 0;
     for (size_t p = 0; p < passes.size(); ++p) {
         out_tile[p] = (int64_t)passes[p].tile;

@@ -20,7 +20,7 @@ SV_FUSE, SV_NO_CHECK, SV_GRAPH, SV_BLOCK = 1, 2, 4, 8
 SV_OPT_KERNEL, SV_OPT_TILE_ELEMS, SV_OPT_TILE_STAGES, SV_OPT_CTAS_PER_SM, SV_OPT_PROFILE, SV_OPT_PASS_TILE = 1, 2, 3, 4, 5, 6
 SV_OPT_PASS_STAGES, SV_OPT_PASS_THREADS, SV_OPT_PASS_GATES, SV_OPT_PASS_GROUPS = 7, 8, 9, 10
 SV_OPT_PASS_WINDOW, SV_OPT_PASS_MERGE, SV_OPT_SHARD_SWAP, SV_OPT_PASS_SEARCH = 11, 12, 13, 14
-SV_OPT_PLAN_CACHE = 15
+SV_OPT_PLAN_CACHE, SV_OPT_PASS_KERNEL = 15, 16
 
 STATUS = {0: "SV_OK", 1: "SV_ERR_INVALID_ARG", 2: "SV_ERR_DIM", 3: "SV_ERR_OVERFLOW",
           4: "SV_ERR_QUDIT_RANGE", 5: "SV_ERR_CTRL_OVERLAP", 6: "SV_ERR_CTRL_DUP",
@@ -122,6 +122,9 @@ _sig("sv_sparse_entries", [_h, C.c_uint64, _u64p, _dp, C.POINTER(C.c_uint64)])
 _sig("sv_sparse_launches", [_h, C.POINTER(C.c_uint64)])
 _sig("sv_block_plan", [_i32p, C.c_int32, C.POINTER(sv_gate), C.c_int64, C.c_int64, C.POINTER(C.c_int64),
                        C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)])
+_sig("sv_block_plan_ex", [_i32p, C.c_int32, C.POINTER(sv_gate), C.c_int64, C.c_int64, C.c_int32, C.c_int32,
+                          C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                          C.POINTER(C.c_int64)])
 
 EXPORTS = ["sv_create", "sv_create_ex", "sv_create_sharded", "sv_nccl_unique_id", "sv_destroy",
            "sv_create_sharded_ipc", "sv_ipc_unique_id",
@@ -129,7 +132,8 @@ EXPORTS = ["sv_create", "sv_create_ex", "sv_create_sharded", "sv_nccl_unique_id"
            "sv_norm", "sv_sync", "sv_last_error", "sv_get_info", "sv_set_option", "sv_plan_gate",
            "sv_enumerate_fibres", "sv_fuse_plan", "sv_merge_plan", "sv_shard_plan", "sv_version", "sv_profile_read", "sv_block_plan",
            "sv_sparse_create", "sv_sparse_destroy", "sv_sparse_reset", "sv_sparse_apply_gate",
-           "sv_sparse_apply_circuit", "sv_sparse_nnz", "sv_sparse_entries", "sv_sparse_launches"]
+           "sv_sparse_apply_circuit", "sv_sparse_nnz", "sv_sparse_entries", "sv_sparse_launches",
+           "sv_block_plan_ex"]
 
 
 def _check(rc: int):
@@ -353,8 +357,10 @@ def merge_plan(dims, gates, window: int = 64):
     return _host_plan(_lib.sv_merge_plan, dims, gates, C.c_int32(int(window)))
 
 
-def block_plan(dims, gates, tile_cap: int = 4096):
-    """Host pass planner: (order, pass_id, tiles) — gate indices in application order."""
+def block_plan(dims, gates, tile_cap: int = 4096, max_gates: int | None = None, window: int = 64,
+               search: bool = False):
+    """Host pass planner: (order, pass_id, tiles) — gate indices in application order.
+    max_gates=None: sv_block_plan (24 gates, window 64, no search); else sv_block_plan_ex."""
     gates = list(gates)
     ga = _GateArray(gates)
     n = max(1, len(gates))
@@ -362,9 +368,14 @@ def block_plan(dims, gates, tile_cap: int = 4096):
     npass = C.c_int64()
     d = _i32(dims)
     p64 = C.POINTER(C.c_int64)
-    _check(_lib.sv_block_plan(d.ctypes.data_as(_i32p), d.size, ga.arr, ga.n, int(tile_cap),
-                              order.ctypes.data_as(p64), pid.ctypes.data_as(p64), tiles.ctypes.data_as(p64),
-                              C.byref(npass)))
+    if max_gates is None:
+        _check(_lib.sv_block_plan(d.ctypes.data_as(_i32p), d.size, ga.arr, ga.n, int(tile_cap),
+                                  order.ctypes.data_as(p64), pid.ctypes.data_as(p64), tiles.ctypes.data_as(p64),
+                                  C.byref(npass)))
+    else:
+        _check(_lib.sv_block_plan_ex(d.ctypes.data_as(_i32p), d.size, ga.arr, ga.n, int(tile_cap), int(max_gates),
+                                     int(window), 1 if search else 0, order.ctypes.data_as(p64),
+                                     pid.ctypes.data_as(p64), tiles.ctypes.data_as(p64), C.byref(npass)))
     return order[:len(gates)], pid[:len(gates)], tiles[:npass.value]
 
 

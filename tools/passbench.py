@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--dtype", default="c128", choices=["c128", "c64"])
     ap.add_argument("--reps", type=int, default=1)
     ap.add_argument("--search", type=int, default=1, help="SV_OPT_PASS_SEARCH (in-tile set search)")
+    ap.add_argument("--skip-noblock", action="store_true", help="do not time the single-gate mode")
+    ap.add_argument("--pass-kernel", type=int, default=0, help="SV_OPT_PASS_KERNEL: 0 auto, 1 per-gate, 2 stages")
     args = ap.parse_args()
     import torch
     import paper_2410_17876_b200 as P
@@ -37,7 +39,7 @@ def main():
     st = P.State(dims, dtype=args.dtype)
     ext = torch.cuda.ExternalStream(st.info().cuda_stream)
     ga = P.sv._GateArray(gates)
-    cases = [("noblock", 0, 0, 0, 0)]
+    cases = [] if args.skip_noblock else [("noblock", 0, 0, 0, 0)]
     for te, s, nt, ng, gr, wi in itertools.product(*[[int(x) for x in a.split(",")] for a in
                                                      (args.tiles, args.stages, args.threads, args.gates, args.groups,
                                                       args.windows)]):
@@ -54,6 +56,7 @@ def main():
             st.set_option(P.sv.SV_OPT_PASS_GROUPS, rest[0])
             st.set_option(P.sv.SV_OPT_PASS_WINDOW, rest[1])
             st.set_option(P.sv.SV_OPT_PASS_SEARCH, args.search)
+            st.set_option(P.sv.SV_OPT_PASS_KERNEL, args.pass_kernel)
         st.reset(0)
         st.apply_circuit(ga, fuse=True, check=False, block=block)
         st.sync()
@@ -68,7 +71,7 @@ def main():
         ms = e0.elapsed_time(e1) / args.reps
         launches = (st.info().kernel_launches - n0) // args.reps
         print(json.dumps({"config": args.config, "D": D, "gates": len(gates), "mode": kind, "tile": te,
-                          "stages": s, "threads": nt, "groups": rest[0] if rest else 0, "window": rest[1] if rest else 0, "max_gates": ng, "ms": ms, "launches": launches,
+                          "stages": s, "threads": nt, "groups": rest[0] if rest else 0, "window": rest[1] if rest else 0, "max_gates": ng, "pass_kernel": args.pass_kernel, "ms": ms, "launches": launches,
                           "updates_per_s": T / (ms / 1e3), "equiv_GBps": 32.0 * T / (ms / 1e3) / 1e9,
                           "pass_GBps": 32.0 * D * launches / (ms / 1e3) / 1e9}), flush=True)
     st.close()
