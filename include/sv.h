@@ -227,11 +227,11 @@ SV_API sv_status sv_get_info(sv_handle h, sv_info *out);
 #define SV_OPT_PASS_SEARCH 14   /* 1 (default): each SV_BLOCK pass's in-tile qudit set is the one that
                                    admits the most window gates (subset search); 0: first come, first
                                    admitted */
-#define SV_OPT_PASS_KERNEL 16   /* SV_BLOCK pass kernel: 0 (default) = register-blocked stages
-                                   (k_gate_stage: consecutive gates on a pair of in-tile digits applied
-                                   to register blocks, one shared-memory round trip per stage) when the
-                                   pass fits them (targets d <= 5), else the per-gate kernel; 1 = per-gate
-                                   kernel (k_gate_pass) only; 2 = stages only                       */
+#define SV_OPT_PASS_KERNEL 16   /* SV_BLOCK pass kernel: 0 (default) = per-gate (k_gate_pass: every gate
+                                   sweeps the shared-memory tile, one group barrier per gate); 1 =
+                                   register-blocked stages (k_gate_stage: consecutive gates on a pair of
+                                   in-tile digits applied to register blocks, one shared-memory round
+                                   trip per stage) when the pass fits them (targets d <= 5)            */
 #define SV_OPT_PLAN_CACHE  15   /* 1 (default): the SV_BLOCK host plan (merged gates + passes) is
                                    memoised per handle and reused while the same gates and options
                                    come again; 0: plan every call (cold-submission timing)          */

@@ -47,6 +47,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
               f'-DSV_NCCL_WHEEL_LIB="{nccl_lib}"', "-DSV_BUILD_LIB"]
     if verbose:
         common += ["-Xptxas", "-v"]
+    common += os.environ.get("SV_BUILD_FLAGS", "").split()      # e.g. -DSV_DEBUG_CHECKS (debug variant)
     objs, procs = [], []
     for src in sources():                       # one nvcc per translation unit, in parallel
         obj = os.path.join(objdir, os.path.basename(src) + ".o")

@@ -28,6 +28,15 @@
 #include "sv_internal.h"
 #include "plan.h"
 
+// SV_DEBUG_CHECKS (a debug build, tools/build_variant.py ... -DSV_DEBUG_CHECKS): every
+// shared-memory class access is checked against its tile and every mbarrier wait against a spin
+// limit; a violation traps (the CUDA error fails the calling test).  Zero cost otherwise.
+#ifdef SV_DEBUG_CHECKS
+#define SV_DCHECK(cond) do { if (!(cond)) __trap(); } while (0)
+#else
+#define SV_DCHECK(cond) do { } while (0)
+#endif
+
 namespace svi {
 
 constexpr int kMaxPassGates = 32;            // fire bits: one 32-bit ballot
@@ -160,11 +169,24 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+#ifdef SV_DEBUG_CHECKS
+    // bounded spin: a lost arrive (or a phase mix-up) traps instead of hanging the GPU
+    for (uint64_t it = 0;; ++it) {
+        uint32_t done;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n}" : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+        if (done) break;
+        SV_DCHECK(it < (1ull << 26));
+    }
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
         "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+#endif
 }
 __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -245,6 +267,7 @@ __device__ __forceinline__ void issue_loads(const PP &p, uint64_t t, V *buf, uin
         si->fire = bits;
     }
     __syncwarp();
+    SV_DCHECK(ti.len <= p.LT && ti.len > 0);
     if (lane == 0) mbar_expect_tx(bar, (uint32_t)p.M * ti.len * (uint32_t)sizeof(V));
     __syncwarp();
     for (int m = lane; m < p.M; m += 32)
@@ -288,6 +311,7 @@ __device__ __forceinline__ uint32_t class_e0(uint32_t c, const PassGateP &g, con
 // What one gate needs to decide its classes inside the current tile.
 struct TileGate {
     uint32_t LT, mLT, len, flags;
+    uint32_t tbytes;            // bytes of the tile (debug bound checks)
     uint32_t nins, active;      // hot gate fields, read from the shared-memory descriptor
     Ins1 first;                 // the first digit insertion of the class index
     const uint32_t *lowoff;     // shared memory: run offsets of the run-digit controls
@@ -405,7 +429,10 @@ __device__ __forceinline__ void gate_tile_general(const TileGate &tg, const Pass
         for (int k = 0; k < K; ++k) {
             a[k] = sb + e[k] * (uint32_t)sizeof(V);
 #pragma unroll
-            for (int j = 0; j < D; ++j) x[k][j] = lds2<V>(a[k] + mo[j]);
+            for (int j = 0; j < D; ++j) {
+                SV_DCHECK(e[k] * (uint32_t)sizeof(V) + mo[j] + (uint32_t)sizeof(V) <= tg.tbytes);
+                x[k][j] = lds2<V>(a[k] + mo[j]);
+            }
         }
 #pragma unroll
         for (int i = 0; i < D; ++i) {
@@ -461,7 +488,13 @@ __device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const Pas
         uint32_t a[K];
         V x[K][D];
 #pragma unroll
-        for (int k = 0; k < K; ++k) a[k] = sb + e[k] * (uint32_t)sizeof(V);
+        for (int k = 0; k < K; ++k) {
+            a[k] = sb + e[k] * (uint32_t)sizeof(V);
+#pragma unroll
+            for (int j = 0; j < D; ++j)
+                SV_DCHECK(!((act >> j) & 1) || (e[k] * (uint32_t)sizeof(V) + (mo[j] > so[j] ? mo[j] : so[j]) +
+                                                 (uint32_t)sizeof(V) <= tg.tbytes));
+        }
 #pragma unroll
         for (int j = 0; j < D; ++j) {
             const bool aj = (act >> j) & 1;
@@ -570,7 +603,9 @@ __global__ void __launch_bounds__(NT + kPassExtra, 1) k_gate_pass(const __grid_c
     extern __shared__ __align__(128) unsigned char smem_raw[];
     V *bufs = reinterpret_cast<V *>(smem_raw);
     V *Us = bufs + (size_t)S * TE;                             // the pass's matrices (in V's precision)
-    uint32_t *moffs = reinterpret_cast<uint32_t *>(Us + p.upool);   // per gate: member offsets
+    // per gate: member offsets (16-byte aligned: the gate descriptors after them are read as uint4,
+    // and a complex64 matrix pool may end at an 8-byte boundary)
+    uint32_t *moffs = reinterpret_cast<uint32_t *>((reinterpret_cast<uintptr_t>(Us + p.upool) + 15) & ~(uintptr_t)15);
     uint32_t *soffs = moffs + kMaxPassGates * kMaxDim;               // per gate: sigma-member offsets
     uint32_t *gdesc = soffs + kMaxPassGates * kMaxDim;               // per gate: hot fields (kGDesc words)
     StageInfo *sinfo = reinterpret_cast<StageInfo *>(gdesc + kMaxPassGates * kGDesc);
@@ -656,6 +691,7 @@ __global__ void __launch_bounds__(NT + kPassExtra, 1) k_gate_pass(const __grid_c
             tg.LT = LT;
             tg.mLT = mLT;
             tg.len = len;
+            tg.tbytes = (uint32_t)p.M * LT * (uint32_t)sizeof(V);
             tg.flags = h0.w;
             tg.nins = h1.x;
             tg.active = h1.z;
@@ -810,6 +846,7 @@ __device__ __forceinline__ void run_stage(const StageParams &p, const StageRec &
         tdiv(e, LT, mLT, l);
         if (ragged && l >= len) continue;
         const uint32_t base = sbase + e * (uint32_t)sizeof(V);
+        SV_DCHECK(e + (uint32_t)(DA - 1) * sr.sa + (uint32_t)(DB - 1) * sr.sb < (uint32_t)p.M * LT);
         V x[DA][DB];
 #pragma unroll
         for (int ja = 0; ja < DA; ++ja)
@@ -1194,7 +1231,7 @@ cudaError_t launch_pass_t(const PassParams &p, cudaStream_t st, const LaunchCfg 
     const size_t smem = (size_t)S * TE * sizeof(V) + (size_t)kPoolC * sizeof(V) +
                         (size_t)2 * kMaxPassGates * kMaxDim * sizeof(uint32_t) +
                         (size_t)kMaxPassGates * kGDesc * sizeof(uint32_t) +
-                        (size_t)S * sizeof(StageInfo) + (size_t)3 * S * sizeof(uint64_t) + 16 + 32 * 16;
+                        (size_t)S * sizeof(StageInfo) + (size_t)3 * S * sizeof(uint64_t) + 16 + 16 + 32 * 16;
     static LaunchAttr attr;
     const int dv = current_device_slot();
     if (attr.configured[dv] < smem) {
@@ -1408,15 +1445,14 @@ cudaError_t launch_stage(const StageParams &p, cudaStream_t st, const LaunchCfg 
 
 cudaError_t run_pass(const Register &reg, const std::vector<GateSpec> &gates, const PassPlan &pp, double2 *psi,
                      cudaStream_t st, const LaunchCfg &cfg, bool *handled, PassWork *work) {
-    // register-blocked stages (k_gate_stage) unless disabled or the pass does not fit them
-    if (cfg.pass_kernel != 1) {
+    // register-blocked stages (k_gate_stage) when selected and the pass fits them
+    if (cfg.pass_kernel == 1) {
         static thread_local StageParams sp;   // ~27 KB; parameters are copied at launch
         if (build_stage_pass(reg, gates, pp, psi, cfg.pass_tile, sp, work) &&
             !(cfg.c64 && (sp.L % 2 != 0 || sp.LT % 2 != 0))) {
             *handled = true;
             return launch_stage(sp, st, cfg);
         }
-        if (cfg.pass_kernel == 2) { *handled = false; return cudaSuccess; }
     }
     static thread_local PassParams p;   // ~23 KB; parameters are copied at launch
     *handled = build_pass(reg, gates, pp, psi, cfg.pass_tile, p, work);

@@ -69,7 +69,7 @@ void default_cfg(LaunchCfg &c, int device) {
     c.pass_groups = 2;         // two consumer groups ping-pong over tiles
     c.shard_swap = 1;          // qubit remapping for gates on sharded qubits
     c.pass_search = 1;         // in-tile set chosen by subset search (c4 29 -> 22 passes)
-    c.pass_kernel = 0;         // register-blocked stages (k_gate_stage) when the pass fits them
+    c.pass_kernel = 0;         // per-gate pass kernel (stages measured slower on c3/c4: profiles/r02)
 }
 
 }  // namespace
@@ -551,7 +551,7 @@ sv_status sv_set_option(sv_handle h, int32_t option, int64_t value) {
             h->cfg.pass_search = value != 0;
             return SV_OK;
         case SV_OPT_PASS_KERNEL:
-            if (value < 0 || value > 2) return fail(SV_ERR_INVALID_ARG, "pass kernel 0..2");
+            if (value < 0 || value > 1) return fail(SV_ERR_INVALID_ARG, "pass kernel 0 or 1");
             h->cfg.pass_kernel = (int)value;
             return SV_OK;
         case SV_OPT_PLAN_CACHE:

@@ -28,9 +28,10 @@ def P():
 
 
 def run_gpu(P, dims, gates, psi0=None, kernel=0, fuse=False, graph=False, per_gate=False, block=False,
-            pass_tile=None, pass_cfg=None):
+            pass_tile=None, pass_cfg=None, pass_kernel=0):
     with P.State(dims) as st:
         st.set_option(P.sv.SV_OPT_KERNEL, kernel)
+        st.set_option(P.sv.SV_OPT_PASS_KERNEL, pass_kernel)
         if pass_tile:
             st.set_option(P.sv.SV_OPT_PASS_TILE, pass_tile)
         if pass_cfg:
@@ -515,6 +516,49 @@ def test_block_passes_labelled_bit_exact(P, pass_cfg):
     ref = O2.run(dims, gates, psi0)
     tile = {2: 6144, 3: 4096}.get(pass_cfg[2], 2048)
     got, _, launched = run_gpu(P, dims, gates, psi0, block=True, pass_tile=tile, pass_cfg=pass_cfg)
+    assert launched < len(gates)
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("pass_cfg", [(256, 1, 3), (384, 2, 3), (512, 2, 3)])
+@pytest.mark.parametrize("pass_tile", [4096, 1024, 256])
+def test_stage_kernel_random_sweep(P, pass_tile, pass_cfg):
+    """The register-blocked stage kernel (SV_OPT_PASS_KERNEL = 1): stages of gates on digit pairs,
+    passive partners, controls on the partner digit / in-tile digits / run digits / outside the
+    tile, diagonal, cyclic-shift and general gates, ragged tiles; against O-2."""
+    rng = np.random.default_rng(pass_tile + 7)
+    for s in range(20):
+        n = int(rng.integers(2, 9))
+        dims = [int(x) for x in rng.integers(2, 6, size=n)]
+        while np.prod(dims) > 3_000_000:
+            dims = dims[:-1]
+        _, gates = random_circuit(80_000 + s, dims, 80, max_ctrl=3)
+        psi0 = random_state(int(np.prod(dims)), s)
+        ref = O2.run(dims, gates, psi0)
+        got, _, _ = run_gpu(P, dims, gates, psi0, block=True, pass_tile=pass_tile, pass_cfg=pass_cfg, pass_kernel=1)
+        assert np.max(np.abs(got - ref)) <= 1e-12, (dims, s)
+
+
+def test_stage_kernel_labelled_bit_exact(P):
+    """Permutations through the stage kernel (cyclic shifts as register moves, other
+    permutations through the general rule with exact 0/1 entries): bit-exact against O-2."""
+    rng = np.random.default_rng(5)
+    dims = config_circuit(4, ngates=0, nqubits=4)[0]
+    n, D = len(dims), int(np.prod(dims))
+    gates = []
+    for _ in range(150):
+        t = int(rng.integers(n))
+        others = [q for q in range(n) if q != t]
+        nc = int(rng.integers(0, 3))
+        ctrl = tuple(int(c) for c in rng.choice(others, size=nc, replace=False))
+        vals = tuple(int(rng.integers(dims[c])) for c in ctrl)
+        U = shift_x(dims[t], int(rng.integers(1, dims[t]))) if rng.random() < 0.5 else \
+            permutation_matrix(rng.permutation(dims[t]))
+        gates.append(Gate(t, ctrl, vals, U))
+    psi0 = labelled_state(0, D)
+    ref = O2.run(dims, gates, psi0)
+    got, _, launched = run_gpu(P, dims, gates, psi0, block=True, pass_tile=4096, pass_cfg=(384, 2, 3),
+                               pass_kernel=1)
     assert launched < len(gates)
     assert np.array_equal(got, ref)
 

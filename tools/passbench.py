@@ -28,7 +28,7 @@ def main():
     ap.add_argument("--reps", type=int, default=1)
     ap.add_argument("--search", type=int, default=1, help="SV_OPT_PASS_SEARCH (in-tile set search)")
     ap.add_argument("--skip-noblock", action="store_true", help="do not time the single-gate mode")
-    ap.add_argument("--pass-kernel", type=int, default=0, help="SV_OPT_PASS_KERNEL: 0 auto, 1 per-gate, 2 stages")
+    ap.add_argument("--pass-kernel", type=int, default=0, help="SV_OPT_PASS_KERNEL: 0 per-gate, 1 register-blocked stages")
     args = ap.parse_args()
     import torch
     import paper_2410_17876_b200 as P

@@ -47,7 +47,7 @@ def main():
     # per-gate pass kernel: (threads, groups, stages)
     for nt, g, s in ((256, 1, 2), (512, 2, 3), (512, 4, 4), (384, 2, 2)):
         with P.State(dims) as st:
-            st.set_option(S.SV_OPT_PASS_KERNEL, 1)
+            st.set_option(S.SV_OPT_PASS_KERNEL, 0)
             st.set_option(S.SV_OPT_PASS_TILE, 256)
             st.set_option(S.SV_OPT_PASS_THREADS, nt)
             st.set_option(S.SV_OPT_PASS_GROUPS, g)
@@ -57,7 +57,7 @@ def main():
             check(f"k_gate_pass nt={nt} groups={g} stages={s}", st.amplitudes(), ref)
     for nt, g in ((256, 1), (384, 2)):
         with P.State(dims) as st:
-            st.set_option(S.SV_OPT_PASS_KERNEL, 2)
+            st.set_option(S.SV_OPT_PASS_KERNEL, 1)
             st.set_option(S.SV_OPT_PASS_TILE, 256)
             st.set_option(S.SV_OPT_PASS_THREADS, nt)
             st.set_option(S.SV_OPT_PASS_GROUPS, g)
