@@ -337,6 +337,20 @@ SV_API sv_status sv_shard_plan(const int32_t *dims, int32_t n, int32_t nranks, i
                         int32_t target, const int32_t *ctrl, const int32_t *ctrl_vals,
                         int32_t nctrl, int32_t *action, int32_t *partner, int32_t *beta);
 
+/* Host-only (no GPU): the sharded schedule rank `rank` of `nranks` runs for a circuit — the same
+ * planner as sv_apply_circuit on a sharded handle (rules ii-vi of SURVEY.md §8(e) / DESIGN.md §9:
+ * sharded-control predicates, local phases, rank relabelling, qubit remapping when shard_swap != 0,
+ * pairwise exchanges), followed by the layout restore a readback performs.  For CPU tests that
+ * replay it on per-rank slices over gloo.  out (cap doubles) receives, per step,
+ * [kind (0 local gates on this rank's slice, 1 qubit swap, 2 exchange), partner, beta, k, j, ngates]
+ * and per gate [target, nctrl, ctrl..., vals..., d, U as re/im pairs, row-major]; *out_len = the
+ * doubles written (or needed: SV_ERR_INVALID_ARG if cap is too small); out_lrank[nranks] = the
+ * final logical slice of every physical rank.  Gate targets/controls are local digit positions
+ * (the sharded controls of local gates already resolved).  flags as sv_apply_circuit. */
+SV_API sv_status sv_shard_schedule(const int32_t *dims, int32_t n, int32_t nranks, int32_t rank,
+                                   const sv_gate *gates, int64_t ngates, uint32_t flags, int32_t shard_swap,
+                                   double *out, int64_t cap, int64_t *out_len, int32_t *out_lrank);
+
 SV_API const char *sv_version(void);
 
 /* ---- sparse states (the paper's "Our Method (Sparse)") --

@@ -545,13 +545,16 @@ __device__ __noinline__ void gate_tile_generic(const TileGate tg, const PassGate
     }
 }
 
-// classes per thread iteration (registers: 4*K*D for the gathered classes), by thread count:
-// 256 threads may use up to ~200 registers, 384 up to 152, 512 up to 120
+// classes per thread iteration (registers: 4*K*D for the gathered classes), by thread count.
+// With 512+ compute threads (96 registers at 18 warps: the per-SMSP register file holds 5 warps)
+// two classes for d <= 3 and one for d = 4, 5 measured best (c4 1816 -> 1628 ms, c3 439 -> 394 ms
+// against the earlier 4/3/2/2, same box; profiles/r02/ab/r02m_ksweep, r02n_ksweep2): fewer
+// in-flight classes, no spills.  384 threads (128 registers) keep the larger batches.
 template <int D, int NT> struct PassK { static constexpr int value = 1; };
-template <int NT> struct PassK<2, NT> { static constexpr int value = 4; };
-template <int NT> struct PassK<3, NT> { static constexpr int value = NT >= 512 ? 3 : 4; };
-template <int NT> struct PassK<4, NT> { static constexpr int value = NT >= 512 ? 2 : 3; };
-template <int NT> struct PassK<5, NT> { static constexpr int value = NT >= 384 ? 2 : 3; };
+template <int NT> struct PassK<2, NT> { static constexpr int value = NT >= 512 ? 2 : 4; };
+template <int NT> struct PassK<3, NT> { static constexpr int value = NT >= 512 ? 2 : 4; };
+template <int NT> struct PassK<4, NT> { static constexpr int value = NT >= 512 ? 1 : 3; };
+template <int NT> struct PassK<5, NT> { static constexpr int value = NT >= 512 ? 1 : (NT >= 384 ? 2 : 3); };
 
 // NT = compute threads of the CTA (sets the register budget), NTG = threads of one consumer
 // group (the class stride)
@@ -1255,6 +1258,8 @@ cudaError_t launch_pass(const PassParams &p, cudaStream_t st, const LaunchCfg &c
     if (cfg.c64) return launch_pass_t<512, 2, float2>(p, st, cfg);   // complex64: one configuration
     int G = cfg.pass_groups;                      // one stage per group at least
     while (G > 1 && cfg.pass_stages < G) G /= 2;
+    if (cfg.pass_threads >= 960) return launch_pass_t<960, 2, double2>(p, st, cfg);   // 32 warps, 64 registers
+    if (cfg.pass_threads >= 768) return launch_pass_t<768, 2, double2>(p, st, cfg);   // 26 warps, 72 registers
     if (cfg.pass_threads >= 512) {
         if (G >= 4) return launch_pass_t<512, 4, double2>(p, st, cfg);
         if (G == 2) return launch_pass_t<512, 2, double2>(p, st, cfg);

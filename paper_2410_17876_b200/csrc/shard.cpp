@@ -133,7 +133,16 @@ struct IpcShm {
 };
 static_assert(std::atomic<uint32_t>::is_always_lock_free, "process-shared atomics");
 
-enum Transport { kLoopback = 0, kNccl = 1, kIpc = 2 };
+enum Transport { kLoopback = 0, kNccl = 1, kIpc = 2, kDryRun = 3 };
+
+// Dry run (sv_shard_schedule, host only): the schedule of one rank recorded instead of executed —
+// the local gate lists its slice runs, and the cross-rank steps with their partners — so a CPU
+// test can replay it on numpy slices over gloo (tests/test_shard_gloo.py).
+struct DryOp {
+    int kind;                    // 0 local gates, 1 qubit swap (rule vi), 2 exchange (rule iii)
+    int partner, beta, k, j;     // swap: local position k <-> sharded position j; exchange: partner, beta
+    std::vector<GateSpec> gates; // local: the gates (local positions); exchange: the gate
+};
 
 double comm_timeout_s() {
     const char *e = getenv("SV_COMM_TIMEOUT_S");
@@ -151,6 +160,7 @@ struct ShardCtx {
     std::vector<double2 *> peer;
     IpcShm *shm = nullptr;
     char shm_name[129] = {0};      // unlinked once every rank has attached (or on failure)
+    std::vector<DryOp> dry;        // kDryRun: the recorded schedule
     int red_parity = 0;
     std::vector<double2 *> slices; // loopback: P slices (slices[0] is h->psi); NCCL: {h->psi}
     double2 *stage[2] = {nullptr, nullptr};
@@ -163,6 +173,7 @@ struct ShardCtx {
     std::vector<int> lrank, prank; // physical rank -> logical slice index, and its inverse
     std::vector<int> pos_of, log_at; // logical qudit -> digit position, and its inverse
     bool loopback() const { return rank < 0; }
+    bool dryrun() const { return transport == kDryRun; }
     void identity_map(int n) {
         lrank.resize(P);
         prank.resize(P);
@@ -415,6 +426,11 @@ sv_status swap_qubits(sv_handle h, int k, int j) {
                 out.push_back({m + (uint64_t)v * b + o, (b - o < c->chunk) ? b - o : c->chunk});
         return out;
     };
+    if (c->dryrun()) {
+        const int l = c->lrank[c->rank], beta = (l >> j) & 1;
+        c->dry.push_back({1, c->prank[l ^ (1 << j)], beta, k, j, {}});
+        ++h->exchanges;
+    }
     if (c->transport == kIpc) {                  // fused: half of the pair's swap space per rank
         sv_status s = ipc_fence(h);
         if (s != SV_OK) return s;
@@ -434,7 +450,7 @@ sv_status swap_qubits(sv_handle h, int k, int j) {
         s = ipc_fence(h);
         if (s != SV_OK) return s;
     }
-    for (int r : (c->transport == kIpc ? std::vector<int>{} : ranks_of(c))) {
+    for (int r : (c->transport == kIpc || c->dryrun() ? std::vector<int>{} : ranks_of(c))) {
         const int l = c->lrank[r];
         const int beta = (l >> j) & 1;
         const int p = c->prank[l ^ (1 << j)];
@@ -570,6 +586,7 @@ sv_status apply_phys(sv_handle h, const GateSpec &g) {
             GateSpec pl;
             if (!fires_on(g.ctrl, h->local.n, c->lrank[r]) || !phase_local(h->local, g, c->lrank[r], &pl))
                 continue;
+            if (c->dryrun()) { c->dry.push_back({0, r, 0, 0, 0, {pl}}); continue; }
             GatePlan p;
             sv_status s = plan_gate(h->local, pl, false, &p, err);
             if (s == SV_OK) s = launch_on(h, p, slice_of(c, r));
@@ -580,6 +597,7 @@ sv_status apply_phys(sv_handle h, const GateSpec &g) {
     if (kind == SK_RELABEL) {
         for (const auto &rs : relabel(c, g, h->local.n)) {
             if (!owns(c, rs.first)) continue;
+            if (c->dryrun()) { c->dry.push_back({0, rs.first, 0, 0, 0, {scale_gate(h->local, rs.second)}}); continue; }
             GatePlan p;
             sv_status s = plan_gate(h->local, scale_gate(h->local, rs.second), false, &p, err);
             if (s == SV_OK) s = launch_on(h, p, slice_of(c, rs.first));
@@ -604,6 +622,7 @@ sv_status apply_phys(sv_handle h, const GateSpec &g) {
         if (s != SV_OK) return s;
         if (a.action == 1) continue;
         if (a.action == 0) {
+            if (c->dryrun()) { c->dry.push_back({0, r, 0, 0, 0, {gl}}); continue; }
             GatePlan p;
             s = plan_gate(h->local, gl, false, &p, err);
             if (s != SV_OK) return s;
@@ -614,6 +633,11 @@ sv_status apply_phys(sv_handle h, const GateSpec &g) {
         const int lpartner = a.partner;
         a.partner = c->prank[lpartner];
         const uint64_t L = h->local.D;
+        if (c->dryrun()) {
+            c->dry.push_back({2, a.partner, a.beta, 0, 0, {g}});
+            ++h->exchanges;
+            continue;
+        }
         if (c->loopback()) {
             double2 *mine = c->slices[r], *theirs = c->slices[a.partner];
             s = exchange_fused(h, g, a.beta ? theirs : mine, a.beta ? mine : theirs, 0, L);
@@ -669,6 +693,11 @@ sv_status shard_apply_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_
             const uint32_t local_flags = flags & (SV_FUSE | SV_BLOCK);
             for (size_t i = 0; i < ranks.size(); ++i) {
                 if (runs[i].empty()) continue;
+                if (h->shard->dryrun()) {
+                    h->shard->dry.push_back({0, ranks[i], 0, 0, 0, runs[i]});
+                    runs[i].clear();
+                    continue;
+                }
                 sv_status s = run_local_circuit(h, runs[i], local_flags, slice_of(h->shard, ranks[i]));
                 if (s != SV_OK) return s;
                 runs[i].clear();
@@ -1083,6 +1112,75 @@ sv_status sv_ipc_unique_id(void *out128) {
 sv_status sv_create_sharded_ipc(const int32_t *dims, int32_t n, sv_dtype dt, int32_t rank, int32_t nranks,
                                 const void *ipc_id, int device, void *cuda_stream, sv_handle *out) {
     return create_sharded(dims, n, dt, rank, nranks, kIpc, ipc_id, device, cuda_stream, out);
+}
+
+// Host only: the sharded schedule of one rank (sv_shard_schedule in sv.h).
+sv_status sv_shard_schedule(const int32_t *dims, int32_t n, int32_t nranks, int32_t rank, const sv_gate *gates,
+                            int64_t ngates, uint32_t flags, int32_t shard_swap, double *out, int64_t cap,
+                            int64_t *out_len, int32_t *out_lrank) {
+    if (!out_len || !out_lrank || (cap > 0 && !out)) return fail_msg(SV_ERR_INVALID_ARG, "null output");
+    if (nranks < 2 || (nranks & (nranks - 1)) || rank < 0 || rank >= nranks)
+        return fail_msg(SV_ERR_INVALID_ARG, "nranks = 2^s >= 2, 0 <= rank < nranks");
+    if (ngates < 0 || (ngates > 0 && !gates)) return fail_msg(SV_ERR_INVALID_ARG, "bad gate list");
+    sv_state_s hs;
+    sv_handle h = &hs;
+    std::string *err = err_slot();
+    sv_status s = make_register(dims, n, &h->reg, err);
+    if (s != SV_OK) return s;
+    int sh = 0;
+    while ((1 << sh) < nranks) ++sh;
+    if (sh >= n) return fail_msg(SV_ERR_UNSUPPORTED, "need at least one local qudit");
+    for (int k = n - sh; k < n; ++k)
+        if (dims[k] != 2) return fail_msg(SV_ERR_UNSUPPORTED, "sharded digits must be qubits");
+    s = make_register(dims, n - sh, &h->local, err);
+    if (s != SV_OK) return s;
+    std::vector<GateSpec> specs;
+    for (int64_t i = 0; i < ngates; ++i) {
+        const sv_gate &g = gates[i];
+        s = validate_gate(h->reg, g.target, g.ctrl, g.ctrl_vals, g.nctrl, g.U, err);
+        if (s != SV_OK) return s;
+        GateSpec q;
+        q.target = g.target;
+        q.d = h->reg.dims[g.target];
+        for (int k = 0; k < g.nctrl; ++k) q.ctrl.push_back({g.ctrl[k], g.ctrl_vals[k]});
+        q.U.resize((size_t)q.d * q.d);
+        for (int k = 0; k < q.d * q.d; ++k) q.U[k] = make_double2(g.U[2 * k], g.U[2 * k + 1]);
+        specs.push_back(std::move(q));
+    }
+    ShardCtx c;
+    c.P = nranks;
+    c.s = sh;
+    c.rank = rank;
+    c.transport = kDryRun;
+    c.identity_map(n);
+    h->shard = &c;
+    h->cfg.shard_swap = shard_swap ? 1 : 0;
+    h->cfg.pass_merge = 1;
+    h->elem = sizeof(double2);
+    s = shard_apply_circuit(h, specs, flags);
+    if (s == SV_OK) s = restore_layout(h);          // what a readback does first
+    h->shard = nullptr;                              // hs is a stack object: nothing to free
+    if (s != SV_OK) return s;
+    // serialise: per op [kind, partner, beta, k, j, ngates] then per gate
+    // [target, nctrl, ctrl..., vals..., d, re/im of U row-major]
+    std::vector<double> buf;
+    for (const DryOp &o : c.dry) {
+        buf.insert(buf.end(), {(double)o.kind, (double)o.partner, (double)o.beta, (double)o.k, (double)o.j,
+                               (double)o.gates.size()});
+        for (const GateSpec &g : o.gates) {
+            buf.push_back(g.target);
+            buf.push_back((double)g.ctrl.size());
+            for (const auto &cc : g.ctrl) buf.push_back(cc.q);
+            for (const auto &cc : g.ctrl) buf.push_back(cc.v);
+            buf.push_back(g.d);
+            for (const double2 &u : g.U) { buf.push_back(u.x); buf.push_back(u.y); }
+        }
+    }
+    *out_len = (int64_t)buf.size();
+    for (int r = 0; r < nranks; ++r) out_lrank[r] = c.lrank[r];
+    if ((int64_t)buf.size() > cap) return fail_msg(SV_ERR_INVALID_ARG, "output buffer too small (see *out_len)");
+    std::memcpy(out, buf.data(), buf.size() * sizeof(double));
+    return SV_OK;
 }
 
 }  // extern "C"

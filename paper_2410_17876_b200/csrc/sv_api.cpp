@@ -534,7 +534,8 @@ sv_status sv_set_option(sv_handle h, int32_t option, int64_t value) {
             h->cfg.pass_stages = (int)value;
             return SV_OK;
         case SV_OPT_PASS_THREADS:
-            if (value != 256 && value != 384 && value != 512) return fail(SV_ERR_INVALID_ARG, "pass threads 256, 384 or 512");
+            if (value != 256 && value != 384 && value != 512 && value != 768 && value != 960)
+                return fail(SV_ERR_INVALID_ARG, "pass threads 256, 384, 512, 768 or 960");
             h->cfg.pass_threads = (int)value;
             return SV_OK;
         case SV_OPT_PASS_GROUPS:

@@ -122,6 +122,8 @@ _sig("sv_sparse_entries", [_h, C.c_uint64, _u64p, _dp, C.POINTER(C.c_uint64)])
 _sig("sv_sparse_launches", [_h, C.POINTER(C.c_uint64)])
 _sig("sv_block_plan", [_i32p, C.c_int32, C.POINTER(sv_gate), C.c_int64, C.c_int64, C.POINTER(C.c_int64),
                        C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)])
+_sig("sv_shard_schedule", [_i32p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(sv_gate), C.c_int64, C.c_uint32,
+                           C.c_int32, _dp, C.c_int64, C.POINTER(C.c_int64), _i32p])
 _sig("sv_block_plan_ex", [_i32p, C.c_int32, C.POINTER(sv_gate), C.c_int64, C.c_int64, C.c_int32, C.c_int32,
                           C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                           C.POINTER(C.c_int64)])
@@ -133,7 +135,7 @@ EXPORTS = ["sv_create", "sv_create_ex", "sv_create_sharded", "sv_nccl_unique_id"
            "sv_enumerate_fibres", "sv_fuse_plan", "sv_merge_plan", "sv_shard_plan", "sv_version", "sv_profile_read", "sv_block_plan",
            "sv_sparse_create", "sv_sparse_destroy", "sv_sparse_reset", "sv_sparse_apply_gate",
            "sv_sparse_apply_circuit", "sv_sparse_nnz", "sv_sparse_entries", "sv_sparse_launches",
-           "sv_block_plan_ex"]
+           "sv_block_plan_ex", "sv_shard_schedule"]
 
 
 def _check(rc: int):
@@ -445,3 +447,41 @@ def shard_plan(dims, nranks, rank, target, ctrl=(), vals=()):
     _check(_lib.sv_shard_plan(d.ctypes.data_as(_i32p), d.size, int(nranks), int(rank), int(target),
                               _p(c, _i32p), _p(v, _i32p), int(c.size), C.byref(a), C.byref(p), C.byref(b)))
     return a.value, p.value, b.value
+
+
+def shard_schedule(dims, nranks: int, rank: int, gates, block: bool = True, fuse: bool = False, swap: bool = True):
+    """Host-only sharded schedule of one rank (sv_shard_schedule): (ops, final lrank).  ops are
+    dicts {kind: 'local'|'swap'|'exchange', partner, beta, k, j, gates: [(target, ctrl, vals, U)]}."""
+    gates = list(gates)
+    ga = _GateArray(gates)
+    d = _i32(dims)
+    flags = (SV_BLOCK if block else 0) | (SV_FUSE if fuse else 0) | SV_NO_CHECK
+    n_out = C.c_int64()
+    lrank = np.zeros(nranks, np.int32)
+    cap = 1 << 16
+    while True:
+        buf = np.zeros(cap, np.float64)
+        rc = _lib.sv_shard_schedule(d.ctypes.data_as(_i32p), d.size, int(nranks), int(rank), ga.arr, ga.n, flags,
+                                    1 if swap else 0, buf.ctypes.data_as(_dp), cap, C.byref(n_out),
+                                    lrank.ctypes.data_as(_i32p))
+        if rc != 0 and n_out.value > cap:
+            cap = int(n_out.value)
+            continue
+        _check(rc)
+        break
+    ops, i = [], 0
+    kinds = {0: "local", 1: "swap", 2: "exchange"}
+    while i < n_out.value:
+        kind, partner, beta, k, j, ng = (int(x) for x in buf[i:i + 6])
+        i += 6
+        gl = []
+        for _ in range(ng):
+            t, nc = int(buf[i]), int(buf[i + 1])
+            i += 2
+            ctrl = tuple(int(x) for x in buf[i:i + nc]); i += nc
+            vals = tuple(int(x) for x in buf[i:i + nc]); i += nc
+            dd = int(buf[i]); i += 1
+            U = buf[i:i + 2 * dd * dd].view(np.complex128).reshape(dd, dd).copy(); i += 2 * dd * dd
+            gl.append((t, ctrl, vals, U))
+        ops.append({"kind": kinds[kind], "partner": partner, "beta": beta, "k": k, "j": j, "gates": gl})
+    return ops, [int(x) for x in lrank]
