@@ -323,7 +323,7 @@ SV_API sv_status sv_block_plan(const int32_t *dims, int32_t n, const sv_gate *ga
                                int64_t *out_tile, int64_t *out_npasses);
 /* As sv_block_plan with the planner's knobs: at most max_gates (1..32) gates per pass, `window`
  * gates scanned ahead, search != 0 = the in-tile set search (the SV_BLOCK defaults are 32, 256, 1;
- * sv_block_plan uses 24, 64, 0). */
+ * sv_block_plan uses 24, 64, 1). */
 SV_API sv_status sv_block_plan_ex(const int32_t *dims, int32_t n, const sv_gate *gates, int64_t ngates,
                                   int64_t tile_cap, int32_t max_gates, int32_t window, int32_t search,
                                   int64_t *out_order, int64_t *out_pass, int64_t *out_tile,

@@ -717,7 +717,7 @@ sv_status sv_merge_plan(const int32_t *dims, int32_t n, const sv_gate *gates, in
 sv_status sv_block_plan(const int32_t *dims, int32_t n, const sv_gate *gates, int64_t ngates,
                         int64_t tile_cap, int64_t *out_order, int64_t *out_pass, int64_t *out_tile,
                         int64_t *out_npasses) {
-    return sv_block_plan_ex(dims, n, gates, ngates, tile_cap, 24, 64, 0, out_order, out_pass, out_tile,
+    return sv_block_plan_ex(dims, n, gates, ngates, tile_cap, 24, 64, 1, out_order, out_pass, out_tile,
                             out_npasses);
 }
 

@@ -362,7 +362,7 @@ def merge_plan(dims, gates, window: int = 64):
 def block_plan(dims, gates, tile_cap: int = 4096, max_gates: int | None = None, window: int = 64,
                search: bool = False):
     """Host pass planner: (order, pass_id, tiles) — gate indices in application order.
-    max_gates=None: sv_block_plan (24 gates, window 64, no search); else sv_block_plan_ex."""
+    max_gates=None: sv_block_plan (24 gates, window 64, search); else sv_block_plan_ex."""
     gates = list(gates)
     ga = _GateArray(gates)
     n = max(1, len(gates))
