@@ -162,6 +162,16 @@ static_assert(sizeof(StageParams) <= 32764, "kernel parameter space (32 KB on sm
 namespace {
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint4 lds_u128(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
@@ -318,6 +328,8 @@ struct TileGate {
     const uint32_t *moff;       // shared memory: tile offset of class member j (j st, or the
                                 //   two-digit offset of a pair gate)
     const uint32_t *soff;       // shared memory: offset of member sigma(j) (monomial gates)
+    uint32_t moff_s, soff_s;    // the same two tables as shared-window addresses (LDS, not generic LD)
+    uint32_t lowoff_s;          // lowoff as a shared-window address
 };
 
 // whether class e0 exists (ragged last tile of a run) and its in-tile controls hold
@@ -330,13 +342,13 @@ __device__ __forceinline__ bool class_ok(const TileGate &tg, const PassGateP &g,
         for (int k = 0; k < g.nctrl; ++k) {
             const PassCtrl &cc = g.c[k];
             if (cc.cls == 3) {
-                const uint32_t x = tg.lowoff[k], t = x & kCls3Mask, mode = x >> 30;
+                const uint32_t x = lds_u32(tg.lowoff_s + 4u * k), t = x & kCls3Mask, mode = x >> 30;
                 ok = ok && (mode == 1 ? l < t : (mode == 2 && l >= t));
                 continue;
             }
             if (cc.cls != 1) continue;
             uint32_t r, r2;
-            fastdiv32(tg.lowoff[k] + l, cc.M, cc.mM, r);
+            fastdiv32(lds_u32(tg.lowoff_s + 4u * k) + l, cc.M, cc.mM, r);
             const uint32_t q = fastdiv32(r, cc.w, cc.mw, r2);
             fastdiv32(q, cc.d, cc.md, r2);
             ok = ok && (r2 == cc.v);
@@ -405,7 +417,7 @@ __device__ __forceinline__ void gate_tile_general(const TileGate &tg, const Pass
     // far as the compiler knows, so it keeps them in registers)
     uint32_t mo[D];
 #pragma unroll
-    for (int j = 0; j < D; ++j) mo[j] = tg.moff[j] * (uint32_t)sizeof(V);
+    for (int j = 0; j < D; ++j) mo[j] = lds_u32(tg.moff_s + 4u * j) * (uint32_t)sizeof(V);
     const uint32_t sb = smem_u32(buf);
     const Ins1 first = tg.first;
     const bool more = tg.nins > 1;
@@ -468,8 +480,8 @@ __device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const Pas
     uint32_t so[D], mo[D];
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-        so[j] = tg.soff[j] * (uint32_t)sizeof(V);
-        mo[j] = tg.moff[j] * (uint32_t)sizeof(V);
+        so[j] = lds_u32(tg.soff_s + 4u * j) * (uint32_t)sizeof(V);
+        mo[j] = lds_u32(tg.moff_s + 4u * j) * (uint32_t)sizeof(V);
     }
     const uint32_t sb = smem_u32(buf);
 #pragma unroll 1
@@ -684,12 +696,14 @@ __global__ void __launch_bounds__(NT + kPassExtra, 1) k_gate_pass(const __grid_c
         const uint32_t len = si.ti.len;
         const uint32_t fire = si.fire;
         const uint32_t LT = p.LT, mLT = p.mLT;
+        const uint32_t gdesc_s = smem_u32(gdesc);
         for (int gi = 0; gi < p.ngates; ++gi) {
             if (!((fire >> gi) & 1)) continue;          // out-of-tile control unmet: uniform skip
             const PassGateP &g = p.g[gi];               // cold fields only (controls, more insertions)
-            const uint4 h0 = *reinterpret_cast<const uint4 *>(gdesc + gi * kGDesc);       // d, kind, ncls, flags
-            const uint4 h1 = *reinterpret_cast<const uint4 *>(gdesc + gi * kGDesc + 4);   // nins, uoff, active, s
-            const uint4 h2 = *reinterpret_cast<const uint4 *>(gdesc + gi * kGDesc + 8);   // m, sd, ps
+            const uint32_t ga = gdesc_s + (uint32_t)(gi * kGDesc) * 4u;
+            const uint4 h0 = lds_u128(ga);         // d, kind, ncls, flags
+            const uint4 h1 = lds_u128(ga + 16u);   // nins, uoff, active, s
+            const uint4 h2 = lds_u128(ga + 32u);   // m, sd, ps
             TileGate tg;
             tg.LT = LT;
             tg.mLT = mLT;
@@ -702,6 +716,9 @@ __global__ void __launch_bounds__(NT + kPassExtra, 1) k_gate_pass(const __grid_c
             tg.lowoff = si.lowoff[gi];
             tg.moff = moffs + gi * kMaxDim;
             tg.soff = soffs + gi * kMaxDim;
+            tg.moff_s = smem_u32(tg.moff);
+            tg.lowoff_s = smem_u32(tg.lowoff);
+            tg.soff_s = smem_u32(tg.soff);
             const bool needck = h0.w != 0 || len < LT;
             const V *U = Us + h1.y;
             const uint32_t ncls = h0.z;
