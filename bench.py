@@ -504,6 +504,7 @@ def main():
                  "nvlink_bytes_per_step_max_rank": allreduce_max(nvl_step),
                  "cross_rank_kernels_per_step": prof.comm_launches / args.steps,
                  "cross_rank_ms_per_step": prof.comm_ms / args.steps,
+                 "cross_rank_nvlink_gbs": (prof.comm_nvlink_bytes / (prof.comm_ms / 1e3) / 1e9) if prof.comm_ms else None,
                  "pairwise_peak": nvl_peak,
                  "bw_nvlink_gbs_used": bw_nvl,
                  "bw_nvlink_source": "in-run pairwise probe" if nvl_peak else "B200_PROFILING.md peer copy 770 GB/s",

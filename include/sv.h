@@ -199,7 +199,9 @@ typedef struct {
     void *device_ptr;        /* the device statevector (local slice)                    */
     void *cuda_stream;
     uint64_t kernel_launches;/* number of this library's kernels launched so far        */
-    uint64_t exchanges;      /* sharded: pairwise exchanges performed                    */
+    uint64_t exchanges;      /* sharded: cross-rank steps performed (exchanges and qubit remaps;
+                                loopback counts slice pairs)                                */
+    uint64_t overlapped;     /* sharded: qubit remaps overlapped with a local run (SV_OPT_SHARD_OVERLAP) */
 } sv_info;
 
 SV_API sv_status sv_get_info(sv_handle h, sv_info *out);
@@ -212,11 +214,11 @@ SV_API sv_status sv_get_info(sv_handle h, sv_info *out);
 #define SV_OPT_PROFILE      5   /* 1 = bracket every gate kernel with CUDA events on the handle's
                                    stream (read back with sv_profile_read)                        */
 #define SV_OPT_PASS_TILE    6   /* amplitudes per shared-memory tile of SV_BLOCK passes (<= 8192)  */
-#define SV_OPT_PASS_STAGES  7   /* shared-memory ring stages of the pass kernel (2..6)             */
+#define SV_OPT_PASS_STAGES  7   /* shared-memory ring stages of the pass kernel (2..12)            */
 #define SV_OPT_PASS_THREADS 8   /* compute threads per CTA of the pass kernel (256, 384 or 512)    */
 #define SV_OPT_PASS_GATES   9   /* max gates applied per pass (1..32)                              */
 #define SV_OPT_PASS_GROUPS 10   /* consumer warp groups of the pass kernel, each on its own tile
-                                   (1, 2, or 4 with 512 threads; at most the number of stages)     */
+                                   (1, 2, 4 or 8 with 512 threads; at most the number of stages)    */
 #define SV_OPT_PASS_WINDOW 11   /* gates the pass planner scans ahead (1..4096)                    */
 #define SV_OPT_PASS_MERGE  12   /* 1 (default): merge commuting same-target gates before SV_BLOCK passes;
                                    0: keep every gate (per-gate microbenchmarks)                   */
@@ -227,6 +229,12 @@ SV_API sv_status sv_get_info(sv_handle h, sv_info *out);
 #define SV_OPT_PASS_SEARCH 14   /* 1 (default): each SV_BLOCK pass's in-tile qudit set is the one that
                                    admits the most window gates (subset search); 0: first come, first
                                    admitted */
+#define SV_OPT_SHARD_OVERLAP 17 /* sharded handles (IPC, loopback): when a qubit remap (rule vi) swaps the
+                                   top local qubit and the pending local gates neither touch it nor
+                                   depend on the remapped sharded digit, the half-slice swap runs on a
+                                   comm stream on this many SMs while the pending gates run on the
+                                   staying half on the others; the moved half gets them afterwards.
+                                   0 = off; default 16                                                */
 #define SV_OPT_PASS_KERNEL 16   /* SV_BLOCK pass kernel: 0 (default) = per-gate (k_gate_pass: every gate
                                    sweeps the shared-memory tile, one group barrier per gate); 1 =
                                    register-blocked stages (k_gate_stage: consecutive gates on a pair of

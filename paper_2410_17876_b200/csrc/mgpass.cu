@@ -1272,12 +1272,16 @@ cudaError_t launch_pass_t(const PassParams &p, cudaStream_t st, const LaunchCfg 
 }
 
 cudaError_t launch_pass(const PassParams &p, cudaStream_t st, const LaunchCfg &cfg) {
-    if (cfg.c64) return launch_pass_t<512, 2, float2>(p, st, cfg);   // complex64: one configuration
+    if (cfg.c64) {                                // complex64: 512 threads, 2 or 4 groups
+        if (cfg.pass_groups >= 4 && cfg.pass_stages >= 4) return launch_pass_t<512, 4, float2>(p, st, cfg);
+        return launch_pass_t<512, 2, float2>(p, st, cfg);
+    }
     int G = cfg.pass_groups;                      // one stage per group at least
     while (G > 1 && cfg.pass_stages < G) G /= 2;
     if (cfg.pass_threads >= 960) return launch_pass_t<960, 2, double2>(p, st, cfg);   // 32 warps, 64 registers
     if (cfg.pass_threads >= 768) return launch_pass_t<768, 2, double2>(p, st, cfg);   // 26 warps, 72 registers
     if (cfg.pass_threads >= 512) {
+        if (G >= 8) return launch_pass_t<512, 8, double2>(p, st, cfg);
         if (G >= 4) return launch_pass_t<512, 4, double2>(p, st, cfg);
         if (G == 2) return launch_pass_t<512, 2, double2>(p, st, cfg);
         return launch_pass_t<512, 1, double2>(p, st, cfg);

@@ -161,6 +161,8 @@ struct ShardCtx {
     IpcShm *shm = nullptr;
     char shm_name[129] = {0};      // unlinked once every rank has attached (or on failure)
     std::vector<DryOp> dry;        // kDryRun: the recorded schedule
+    cudaEvent_t ev_join = nullptr; // overlapped remap: the comm stream's swap done
+    uint64_t overlapped = 0;       // remaps that overlapped a local run
     int red_parity = 0;
     std::vector<double2 *> slices; // loopback: P slices (slices[0] is h->psi); NCCL: {h->psi}
     double2 *stage[2] = {nullptr, nullptr};
@@ -203,6 +205,7 @@ void shard_destroy(ShardCtx *c) {
     for (cudaEvent_t e : c->ev_recv) if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : c->ev_done) if (e) cudaEventDestroy(e);
     if (c->ev_start) cudaEventDestroy(c->ev_start);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->d_scalar) cudaFree(c->d_scalar);
     delete c;
@@ -240,6 +243,7 @@ sv_status ipc_barrier_raw(ShardCtx *c) {
 }
 
 int shard_rank(const ShardCtx *c) { return c->rank; }
+uint64_t shard_overlapped(const ShardCtx *c) { return c->overlapped; }
 int shard_nranks(const ShardCtx *c) { return c->P; }
 
 namespace {
@@ -674,6 +678,101 @@ sv_status shard_apply(sv_handle h, const GateSpec &g_logical, bool check_unitary
     return apply_phys(h, g);
 }
 
+namespace {
+
+// Run a local gate list on one half of a slice: the local register without its top digit (whose
+// value is fixed over the half), at buf.  The host plan cache is bypassed (keyed by gates, not
+// registers); profiling records half-slice state bytes.
+sv_status run_on_half(sv_handle h, const Register &sub, std::vector<GateSpec> gates, uint32_t flags, double2 *buf) {
+    const Register keep = h->local;
+    const bool cache = h->plan_cache;
+    h->local = sub;
+    h->plan_cache = false;
+    sv_status s = run_local_circuit(h, gates, flags, buf);
+    h->local = keep;
+    h->plan_cache = cache;
+    return s;
+}
+
+}  // namespace
+
+// Rule vi with overlap (SV_OPT_SHARD_OVERLAP): the remap of sharded position j with the TOP local
+// position k moves the half of each slice whose digit k is 1 - beta (a contiguous half: k is the
+// top digit) and keeps the other.  When the pending local run R neither targets nor controls k and
+// no gate of it depends on digit j (a sharded control on j, a local phase from a gate on j),
+// R commutes with the remap, so: the half that moves is swapped on the comm stream by
+// k_pair_swap on `lend` SMs while R runs on the staying half on the remaining SMs; after the
+// swap, R runs on the half that arrived (the partner's, which its owner did not update — by the
+// same rule).  Every amplitude gets R once; the swap kernel and the passes touch disjoint halves.
+sv_status overlapped_remap(sv_handle h, int k, int j, std::vector<std::vector<GateSpec>> &runs,
+                           const std::vector<int> &ranks, uint32_t flags) {
+    ShardCtx *c = h->shard;
+    const uint64_t L = h->local.D, half = L / 2;
+    Register sub;
+    std::string *err = err_slot();
+    sv_status s = make_register(h->local.dims, h->local.n - 1, &sub, err);
+    if (s != SV_OK) return s;
+    const int lend = h->cfg.shard_overlap;
+    const uint32_t lf = flags & (SV_FUSE | SV_BLOCK);
+    s = ipc_fence(h);                               // both halves final everywhere before the swap
+    if (s != SV_OK) return s;
+    cudaError_t e = cudaEventRecord(c->ev_join, h->stream);   // loopback: the swap after earlier work
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->comm_stream, c->ev_join, 0);
+    if (e != cudaSuccess) return cuda_fail_h(h, e, "overlapped swap setup");
+    // (1) the moving halves, on the comm stream, on `lend` SMs
+    auto beta_of = [&](int r) { return (c->lrank[r] >> j) & 1; };
+    if (c->transport == kIpc) {
+        const int r = c->rank, beta = beta_of(r), p = c->prank[c->lrank[r] ^ (1 << j)];
+        const uint64_t q0 = half / 2, n = beta ? half - q0 : q0;
+        void *tok;
+        prof_begin(h, &tok, c->comm_stream);
+        e = launch_pair_swap(at(c->peer[r], (uint64_t)(1 - beta) * half, h->elem), at(c->peer[p], (uint64_t)beta * half, h->elem),
+                             half, beta ? q0 : 0, n, c->comm_stream, lend, &h->launches, h->c64);
+        prof_end(h, tok, (double)h->elem * (double)L, 2.0 * (double)h->elem * (double)n, 0.0, c->comm_stream);
+        ++h->exchanges;
+    } else {                                        // loopback: one kernel per slice pair
+        for (int r : ranks) {
+            const int p = c->prank[c->lrank[r] ^ (1 << j)];
+            if (p < r || e != cudaSuccess) continue;
+            const int beta = beta_of(r);
+            void *tok;
+            prof_begin(h, &tok, c->comm_stream);
+            e = launch_pair_swap(at(c->slices[r], (uint64_t)(1 - beta) * half, h->elem),
+                                 at(c->slices[p], (uint64_t)beta * half, h->elem), half, 0, half, c->comm_stream, lend,
+                                 &h->launches, h->c64);
+            prof_end(h, tok, 2.0 * (double)h->elem * (double)L, 0.0, 0.0, c->comm_stream);
+            ++h->exchanges;
+        }
+    }
+    if (e != cudaSuccess) return cuda_fail_h(h, e, "overlapped qubit swap");
+    // (2) the staying halves, on the main stream, on the other SMs
+    const int sms = h->cfg.num_sms;
+    h->cfg.num_sms = sms - lend;
+    for (size_t i = 0; i < ranks.size() && s == SV_OK; ++i)
+        if (!runs[i].empty())
+            s = run_on_half(h, sub, runs[i], lf, at(slice_of(c, ranks[i]), (uint64_t)beta_of(ranks[i]) * half, h->elem));
+    h->cfg.num_sms = sms;
+    if (s != SV_OK) return s;
+    // join: the swap done on this device; IPC: on every device (the partner writes our half)
+    e = cudaEventRecord(c->ev_join, c->comm_stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->stream, c->ev_join, 0);
+    if (e != cudaSuccess) return cuda_fail_h(h, e, "overlapped swap join");
+    s = ipc_fence(h);
+    if (s != SV_OK) return s;
+    // (3) the arrived halves (digit k = 1 - beta before the relabel of positions)
+    for (size_t i = 0; i < ranks.size() && s == SV_OK; ++i)
+        if (!runs[i].empty())
+            s = run_on_half(h, sub, runs[i], lf, at(slice_of(c, ranks[i]), (uint64_t)(1 - beta_of(ranks[i])) * half, h->elem));
+    if (s != SV_OK) return s;
+    for (auto &r : runs) r.clear();
+    const int q = h->local.n + j;                  // the remap itself (as swap_qubits)
+    std::swap(c->log_at[k], c->log_at[q]);
+    c->pos_of[c->log_at[k]] = k;
+    c->pos_of[c->log_at[q]] = q;
+    ++c->overlapped;
+    return SV_OK;
+}
+
 sv_status shard_apply_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_t flags) {
     // Runs of gates with a local target go through the local circuit driver on every slice
     // this handle owns (fusion / multi-gate passes included).  Controls on sharded digits are
@@ -688,6 +787,7 @@ sv_status shard_apply_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_
     std::vector<std::vector<GateSpec>> runs(ranks.size());
     std::vector<GateSpec> pending;                 // exchange gates not applied yet, in order
     bool any = false;
+    uint32_t run_dep = 0;                          // sharded positions the pending runs depend on
     auto flush = [&]() -> sv_status {
         if (any) {
             const uint32_t local_flags = flags & (SV_FUSE | SV_BLOCK);
@@ -703,6 +803,7 @@ sv_status shard_apply_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_
                 runs[i].clear();
             }
             any = false;
+            run_dep = 0;
         }
         for (const GateSpec &g : pending) {
             sv_status s = apply_phys(h, g);
@@ -718,9 +819,26 @@ sv_status shard_apply_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_
         GateSpec g = to_phys(c, gl0);
         ShardKind kind = classify(h->local, g);
         if (kind == SK_EXCHANGE && h->cfg.shard_swap && pick_local(h, g.target - first_sh, &specs, gi) >= 0) {
-            sv_status s = flush();                  // rule vi: remap, then the gate is local
-            bool swapped = false;
-            if (s == SV_OK) s = try_swap(h, g.target - first_sh, &specs, gi, &swapped);
+            const int j = g.target - first_sh, k = pick_local(h, j, &specs, gi);
+            const int top = h->local.n - 1;
+            bool ov = any && pending.empty() && k == top && h->cfg.shard_overlap > 0 && h->local.n >= 2 &&
+                      h->cfg.shard_overlap < h->cfg.num_sms && !((run_dep >> j) & 1u) &&
+                      (c->transport == kIpc || c->transport == kLoopback);
+            for (size_t i = 0; ov && i < runs.size(); ++i)
+                for (const GateSpec &q : runs[i]) {
+                    if (q.target + q.span > top) ov = false;          // touches digit k
+                    for (const auto &cs : q.ctrl) if (cs.q == top) ov = false;
+                }
+            sv_status s = SV_OK;
+            if (ov) {                               // rule vi overlapped with the pending run
+                s = overlapped_remap(h, k, j, runs, ranks, flags);
+                any = false;
+                run_dep = 0;
+            } else {
+                s = flush();                        // rule vi: remap, then the gate is local
+                bool swapped = false;
+                if (s == SV_OK) s = try_swap(h, j, &specs, gi, &swapped);
+            }
             if (s != SV_OK) return s;
             g = to_phys(c, gl0);
             kind = classify(h->local, g);
@@ -733,6 +851,7 @@ sv_status shard_apply_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_
                     if (ranks[i] == rs.first) {
                         runs[i].push_back(scale_gate(h->local, rs.second));
                         any = true;
+                        run_dep = ~0u;              // slice-specific scaling: no overlapped remap
                     }
             continue;
         }
@@ -752,8 +871,11 @@ sv_status shard_apply_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_
         }
         for (size_t i = 0; i < ranks.size(); ++i) {
             const int l = c->lrank[ranks[i]];          // bit j of l = digit of q_{n-s+j}
+            for (const auto &cs : g.ctrl)
+                if (cs.q >= first_sh) run_dep |= 1u << (cs.q - first_sh);   // rank predicate on that digit
             if (!fires_on(g.ctrl, first_sh, l)) continue;
             if (kind == SK_PHASE) {
+                run_dep |= 1u << (g.target - first_sh);                    // phase of that digit's value
                 GateSpec pl;
                 if (phase_local(h->local, g, l, &pl)) {
                     runs[i].push_back(std::move(pl));
@@ -1074,6 +1196,11 @@ static sv_status create_sharded(const int32_t *dims, int32_t n, sv_dtype dt, int
     c->chunk = ch ? strtoull(ch, nullptr, 10) : (16ull << 20);     // 16 Mi amplitudes = 256 MiB
     if (c->chunk == 0) c->chunk = 16ull << 20;
     if (c->chunk > L) c->chunk = L;
+    if (transport == kIpc || transport == kLoopback) {   // the stream an overlapped remap swaps on
+        e = cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
+        if (e != cudaSuccess) { cudaGetLastError(); state_free(h); return fail_msg(SV_ERR_NOMEM, "comm stream"); }
+    }
     if (transport == kNccl) {                 // staging and the comm stream: the NCCL path only
         for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaMalloc(&c->stage[i], c->chunk * h->elem);
         if (e == cudaSuccess) e = cudaMalloc(&c->d_scalar, sizeof(double));

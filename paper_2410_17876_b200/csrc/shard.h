@@ -20,13 +20,15 @@ sv_status local_norm2(sv_handle h, double *out);
 sv_status local_apply(sv_handle h, const GatePlan &p);
 sv_status launch_on(sv_handle h, const GatePlan &p, double2 *buf);
 sv_status run_local_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_t flags, double2 *buf);
-void prof_begin(sv_handle h, void **tok);
-void prof_end(sv_handle h, void *tok, double hbm_bytes, double nvlink_bytes, double touched);
+void prof_begin(sv_handle h, void **tok, cudaStream_t st = nullptr);
+void prof_end(sv_handle h, void *tok, double hbm_bytes, double nvlink_bytes, double touched,
+              cudaStream_t st = nullptr);
 
 // implemented in shard.cpp
 void shard_destroy(ShardCtx *c);
 int shard_rank(const ShardCtx *c);
 int shard_nranks(const ShardCtx *c);
+uint64_t shard_overlapped(const ShardCtx *c);
 sv_status shard_reset(sv_handle h, uint64_t idx);
 sv_status shard_apply(sv_handle h, const GateSpec &g, bool check_unitary);
 sv_status shard_apply_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_t flags);

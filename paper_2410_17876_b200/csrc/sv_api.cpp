@@ -60,15 +60,16 @@ void default_cfg(LaunchCfg &c, int device) {
     c.tile_stages = 3;
     c.ctas_per_sm = 2;
     c.num_sms = sms;
-    c.pass_tile = 4096;        // measured best on c2-c4 (profiles/r01/passbench_*_groups.jsonl)
-    c.pass_stages = 3;
+    c.pass_tile = 2560;        // 5 stages x 2560 amplitudes, 4 consumer groups of 4 warps: c4 1588 -> 1440 ms,
+    c.pass_stages = 5;         //   c3 389 -> 387 ms against 4096 x 3 with 2 groups (profiles/r02/ab/r02s-r02u)
     c.pass_threads = 512;
     c.pass_gates = 32;         // with the in-tile set search: c3 -1.4%, c4 unchanged (ab/gates_window_*)
     c.pass_window = 256;       // gates scanned ahead when filling a pass (profiles/r01/ab/window_*, ab/gates_window_*)
     c.pass_merge = 1;          // commutation-aware merging before pass planning
-    c.pass_groups = 2;         // two consumer groups ping-pong over tiles
+    c.pass_groups = 4;         // four consumer groups rotate over the CTA's tiles (one stage in flight)
     c.shard_swap = 1;          // qubit remapping for gates on sharded qubits
     c.pass_search = 1;         // in-tile set chosen by subset search (c4 29 -> 22 passes)
+    c.shard_overlap = 16;      // remap overlapped with the pending local run on 132 + 16 SMs
     c.pass_kernel = 0;         // per-gate pass kernel (stages measured slower on c3/c4: profiles/r02)
 }
 
@@ -94,7 +95,11 @@ sv_status state_init_device(sv_handle h, int device, void *cuda_stream, void *ex
         h->own_stream = true;
     }
     h->cfg.c64 = h->c64 ? 1 : 0;
-    if (h->c64) h->cfg.pass_tile = 8192;   // 8-byte elements: twice the amplitudes per stage (c4: 1.78 -> 1.25 s)
+    if (h->c64) {                          // 8-byte elements: twice the amplitudes per stage (c4: 1.78 -> 1.25 s);
+        h->cfg.pass_tile = 8192;           // 3 stages and 2 groups stay best for complex64 (profiles/r02/ab/r02u)
+        h->cfg.pass_stages = 3;
+        h->cfg.pass_groups = 2;
+    }
     const uint64_t bytes = h->local.D * h->elem;
     if (ext) {
         if (ext_bytes < bytes || ((uintptr_t)ext & 15))
@@ -170,17 +175,17 @@ sv_status local_apply(sv_handle h, const GatePlan &p) { return launch_on(h, p, h
 
 // SV_OPT_PROFILE brackets for the cross-rank kernels (shard.cpp): hbm = bytes this rank's HBM
 // moves, nvl = bytes per direction over this rank's NVLink ports.
-void prof_begin(sv_handle h, void **tok) {
+void prof_begin(sv_handle h, void **tok, cudaStream_t st) {
     *tok = nullptr;
     if (!h->profile) return;
     cudaEvent_t a = pool_event(h);
-    cudaEventRecord(a, h->stream);
+    cudaEventRecord(a, st ? st : h->stream);
     *tok = a;
 }
-void prof_end(sv_handle h, void *tok, double hbm, double nvl, double touched) {
+void prof_end(sv_handle h, void *tok, double hbm, double nvl, double touched, cudaStream_t st) {
     if (!h->profile || !tok) return;
     cudaEvent_t b = pool_event(h);
-    cudaEventRecord(b, h->stream);
+    cudaEventRecord(b, st ? st : h->stream);
     h->prof.push_back({(cudaEvent_t)tok, b, hbm, touched, hbm, sv_state_s::kProfComm, 0.0, 0.0, nvl});
 }
 
@@ -504,6 +509,7 @@ sv_status sv_get_info(sv_handle h, sv_info *out) {
     out->cuda_stream = h->stream;
     out->kernel_launches = h->launches;
     out->exchanges = h->exchanges;
+    out->overlapped = h->shard ? shard_overlapped(h->shard) : 0;
     return SV_OK;
 }
 
@@ -530,7 +536,7 @@ sv_status sv_set_option(sv_handle h, int32_t option, int64_t value) {
             h->cfg.pass_tile = (int)value;
             return SV_OK;
         case SV_OPT_PASS_STAGES:
-            if (value < 2 || value > 6) return fail(SV_ERR_INVALID_ARG, "pass stages 2..6");
+            if (value < 2 || value > 12) return fail(SV_ERR_INVALID_ARG, "pass stages 2..12");
             h->cfg.pass_stages = (int)value;
             return SV_OK;
         case SV_OPT_PASS_THREADS:
@@ -539,7 +545,7 @@ sv_status sv_set_option(sv_handle h, int32_t option, int64_t value) {
             h->cfg.pass_threads = (int)value;
             return SV_OK;
         case SV_OPT_PASS_GROUPS:
-            if (value != 1 && value != 2 && value != 4) return fail(SV_ERR_INVALID_ARG, "pass groups 1, 2 or 4");
+            if (value != 1 && value != 2 && value != 4 && value != 8) return fail(SV_ERR_INVALID_ARG, "pass groups 1, 2, 4 or 8");
             h->cfg.pass_groups = (int)value;
             return SV_OK;
         case SV_OPT_PASS_MERGE:
@@ -550,6 +556,10 @@ sv_status sv_set_option(sv_handle h, int32_t option, int64_t value) {
             return SV_OK;
         case SV_OPT_PASS_SEARCH:
             h->cfg.pass_search = value != 0;
+            return SV_OK;
+        case SV_OPT_SHARD_OVERLAP:
+            if (value < 0 || value > 64) return fail(SV_ERR_INVALID_ARG, "shard overlap SMs 0..64");
+            h->cfg.shard_overlap = (int)value;
             return SV_OK;
         case SV_OPT_PASS_KERNEL:
             if (value < 0 || value > 1) return fail(SV_ERR_INVALID_ARG, "pass kernel 0 or 1");

@@ -20,7 +20,7 @@ SV_FUSE, SV_NO_CHECK, SV_GRAPH, SV_BLOCK = 1, 2, 4, 8
 SV_OPT_KERNEL, SV_OPT_TILE_ELEMS, SV_OPT_TILE_STAGES, SV_OPT_CTAS_PER_SM, SV_OPT_PROFILE, SV_OPT_PASS_TILE = 1, 2, 3, 4, 5, 6
 SV_OPT_PASS_STAGES, SV_OPT_PASS_THREADS, SV_OPT_PASS_GATES, SV_OPT_PASS_GROUPS = 7, 8, 9, 10
 SV_OPT_PASS_WINDOW, SV_OPT_PASS_MERGE, SV_OPT_SHARD_SWAP, SV_OPT_PASS_SEARCH = 11, 12, 13, 14
-SV_OPT_PLAN_CACHE, SV_OPT_PASS_KERNEL = 15, 16
+SV_OPT_PLAN_CACHE, SV_OPT_PASS_KERNEL, SV_OPT_SHARD_OVERLAP = 15, 16, 17
 
 STATUS = {0: "SV_OK", 1: "SV_ERR_INVALID_ARG", 2: "SV_ERR_DIM", 3: "SV_ERR_OVERFLOW",
           4: "SV_ERR_QUDIT_RANGE", 5: "SV_ERR_CTRL_OVERLAP", 6: "SV_ERR_CTRL_DUP",
@@ -45,7 +45,7 @@ class sv_info(C.Structure):
     _fields_ = [("D", C.c_uint64), ("local_D", C.c_uint64), ("n", C.c_int32),
                 ("rank", C.c_int32), ("nranks", C.c_int32), ("device_ptr", C.c_void_p),
                 ("cuda_stream", C.c_void_p), ("kernel_launches", C.c_uint64),
-                ("exchanges", C.c_uint64)]
+                ("exchanges", C.c_uint64), ("overlapped", C.c_uint64)]
 
 
 class sv_profile(C.Structure):

@@ -26,6 +26,7 @@ def main():
     st = P.State.sharded_ipc(dims, rank, job["nranks"], job["ipc_id"], device=dev, dtype=job.get("dtype", "c128"))
     try:
         st.set_option(P.sv.SV_OPT_SHARD_SWAP, job.get("swap", 1))
+        st.set_option(P.sv.SV_OPT_SHARD_OVERLAP, job.get("overlap", 16))
         if job.get("psi0") is not None:
             st.set_amplitudes(0, job["psi0"])      # each rank writes the part it owns
         mode = job.get("mode", "block")
@@ -44,6 +45,7 @@ def main():
         else:
             res["psi"] = st.amplitudes()           # collective: reads every slice
         res["exchanges"] = int(st.info().exchanges)
+        res["overlapped"] = int(st.info().overlapped)
         if job.get("extra"):
             st.apply_circuit(job["extra"], block=True)
             res["psi_extra"] = st.amplitudes()

@@ -163,3 +163,17 @@ def test_ipc_c5_full_size_adjoint_return(P):
     assert abs(res["norm"] - 1.0) <= 1e-10 and abs(res["norm2"] - 1.0) <= 1e-10
     assert abs(res["head"][0] - 1.0) <= 1e-10
     assert np.max(np.abs(res["head"][1:])) <= 1e-10 and np.max(np.abs(res["tail"])) <= 1e-10
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_ipc_overlapped_remap(P, nranks):
+    """The overlapped remap across processes: the swap kernel on the comm stream reads and writes
+    the partner's moving half while each rank's passes update its staying half; vs O-2."""
+    from _circuits import overlap_circuit as _overlap_circuit
+    dims = [3, 3, 4, 2, 2, 2, 2, 2, 2]
+    gates = _overlap_circuit(dims, 41 + nranks)
+    psi0 = random_state(int(np.prod(dims)), 10)
+    ref = O2.run(dims, gates, psi0)
+    res = _run(P, {"dims": dims, "gates": gates, "psi0": psi0, "swap": 1, "mode": "block", "overlap": 16}, nranks)
+    assert np.max(np.abs(res["psi"] - ref)) <= 1e-12
+    assert res["overlapped"] > 0

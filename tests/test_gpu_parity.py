@@ -10,6 +10,7 @@ pytestmark = pytest.mark.gpu
 
 from oracle import blocksim as O2  # noqa: E402
 from oracle import kron as O1  # noqa: E402
+from _circuits import overlap_circuit as _overlap_circuit  # noqa: E402
 from sv_inputs import (Gate, shift_x, clock_z, fourier, hadamard, t_gate, haar_unitary,  # noqa: E402
                        permutation_matrix, phase_gate, ghz_circuit, worked_example,
                        random_circuit, adjoint_circuit, labelled_state, random_state,
@@ -473,8 +474,29 @@ def test_loopback_c5_recipe_reduced_register(P, nranks):
         assert abs(nrm - 1.0) <= 1e-10
 
 
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_loopback_overlapped_remap(P, nranks):
+    """Remaps overlapped with the pending local run (the half that moves swapped on a comm stream
+    while the run updates the staying half, then the arrived half): same state as O-2 and as the
+    non-overlapped schedule; the overlap path actually runs."""
+    dims = [3, 3, 4, 2, 2, 2, 2, 2, 2]
+    gates = _overlap_circuit(dims, 31 + nranks)
+    psi0 = random_state(int(np.prod(dims)), 9)
+    ref = O2.run(dims, gates, psi0)
+    for ov, block in ((16, True), (0, True), (16, False)):
+        with P.State.loopback(dims, nranks) as st:
+            st.set_option(P.sv.SV_OPT_SHARD_OVERLAP, ov)
+            st.set_amplitudes(0, psi0)
+            st.apply_circuit(gates, block=block)
+            got = st.amplitudes()
+            over = st.info().overlapped
+        assert np.max(np.abs(got - ref)) <= 1e-12, (ov, block)
+        assert (over > 0) == (ov > 0), (ov, block, over)
+
+
 # (compute threads, consumer groups, stages) of the pass kernel
-PASS_CFGS = [(256, 1, 2), (384, 1, 2), (512, 1, 2), (384, 2, 2), (256, 2, 3), (384, 2, 3), (512, 2, 3), (512, 4, 4)]
+PASS_CFGS = [(256, 1, 2), (384, 1, 2), (512, 1, 2), (384, 2, 2), (256, 2, 3), (384, 2, 3), (512, 2, 3), (512, 4, 4),
+             (512, 4, 5), (512, 8, 9)]
 
 
 @pytest.mark.parametrize("pass_cfg", PASS_CFGS)
@@ -514,7 +536,7 @@ def test_block_passes_labelled_bit_exact(P, pass_cfg):
         gates.append(Gate(t, ctrl, vals, permutation_matrix(rng.permutation(dims[t]))))
     psi0 = labelled_state(0, D)
     ref = O2.run(dims, gates, psi0)
-    tile = {2: 6144, 3: 4096}.get(pass_cfg[2], 2048)
+    tile = {2: 6144, 3: 4096, 4: 3072, 5: 2560}.get(pass_cfg[2], 1280)   # the ring fits shared memory
     got, _, launched = run_gpu(P, dims, gates, psi0, block=True, pass_tile=tile, pass_cfg=pass_cfg)
     assert launched < len(gates)
     assert np.array_equal(got, ref)
