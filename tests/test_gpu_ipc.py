@@ -171,7 +171,7 @@ def test_ipc_overlapped_remap(P, nranks):
     the partner's moving half while each rank's passes update its staying half; vs O-2."""
     from _circuits import overlap_circuit as _overlap_circuit
     dims = [3, 3, 4, 2, 2, 2, 2, 2, 2]
-    gates = _overlap_circuit(dims, 41 + nranks)
+    gates = _overlap_circuit(dims, 41 + nranks, nranks)
     psi0 = random_state(int(np.prod(dims)), 10)
     ref = O2.run(dims, gates, psi0)
     res = _run(P, {"dims": dims, "gates": gates, "psi0": psi0, "swap": 1, "mode": "block", "overlap": 16}, nranks)

@@ -480,7 +480,7 @@ def test_loopback_overlapped_remap(P, nranks):
     while the run updates the staying half, then the arrived half): same state as O-2 and as the
     non-overlapped schedule; the overlap path actually runs."""
     dims = [3, 3, 4, 2, 2, 2, 2, 2, 2]
-    gates = _overlap_circuit(dims, 31 + nranks)
+    gates = _overlap_circuit(dims, 31 + nranks, nranks)
     psi0 = random_state(int(np.prod(dims)), 9)
     ref = O2.run(dims, gates, psi0)
     for ov, block in ((16, True), (0, True), (16, False)):

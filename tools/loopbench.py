@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--nqubits", type=int, default=None)
     ap.add_argument("--block", type=int, default=1)
     ap.add_argument("--swap", type=int, default=1, help="SV_OPT_SHARD_SWAP: qubit remapping (1) or exchange (0)")
+    ap.add_argument("--overlap", type=int, default=16, help="SV_OPT_SHARD_OVERLAP: SMs lent to overlapped remaps (0 off)")
     args = ap.parse_args()
     import torch
     import paper_2410_17876_b200 as P
@@ -30,11 +31,12 @@ def main():
         st = P.State(dims) if nr == 1 else P.State.loopback(dims, nr)
         if nr > 1:
             st.set_option(P.sv.SV_OPT_SHARD_SWAP, args.swap)
+            st.set_option(P.sv.SV_OPT_SHARD_OVERLAP, args.overlap)
         ext = torch.cuda.ExternalStream(st.info().cuda_stream)
         st.reset(0)
         st.apply_circuit(ga, fuse=True, check=False, block=bool(args.block))
         st.sync()
-        x0 = st.info().exchanges
+        x0, o0 = st.info().exchanges, st.info().overlapped
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(ext)
         for _ in range(args.reps):
@@ -44,7 +46,8 @@ def main():
         st.sync()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / args.reps
-        print(json.dumps({"config": args.config, "ranks": nr, "swap": args.swap, "ms_per_circuit": ms,
+        print(json.dumps({"config": args.config, "ranks": nr, "swap": args.swap, "overlap": args.overlap,
+                          "overlapped_per_circuit": (st.info().overlapped - o0) / args.reps, "ms_per_circuit": ms,
                           "ms_per_rank_slice": ms / nr,
                           "exchanges_per_circuit": (st.info().exchanges - x0) / args.reps}), flush=True)
         st.close()
