@@ -235,6 +235,9 @@ SV_API sv_status sv_get_info(sv_handle h, sv_info *out);
                                    comm stream on this many SMs while the pending gates run on the
                                    staying half on the others; the moved half gets them afterwards.
                                    0 = off; default 16                                                */
+#define SV_OPT_PASS_LOW    18   /* SV_BLOCK: the low prefix every pass tile holds whole = the qudits whose
+                                   stride is below this many amplitudes (default 32: tile runs, i.e.
+                                   bulk copies, of >= 512 B for complex128)                          */
 #define SV_OPT_PASS_KERNEL 16   /* SV_BLOCK pass kernel: 0 (default) = per-gate (k_gate_pass: every gate
                                    sweeps the shared-memory tile, one group barrier per gate); 1 =
                                    register-blocked stages (k_gate_stage: consecutive gates on a pair of

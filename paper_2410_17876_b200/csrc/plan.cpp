@@ -392,14 +392,14 @@ static std::vector<char> best_in_tile_set(const Register &reg, const std::vector
 }
 
 std::vector<PassPlan> plan_passes(const Register &reg, const std::vector<GateSpec> &g, uint64_t tile_cap,
-                                  int max_gates, int window, bool search) {
+                                  int max_gates, int window, bool search, uint64_t low_stride) {
     std::vector<PassPlan> passes;
     std::vector<char> diag(g.size(), 0);
     if (search)
         for (size_t i = 0; i < g.size(); ++i) diag[i] = is_diag(g[i]);
     // forced low prefix: every qudit whose stride is < 32 amplitudes
     int m0 = 0;
-    while (m0 < reg.n && reg.b[m0] < 32) ++m0;
+    while (m0 < reg.n && reg.b[m0] < low_stride) ++m0;
     const uint64_t base_tile = (m0 < reg.n) ? reg.b[m0] : reg.D;
     std::vector<char> done(g.size(), 0);
     size_t first = 0;

@@ -76,8 +76,10 @@ struct PassPlan {
 };
 // search: choose each pass's in-tile set by scoring every subset of the window's targets
 // that fits (else first come, first admitted).
+// low_stride: the forced low prefix is every qudit whose stride is below it (in amplitudes; the
+// bulk copies of a tile are runs of at least b_{m0} amplitudes)
 std::vector<PassPlan> plan_passes(const Register &reg, const std::vector<GateSpec> &g, uint64_t tile_cap,
-                                  int max_gates, int window, bool search = true);
+                                  int max_gates, int window, bool search = true, uint64_t low_stride = 32);
 
 // Work of one multi-gate pass as executed (after merging and pairing), for the roofline:
 //   touched      sum of T over the pass's gates (SURVEY.md §8(d) amplitude updates);

@@ -69,6 +69,7 @@ void default_cfg(LaunchCfg &c, int device) {
     c.pass_groups = 4;         // four consumer groups rotate over the CTA's tiles (one stage in flight)
     c.shard_swap = 1;          // qubit remapping for gates on sharded qubits
     c.pass_search = 1;         // in-tile set chosen by subset search (c4 29 -> 22 passes)
+    c.pass_low = 32;           // tile runs of >= 32 amplitudes (512 B bulk copies)
     c.shard_overlap = 16;      // remap overlapped with the pending local run on 132 + 16 SMs
     c.pass_kernel = 0;         // per-gate pass kernel (stages measured slower on c3/c4: profiles/r02)
 }
@@ -273,7 +274,7 @@ sv_status run_local_circuit(sv_handle h, std::vector<GateSpec> &specs, uint32_t 
         } else {
             if (h->cfg.pass_merge) specs = merge_commuting(specs, 64);
             passes = plan_passes(h->local, specs, (uint64_t)h->cfg.pass_tile, h->cfg.pass_gates,
-                                 h->cfg.pass_window, h->cfg.pass_search != 0);
+                                 h->cfg.pass_window, h->cfg.pass_search != 0, (uint64_t)h->cfg.pass_low);
             if (h->plan_cache) {
                 h->plan_key.swap(pkey);
                 h->plan_specs = specs;
@@ -556,6 +557,10 @@ sv_status sv_set_option(sv_handle h, int32_t option, int64_t value) {
             return SV_OK;
         case SV_OPT_PASS_SEARCH:
             h->cfg.pass_search = value != 0;
+            return SV_OK;
+        case SV_OPT_PASS_LOW:
+            if (value < 1 || value > 4096) return fail(SV_ERR_INVALID_ARG, "pass low-prefix stride 1..4096");
+            h->cfg.pass_low = (int)value;
             return SV_OK;
         case SV_OPT_SHARD_OVERLAP:
             if (value < 0 || value > 64) return fail(SV_ERR_INVALID_ARG, "shard overlap SMs 0..64");

@@ -202,6 +202,7 @@ struct LaunchCfg {
     int shard_swap;    // 1: sharded mode remaps qubits instead of pairwise exchanges (shard.cpp vi)
     int pass_search;   // 1: pass planner scores in-tile sets (plan.cpp best_in_tile_set)
     int c64;           // 1: the state is complex64 (float2), else complex128 (double2)
+    int pass_low;      // SV_BLOCK: qudits with stride below this many amplitudes form the low prefix
     int shard_overlap; // SMs lent to a qubit remap that overlaps the pending local run (0 = off)
     int pass_kernel;   // SV_BLOCK passes: 0 = per-gate kernel (k_gate_pass); 1 = register-blocked
                        // stages (k_gate_stage) when the pass fits them, else per-gate

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--reps", type=int, default=1)
     ap.add_argument("--search", type=int, default=1, help="SV_OPT_PASS_SEARCH (in-tile set search)")
     ap.add_argument("--skip-noblock", action="store_true", help="do not time the single-gate mode")
+    ap.add_argument("--low", type=int, default=32, help="SV_OPT_PASS_LOW (low-prefix stride threshold)")
     ap.add_argument("--pass-kernel", type=int, default=0, help="SV_OPT_PASS_KERNEL: 0 per-gate, 1 register-blocked stages")
     args = ap.parse_args()
     import torch
@@ -57,6 +58,7 @@ def main():
             st.set_option(P.sv.SV_OPT_PASS_WINDOW, rest[1])
             st.set_option(P.sv.SV_OPT_PASS_SEARCH, args.search)
             st.set_option(P.sv.SV_OPT_PASS_KERNEL, args.pass_kernel)
+            st.set_option(P.sv.SV_OPT_PASS_LOW, args.low)
         st.reset(0)
         st.apply_circuit(ga, fuse=True, check=False, block=block)
         st.sync()
