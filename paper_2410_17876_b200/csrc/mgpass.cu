@@ -1287,6 +1287,7 @@ cudaError_t launch_pass(const PassParams &p, cudaStream_t st, const LaunchCfg &c
         return launch_pass_t<512, 1, double2>(p, st, cfg);
     }
     if (cfg.pass_threads >= 384) {
+        if (cfg.pass_groups == 3 && cfg.pass_stages >= 3) return launch_pass_t<384, 3, double2>(p, st, cfg);
         if (G >= 2) return launch_pass_t<384, 2, double2>(p, st, cfg);
         return launch_pass_t<384, 1, double2>(p, st, cfg);
     }

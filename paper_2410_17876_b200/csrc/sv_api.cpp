@@ -546,7 +546,8 @@ sv_status sv_set_option(sv_handle h, int32_t option, int64_t value) {
             h->cfg.pass_threads = (int)value;
             return SV_OK;
         case SV_OPT_PASS_GROUPS:
-            if (value != 1 && value != 2 && value != 4 && value != 8) return fail(SV_ERR_INVALID_ARG, "pass groups 1, 2, 4 or 8");
+            if (value != 1 && value != 2 && value != 3 && value != 4 && value != 8)
+                return fail(SV_ERR_INVALID_ARG, "pass groups 1, 2, 3 (384 threads), 4 or 8");
             h->cfg.pass_groups = (int)value;
             return SV_OK;
         case SV_OPT_PASS_MERGE:
