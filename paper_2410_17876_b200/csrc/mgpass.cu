@@ -45,7 +45,7 @@ constexpr int kPoolC = 768;
 constexpr int kMaxPassCtrl = 4;
 constexpr int kMaxIns = 2 + kMaxPassCtrl;   // inserted in-tile digits: the target(s) + pinned controls
 constexpr int kMaxPairDim = 4;             // pair gates: d_a d_b <= 4 (qubit pairs)
-constexpr int kGDesc = 12;                 // words of a gate's shared-memory descriptor
+constexpr int kGDesc = 16;                 // words of a gate's shared-memory descriptor
 
 // in-pass gate kinds: general y = U x (§2.3), monomial y_{sigma(j)} = c_j x_j (§2.1-2.2),
 // and the pure permutation (every moving coefficient exactly 1: no arithmetic at all)
@@ -307,13 +307,18 @@ __device__ __forceinline__ uint32_t insert1(uint32_t e, const Ins1 &a) {
     const uint32_t q = tdiv(e, a.s, a.m, r);
     return q * a.sd + a.ps + r;
 }
-// first insertion from registers (the common uncontrolled case has only it), further ones
-// (in-tile controls) from the parameter bank
-__device__ __forceinline__ uint32_t class_e0(uint32_t c, const PassGateP &g, const Ins1 &first, bool more) {
-    uint32_t e = insert1(c, first);
+// the first two insertions from registers (an uncontrolled gate has one; a gate with one
+// enumerated in-tile control has two), further ones from the parameter bank
+struct Ins2 {
+    Ins1 a, b;
+    uint32_t n;            // insertions in all
+};
+__device__ __forceinline__ uint32_t class_e0(uint32_t c, const PassGateP &g, const Ins2 &ins, bool more) {
+    uint32_t e = insert1(c, ins.a);
     if (more) {
+        e = insert1(e, ins.b);
 #pragma unroll 1
-        for (int i = 1; i < g.nins; ++i) e = insert1(e, ins_at(g, i));
+        for (uint32_t i = 2; i < ins.n; ++i) e = insert1(e, ins_at(g, (int)i));
     }
     return e;
 }
@@ -323,7 +328,7 @@ struct TileGate {
     uint32_t LT, mLT, len, flags;
     uint32_t tbytes;            // bytes of the tile (debug bound checks)
     uint32_t nins, active;      // hot gate fields, read from the shared-memory descriptor
-    Ins1 first;                 // the first digit insertion of the class index
+    Ins2 first;                 // the first two digit insertions of the class index
     const uint32_t *lowoff;     // shared memory: run offsets of the run-digit controls
     const uint32_t *moff;       // shared memory: tile offset of class member j (j st, or the
                                 //   two-digit offset of a pair gate)
@@ -361,7 +366,7 @@ __device__ __forceinline__ bool class_ok(const TileGate &tg, const PassGateP &g,
 // contiguous for strides >= 32): member-0 smem index and whether the class exists and fires.
 // Classes past ncls read index 0 and do not store.
 template <int K, int NT>
-__device__ __forceinline__ void class_batch(const TileGate &tg, const PassGateP &g, const Ins1 &first, bool more,
+__device__ __forceinline__ void class_batch(const TileGate &tg, const PassGateP &g, const Ins2 &first, bool more,
                                             uint32_t c0, uint32_t ncls, bool needck, uint32_t (&e)[K],
                                             bool (&ok)[K]) {
 #pragma unroll
@@ -403,6 +408,14 @@ __device__ __forceinline__ void sts2(uint32_t a, float2 v) {
     asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
 }
 
+// matrix-vector order of general gates, by dimension: row-outer (one output row at a time, the
+// row's matrix entries read per row) or column-outer (all rows at once, one matrix column at a
+// time).  SV_COLOUTER_MASK (bit d): timing A/B builds.
+#ifndef SV_COLOUTER_MASK
+#define SV_COLOUTER_MASK 0u
+#endif
+template <int D> struct PassColOuter { static constexpr bool value = (SV_COLOUTER_MASK >> D) & 1u; };
+
 // One general gate (y = U x per class) on one tile, K classes per thread
 // iteration.  All K*D gathers are issued before the matvecs; buf and U are restrict-qualified
 // so the matrix reads may be scheduled across the stores of earlier rows.  Branch-free: a class
@@ -419,7 +432,7 @@ __device__ __forceinline__ void gate_tile_general(const TileGate &tg, const Pass
 #pragma unroll
     for (int j = 0; j < D; ++j) mo[j] = lds_u32(tg.moff_s + 4u * j) * (uint32_t)sizeof(V);
     const uint32_t sb = smem_u32(buf);
-    const Ins1 first = tg.first;
+    const Ins2 first = tg.first;
     const bool more = tg.nins > 1;
 #pragma unroll 1
     for (uint32_t c0 = cbeg + (uint32_t)tid; c0 < cend; c0 += (uint32_t)(NT * K)) {
@@ -446,19 +459,44 @@ __device__ __forceinline__ void gate_tile_general(const TileGate &tg, const Pass
                 x[k][j] = lds2<V>(a[k] + mo[j]);
             }
         }
+        if constexpr (PassColOuter<D>::value) {
+            // column-outer: every output row of every class accumulates at once (2 K D independent
+            // FMA chains instead of 2 K), matrix column j read once per iteration; the per-element
+            // summation order (j = 0..D-1) is the row-outer one, so results are bit-identical
+            V acc[K][D];
 #pragma unroll
-        for (int i = 0; i < D; ++i) {
-            V acc[K];
+            for (int k = 0; k < K; ++k)
 #pragma unroll
-            for (int k = 0; k < K; ++k) acc[k] = cz<V>();
+                for (int i = 0; i < D; ++i) acc[k][i] = cz<V>();
 #pragma unroll
             for (int j = 0; j < D; ++j) {
-                const V u = Ui[i * D + j];
+                V u[D];
 #pragma unroll
-                for (int k = 0; k < K; ++k) cfma(acc[k], u, x[k][j]);
+                for (int i = 0; i < D; ++i) u[i] = Ui[i * D + j];
+#pragma unroll
+                for (int i = 0; i < D; ++i)
+#pragma unroll
+                    for (int k = 0; k < K; ++k) cfma(acc[k][i], u[i], x[k][j]);
             }
 #pragma unroll
-            for (int k = 0; k < K; ++k) sts2(CHECK ? (ok[k] ? a[k] + mo[i] : trash) : a[k] + mo[i], acc[k]);
+            for (int i = 0; i < D; ++i)
+#pragma unroll
+                for (int k = 0; k < K; ++k) sts2(CHECK ? (ok[k] ? a[k] + mo[i] : trash) : a[k] + mo[i], acc[k][i]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                V acc[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) acc[k] = cz<V>();
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    const V u = Ui[i * D + j];
+#pragma unroll
+                    for (int k = 0; k < K; ++k) cfma(acc[k], u, x[k][j]);
+                }
+#pragma unroll
+                for (int k = 0; k < K; ++k) sts2(CHECK ? (ok[k] ? a[k] + mo[i] : trash) : a[k] + mo[i], acc[k]);
+            }
         }
     }
 }
@@ -472,7 +510,7 @@ __device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const Pas
                                                    const V *__restrict__ U, uint32_t cbeg, uint32_t cend,
                                                    uint32_t ncls, bool needck, int tid, uint32_t trash) {
     const uint32_t act = tg.active;
-    const Ins1 first = tg.first;
+    const Ins2 first = tg.first;
     const bool more = tg.nins > 1;
     // destination offsets sigma(j) * st, read once from shared memory: the stores below may
     // alias that table as far as the compiler knows, so it keeps them in registers instead of
@@ -538,7 +576,8 @@ __device__ __noinline__ void gate_tile_generic(const TileGate tg, const PassGate
                                                const V *U, uint32_t ncls, bool needck, int tid, int nt) {
     const int d = g.d;
     for (uint32_t c = tid; c < ncls; c += nt) {
-        const uint32_t e0 = class_e0(c, g, ins_at(g, 0), true);
+        const uint32_t e0 = class_e0(c, g, Ins2{ins_at(g, 0), ins_at(g, g.nins > 1 ? 1 : 0), (uint32_t)g.nins},
+                                     g.nins > 1);
         if (needck && !class_ok(tg, g, e0)) continue;
         V x[kMaxDim];
         if (g.kind == kPGeneral) {
@@ -646,6 +685,8 @@ __global__ void __launch_bounds__(NT + kPassExtra, 1) k_gate_pass(const __grid_c
         d[0] = (uint32_t)g.d; d[1] = (uint32_t)g.kind; d[2] = g.ncls; d[3] = g.flags;
         d[4] = (uint32_t)g.nins; d[5] = (uint32_t)g.uoff; d[6] = g.active; d[7] = g.ins_s[0];
         d[8] = g.ins_m[0]; d[9] = g.ins_sd[0]; d[10] = g.ins_ps[0]; d[11] = 0;
+        const int i1 = g.nins > 1 ? 1 : 0;                // the second insertion (if any)
+        d[12] = g.ins_s[i1]; d[13] = g.ins_m[i1]; d[14] = g.ins_sd[i1]; d[15] = g.ins_ps[i1];
     }
     __syncthreads();
     const uint64_t first = blockIdx.x, step = gridDim.x;
@@ -702,8 +743,12 @@ __global__ void __launch_bounds__(NT + kPassExtra, 1) k_gate_pass(const __grid_c
             const PassGateP &g = p.g[gi];               // cold fields only (controls, more insertions)
             const uint32_t ga = gdesc_s + (uint32_t)(gi * kGDesc) * 4u;
             const uint4 h0 = lds_u128(ga);         // d, kind, ncls, flags
+#ifdef SV_AB_SKIP_KIND   // timing-only A/B builds (wrong results): drop one gate kind's work
+            if ((int)h0.y == SV_AB_SKIP_KIND || (SV_AB_SKIP_KIND == 3 && h0.y != 0)) continue;
+#endif
             const uint4 h1 = lds_u128(ga + 16u);   // nins, uoff, active, s
             const uint4 h2 = lds_u128(ga + 32u);   // m, sd, ps
+            const uint4 h3 = lds_u128(ga + 48u);   // second insertion: s, m, sd, ps
             TileGate tg;
             tg.LT = LT;
             tg.mLT = mLT;
@@ -712,7 +757,7 @@ __global__ void __launch_bounds__(NT + kPassExtra, 1) k_gate_pass(const __grid_c
             tg.flags = h0.w;
             tg.nins = h1.x;
             tg.active = h1.z;
-            tg.first = Ins1{h1.w, h2.x, h2.y, h2.z};
+            tg.first = Ins2{Ins1{h1.w, h2.x, h2.y, h2.z}, Ins1{h3.x, h3.y, h3.z, h3.w}, h1.x};
             tg.lowoff = si.lowoff[gi];
             tg.moff = moffs + gi * kMaxDim;
             tg.soff = soffs + gi * kMaxDim;
@@ -1046,13 +1091,17 @@ static bool pass_geometry(const Register &reg, const PassPlan &pp, double2 *psi,
 }
 
 // A control decided per tile (not on an in-tile digit): a run digit below min H (cls 1, or cls 3
-// when b_c d_c >= 2^31) or a digit outside the tile (cls 2).  Returns true for a run digit.
-static bool fill_tile_ctrl(PassCtrl &cc, const Register &reg, int c, uint32_t v, uint64_t R) {
+// when b_c d_c >= 2^31) or a digit constant over the tile (cls 2: outside the tile, or a run
+// digit whose stride is a multiple of the tile's run length LT — tiles start at multiples of LT,
+// so such a digit cannot change inside one; its value is that of the tile's first index and the
+// gate is skipped or applied whole, like an out-of-tile control).  Returns true for a run digit
+// checked per class.
+static bool fill_tile_ctrl(PassCtrl &cc, const Register &reg, int c, uint32_t v, uint64_t R, uint64_t LT) {
     const uint64_t dc = (uint64_t)reg.dims[c];
     cc.v = v;
     cc.d = (uint32_t)dc;
     cc.md = make_fastdiv32(cc.d).m;
-    if (reg.b[c] < R && reg.b[c] * dc < (1ull << 31)) {   // run digit: tile's run offset
+    if (reg.b[c] < R && reg.b[c] % LT != 0 && reg.b[c] * dc < (1ull << 31)) {   // run digit: tile's run offset
         cc.cls = 1;
         cc.w = (uint32_t)reg.b[c];
         cc.mw = make_fastdiv32(cc.w).m;
@@ -1061,14 +1110,14 @@ static bool fill_tile_ctrl(PassCtrl &cc, const Register &reg, int c, uint32_t v,
         cc.mb64 = make_fastdiv64(cc.M).m;
         return true;
     }
-    if (reg.b[c] < R) {                                    // b_c d_c >= 2^31: per-tile threshold
+    if (reg.b[c] < R && reg.b[c] % LT != 0) {              // b_c d_c >= 2^31: per-tile threshold
         cc.cls = 3;
         cc.b64 = reg.b[c];
         cc.mb64 = make_fastdiv64(cc.b64).m;
         cc.md64 = make_fastdiv64(dc).m;
         return true;
     }
-    cc.cls = 2;                                            // outside the tile: constant per tile
+    cc.cls = 2;                                            // constant over the tile
     cc.b64 = reg.b[c];
     cc.mb64 = make_fastdiv64(cc.b64).m;
     cc.md64 = make_fastdiv64(cc.d).m;
@@ -1227,7 +1276,7 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
                 cls_div *= dc;
                 continue;
             }
-            if (fill_tile_ctrl(q.c[nc++], reg, c, v, R)) q.flags |= kFRunCtrl;
+            if (fill_tile_ctrl(q.c[nc++], reg, c, v, R, LT)) q.flags |= kFRunCtrl;
         }
         q.nctrl = nc;
         if ((int)ins.size() > kMaxIns) return false;
@@ -1412,7 +1461,7 @@ bool build_stage_pass(const Register &reg, const std::vector<GateSpec> &gates, c
                     q.ic_v[k] = v;
                     continue;
                 }
-                if (fill_tile_ctrl(q.c[q.nctrl++], reg, c.q, v, R)) q.runck = 1;
+                if (fill_tile_ctrl(q.c[q.nctrl++], reg, c.q, v, R, LT)) q.runck = 1;
             }
         }
     }
