@@ -213,8 +213,11 @@ SV_API sv_status sv_get_info(sv_handle h, sv_info *out);
 #define SV_OPT_CTAS_PER_SM  4   /* resident CTAs per SM (tiled kernel)                           */
 #define SV_OPT_PROFILE      5   /* 1 = bracket every gate kernel with CUDA events on the handle's
                                    stream (read back with sv_profile_read)                        */
-#define SV_OPT_PASS_TILE    6   /* amplitudes per shared-memory tile of SV_BLOCK passes (<= 8192)  */
-#define SV_OPT_PASS_STAGES  7   /* shared-memory ring stages of the pass kernel (2..12)            */
+#define SV_OPT_PASS_TILE    6   /* SV_BLOCK: the planner's cap on a pass tile, in amplitudes (<= 8192;
+                                   default 3200)                                                   */
+#define SV_OPT_PASS_STAGES  7   /* SV_BLOCK: ring capacity = this many tiles of SV_OPT_PASS_TILE (2..12,
+                                   default 4); each pass re-cuts it into as many stages of its own
+                                   tile size as fit (at most 8), so smaller tiles get a deeper ring */
 #define SV_OPT_PASS_THREADS 8   /* compute threads per CTA of the pass kernel (256, 384 or 512)    */
 #define SV_OPT_PASS_GATES   9   /* max gates applied per pass (1..32)                              */
 #define SV_OPT_PASS_GROUPS 10   /* consumer warp groups of the pass kernel, each on its own tile

@@ -691,22 +691,27 @@ __global__ void __launch_bounds__(NT + kPassExtra, 1) k_gate_pass(const __grid_c
     __syncthreads();
     const uint64_t first = blockIdx.x, step = gridDim.x;
     if (first >= p.ntiles) return;
-    const uint64_t my = (p.ntiles - first + step - 1) / step;
+    // tiles of this CTA (< 2^32: ntiles <= D / b_{m0}); stage i mod S and ring phase (i / S) & 1
+    // are tracked incrementally (a 64-bit i % S was a runtime-library call per tile)
+    const uint32_t my = (uint32_t)((p.ntiles - first + step - 1) / step);
 
     if (warp == NT / 32) {
         // ---------------- load warp: tile i into stage i mod S once the store of tile i-S has read it
-        for (uint64_t i = 0; i < my; ++i) {
-            const int s = (int)(i % (uint64_t)S);
-            if (i >= (uint64_t)S) mbar_wait(&empty[s], (uint32_t)(((i - (uint64_t)S) / (uint64_t)S) & 1));
-            issue_loads(p, first + i * step, bufs + (size_t)s * TE, &full[s], &sinfo[s], lane);
+        int s = 0;
+        uint32_t ph = 0;
+        for (uint32_t i = 0; i < my; ++i) {
+            if (i >= (uint32_t)S) mbar_wait(&empty[s], ph ^ 1u);
+            issue_loads(p, first + (uint64_t)i * step, bufs + (size_t)s * TE, &full[s], &sinfo[s], lane);
+            if (++s == S) { s = 0; ph ^= 1u; }
         }
         return;
     }
     if (warp == NT / 32 + 1) {
         // ---------------- store warp: tile j back to HBM once computed; frees the stage when read
-        for (uint64_t j = 0; j < my; ++j) {
-            const int s = (int)(j % (uint64_t)S);
-            mbar_wait(&done[s], (uint32_t)((j / (uint64_t)S) & 1));
+        int s = 0;
+        uint32_t ph = 0;
+        for (uint32_t j = 0; j < my; ++j, (++s == S ? (s = 0, ph ^= 1u) : 0u)) {
+            mbar_wait(&done[s], ph);
             const StageInfo &si = sinfo[s];
             for (int m = lane; m < p.M; m += 32)
                 bulk_store(reinterpret_cast<V *>(p.psi) + si.ti.gbase + p.moff[m],
@@ -714,7 +719,7 @@ __global__ void __launch_bounds__(NT + kPassExtra, 1) k_gate_pass(const __grid_c
             bulk_commit();
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             __syncwarp();
-            if (lane == 0 && j + (uint64_t)S < my) mbar_arrive(&empty[s]);
+            if (lane == 0 && j + (uint32_t)S < my) mbar_arrive(&empty[s]);
         }
         bulk_wait_all();
         return;
@@ -722,8 +727,9 @@ __global__ void __launch_bounds__(NT + kPassExtra, 1) k_gate_pass(const __grid_c
 
     // ---------------- compute warps
     const int grp = tid / NTG, gtid = tid % NTG;
-    for (uint64_t i = (uint64_t)grp; i < my; i += (uint64_t)G) {
-        const int s = (int)(i % (uint64_t)S);
+    int s = grp;                    // G <= S: the group's first stage, phase 0
+    uint32_t ph = 0;
+    for (uint32_t i = (uint32_t)grp; i < my; i += (uint32_t)G, ((s += G) >= S ? (s -= S, ph ^= 1u) : 0u)) {
         V *buf = bufs + (size_t)s * TE;
         // With several groups, consecutive tiles of a stage belong to different groups, so this
         // group may reach tile i while the stage's previous tile (i - S, another group) is not
@@ -731,8 +737,8 @@ __global__ void __launch_bounds__(NT + kPassExtra, 1) k_gate_pass(const __grid_c
         // wait cannot tell a phase two steps back from a completed one.  Waiting first for
         // tile i - S to be consumed (done[s], whose previous phase this group completed itself)
         // puts full[s] exactly one phase before tile i.
-        if (G > 1 && i >= (uint64_t)S) mbar_wait(&done[s], (uint32_t)(((i - (uint64_t)S) / (uint64_t)S) & 1));
-        mbar_wait(&full[s], (uint32_t)((i / (uint64_t)S) & 1));
+        if (G > 1 && i >= (uint32_t)S) mbar_wait(&done[s], ph ^ 1u);
+        mbar_wait(&full[s], ph);
         const StageInfo &si = sinfo[s];
         const uint32_t len = si.ti.len;
         const uint32_t fire = si.fire;
@@ -965,20 +971,25 @@ __global__ void __launch_bounds__(NT + kPassExtra, 1) k_gate_stage(const __grid_
     __syncthreads();
     const uint64_t first = blockIdx.x, step = gridDim.x;
     if (first >= p.ntiles) return;
-    const uint64_t my = (p.ntiles - first + step - 1) / step;
+    // tiles of this CTA (< 2^32: ntiles <= D / b_{m0}); stage i mod S and ring phase (i / S) & 1
+    // are tracked incrementally (a 64-bit i % S was a runtime-library call per tile)
+    const uint32_t my = (uint32_t)((p.ntiles - first + step - 1) / step);
 
     if (warp == NT / 32) {
-        for (uint64_t i = 0; i < my; ++i) {
-            const int s = (int)(i % (uint64_t)S);
-            if (i >= (uint64_t)S) mbar_wait(&empty[s], (uint32_t)(((i - (uint64_t)S) / (uint64_t)S) & 1));
-            issue_loads(p, first + i * step, bufs + (size_t)s * TE, &full[s], &sinfo[s], lane);
+        int s = 0;
+        uint32_t ph = 0;
+        for (uint32_t i = 0; i < my; ++i) {
+            if (i >= (uint32_t)S) mbar_wait(&empty[s], ph ^ 1u);
+            issue_loads(p, first + (uint64_t)i * step, bufs + (size_t)s * TE, &full[s], &sinfo[s], lane);
+            if (++s == S) { s = 0; ph ^= 1u; }
         }
         return;
     }
     if (warp == NT / 32 + 1) {
-        for (uint64_t j = 0; j < my; ++j) {
-            const int s = (int)(j % (uint64_t)S);
-            mbar_wait(&done[s], (uint32_t)((j / (uint64_t)S) & 1));
+        int s = 0;
+        uint32_t ph = 0;
+        for (uint32_t j = 0; j < my; ++j, (++s == S ? (s = 0, ph ^= 1u) : 0u)) {
+            mbar_wait(&done[s], ph);
             const StageInfo &si = sinfo[s];
             for (int m = lane; m < p.M; m += 32)
                 bulk_store(reinterpret_cast<V *>(p.psi) + si.ti.gbase + p.moff[m],
@@ -986,18 +997,19 @@ __global__ void __launch_bounds__(NT + kPassExtra, 1) k_gate_stage(const __grid_
             bulk_commit();
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             __syncwarp();
-            if (lane == 0 && j + (uint64_t)S < my) mbar_arrive(&empty[s]);
+            if (lane == 0 && j + (uint32_t)S < my) mbar_arrive(&empty[s]);
         }
         bulk_wait_all();
         return;
     }
 
     const int grp = tid / NTG, gtid = tid % NTG;
-    for (uint64_t i = (uint64_t)grp; i < my; i += (uint64_t)G) {
-        const int s = (int)(i % (uint64_t)S);
+    int s = grp;                    // G <= S: the group's first stage, phase 0
+    uint32_t ph = 0;
+    for (uint32_t i = (uint32_t)grp; i < my; i += (uint32_t)G, ((s += G) >= S ? (s -= S, ph ^= 1u) : 0u)) {
         V *buf = bufs + (size_t)s * TE;
-        if (G > 1 && i >= (uint64_t)S) mbar_wait(&done[s], (uint32_t)(((i - (uint64_t)S) / (uint64_t)S) & 1));
-        mbar_wait(&full[s], (uint32_t)((i / (uint64_t)S) & 1));
+        if (G > 1 && i >= (uint32_t)S) mbar_wait(&done[s], ph ^ 1u);
+        mbar_wait(&full[s], ph);
         const StageInfo &si = sinfo[s];
         for (int st = 0; st < p.nstages; ++st) {
             if (st > 0) compute_barrier(1 + grp, NTG);
@@ -1293,14 +1305,34 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
     return p.ntiles > 0;
 }
 
+template <typename V>
+static size_t pass_smem_bytes(int S, int TE) {
+    // sized for the largest matrix pool so the attribute is set once per configuration
+    return (size_t)S * TE * sizeof(V) + (size_t)kPoolC * sizeof(V) +
+           (size_t)2 * kMaxPassGates * kMaxDim * sizeof(uint32_t) +
+           (size_t)kMaxPassGates * kGDesc * sizeof(uint32_t) +
+           (size_t)S * sizeof(StageInfo) + (size_t)3 * S * sizeof(uint64_t) + 16 + 16 + 32 * 16;
+}
+
+// Ring geometry of a pass: stage buffers hold the pass's actual tile (M LT amplitudes, rounded
+// to 16 bytes), and the configured capacity (pass_stages x pass_tile) is spent on as many stages
+// as fit (at most kMaxRing): a pass whose tile is smaller than pass_tile gets more tiles in flight
+// beyond the G being computed, so a group rarely waits for its next tile.
+template <typename V>
+static void pass_ring(const PassParams &p, const LaunchCfg &cfg, int &S, int &TE) {
+    constexpr int kMaxRing = 8;
+    TE = (int)((uint64_t)p.M * p.LT);
+    if (TE > cfg.pass_tile || TE <= 0) TE = cfg.pass_tile;
+    TE = (TE + 1) & ~1;
+    S = (int)(((int64_t)cfg.pass_stages * cfg.pass_tile) / TE);
+    if (S > kMaxRing) S = kMaxRing;
+    if (S < cfg.pass_stages) S = cfg.pass_stages;
+    while (S > cfg.pass_stages && pass_smem_bytes<V>(S, TE) > pass_smem_bytes<V>(cfg.pass_stages, cfg.pass_tile)) --S;
+}
+
 template <int NT, int G, typename V>
-cudaError_t launch_pass_t(const PassParams &p, cudaStream_t st, const LaunchCfg &cfg) {
-    const int S = cfg.pass_stages, TE = cfg.pass_tile;
-    // size for the largest matrix pool so the attribute and the occupancy are set once per config
-    const size_t smem = (size_t)S * TE * sizeof(V) + (size_t)kPoolC * sizeof(V) +
-                        (size_t)2 * kMaxPassGates * kMaxDim * sizeof(uint32_t) +
-                        (size_t)kMaxPassGates * kGDesc * sizeof(uint32_t) +
-                        (size_t)S * sizeof(StageInfo) + (size_t)3 * S * sizeof(uint64_t) + 16 + 16 + 32 * 16;
+cudaError_t launch_pass_t(const PassParams &p, cudaStream_t st, const LaunchCfg &cfg, int S, int TE) {
+    const size_t smem = pass_smem_bytes<V>(S, TE);
     static LaunchAttr attr;
     const int dv = current_device_slot();
     if (attr.configured[dv] < smem) {
@@ -1321,27 +1353,30 @@ cudaError_t launch_pass_t(const PassParams &p, cudaStream_t st, const LaunchCfg 
 }
 
 cudaError_t launch_pass(const PassParams &p, cudaStream_t st, const LaunchCfg &cfg) {
+    int S, TE;
     if (cfg.c64) {                                // complex64: 512 threads, 2 or 4 groups
-        if (cfg.pass_groups >= 4 && cfg.pass_stages >= 4) return launch_pass_t<512, 4, float2>(p, st, cfg);
-        return launch_pass_t<512, 2, float2>(p, st, cfg);
+        pass_ring<float2>(p, cfg, S, TE);
+        if (cfg.pass_groups >= 4 && S >= 4) return launch_pass_t<512, 4, float2>(p, st, cfg, S, TE);
+        return launch_pass_t<512, 2, float2>(p, st, cfg, S, TE);
     }
+    pass_ring<double2>(p, cfg, S, TE);
     int G = cfg.pass_groups;                      // one stage per group at least
-    while (G > 1 && cfg.pass_stages < G) G /= 2;
-    if (cfg.pass_threads >= 960) return launch_pass_t<960, 2, double2>(p, st, cfg);   // 32 warps, 64 registers
-    if (cfg.pass_threads >= 768) return launch_pass_t<768, 2, double2>(p, st, cfg);   // 26 warps, 72 registers
+    while (G > 1 && S < G) G /= 2;
+    if (cfg.pass_threads >= 960) return launch_pass_t<960, 2, double2>(p, st, cfg, S, TE);   // 32 warps, 64 registers
+    if (cfg.pass_threads >= 768) return launch_pass_t<768, 2, double2>(p, st, cfg, S, TE);   // 26 warps, 72 registers
     if (cfg.pass_threads >= 512) {
-        if (G >= 8) return launch_pass_t<512, 8, double2>(p, st, cfg);
-        if (G >= 4) return launch_pass_t<512, 4, double2>(p, st, cfg);
-        if (G == 2) return launch_pass_t<512, 2, double2>(p, st, cfg);
-        return launch_pass_t<512, 1, double2>(p, st, cfg);
+        if (G >= 8) return launch_pass_t<512, 8, double2>(p, st, cfg, S, TE);
+        if (G >= 4) return launch_pass_t<512, 4, double2>(p, st, cfg, S, TE);
+        if (G == 2) return launch_pass_t<512, 2, double2>(p, st, cfg, S, TE);
+        return launch_pass_t<512, 1, double2>(p, st, cfg, S, TE);
     }
     if (cfg.pass_threads >= 384) {
-        if (cfg.pass_groups == 3 && cfg.pass_stages >= 3) return launch_pass_t<384, 3, double2>(p, st, cfg);
-        if (G >= 2) return launch_pass_t<384, 2, double2>(p, st, cfg);
-        return launch_pass_t<384, 1, double2>(p, st, cfg);
+        if (cfg.pass_groups == 3 && S >= 3) return launch_pass_t<384, 3, double2>(p, st, cfg, S, TE);
+        if (G >= 2) return launch_pass_t<384, 2, double2>(p, st, cfg, S, TE);
+        return launch_pass_t<384, 1, double2>(p, st, cfg, S, TE);
     }
-    if (G >= 2) return launch_pass_t<256, 2, double2>(p, st, cfg);
-    return launch_pass_t<256, 1, double2>(p, st, cfg);
+    if (G >= 2) return launch_pass_t<256, 2, double2>(p, st, cfg, S, TE);
+    return launch_pass_t<256, 1, double2>(p, st, cfg, S, TE);
 }
 
 // ---- register-blocked stages: host side

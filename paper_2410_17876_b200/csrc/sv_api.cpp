@@ -60,8 +60,9 @@ void default_cfg(LaunchCfg &c, int device) {
     c.tile_stages = 3;
     c.ctas_per_sm = 2;
     c.num_sms = sms;
-    c.pass_tile = 2560;        // 5 stages x 2560 amplitudes, 4 consumer groups of 4 warps: c4 1588 -> 1440 ms,
-    c.pass_stages = 5;         //   c3 389 -> 387 ms against 4096 x 3 with 2 groups (profiles/r02/ab/r02s-r02u)
+    c.pass_tile = 3200;        // planner tile cap; the ring capacity (4 x 3200 amplitudes) is re-cut per pass
+    c.pass_stages = 4;         //   into as many stages of the pass's actual tile as fit (mgpass.cu pass_ring):
+                               //   c4 1305 -> 1257 ms, c3 369 -> 339 ms against 2560 x 5 (profiles/r02/ab/r02ad)
     c.pass_threads = 512;
     c.pass_gates = 32;         // with the in-tile set search: c3 -1.4%, c4 unchanged (ab/gates_window_*)
     c.pass_window = 256;       // gates scanned ahead when filling a pass (profiles/r01/ab/window_*, ab/gates_window_*)
@@ -97,9 +98,9 @@ sv_status state_init_device(sv_handle h, int device, void *cuda_stream, void *ex
     }
     h->cfg.c64 = h->c64 ? 1 : 0;
     if (h->c64) {                          // 8-byte elements: twice the amplitudes per stage (c4: 1.78 -> 1.25 s);
-        h->cfg.pass_tile = 8192;           // 3 stages and 2 groups stay best for complex64 (profiles/r02/ab/r02u)
-        h->cfg.pass_stages = 3;
-        h->cfg.pass_groups = 2;
+        h->cfg.pass_tile = 8192;           // ring of 3 x 8192, re-cut per pass; 4 groups where it yields
+        h->cfg.pass_stages = 3;            //   4+ stages (c4 765 -> 745 ms against 2 groups, r02/ab/r02ad)
+        h->cfg.pass_groups = 4;
     }
     const uint64_t bytes = h->local.D * h->elem;
     if (ext) {

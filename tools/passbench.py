@@ -44,7 +44,7 @@ def main():
     for te, s, nt, ng, gr, wi in itertools.product(*[[int(x) for x in a.split(",")] for a in
                                                      (args.tiles, args.stages, args.threads, args.gates, args.groups,
                                                       args.windows)]):
-        if te * (16 if args.dtype == 'c128' else 8) * s > 210 * 1024 or s < gr or (gr == 3 and nt % 96):
+        if te * (16 if args.dtype == 'c128' else 8) * s > 210 * 1024 or (gr == 3 and nt % 96):
             continue
         cases.append(("block", te, s, nt, ng, gr, wi))
     for kind, te, s, nt, ng, *rest in cases:
