@@ -268,8 +268,10 @@ typedef struct {
     double pass_ms;
     double pass_touched;       /* sum of T over the gates the passes applied                   */
     double pass_item_touched;  /* amplitudes read + written in shared memory, one round trip per
-                                  executed item (a gate, or a qubit pair applied as one class)   */
-    double pass_flops;         /* FP64 flops of the general items: 8 d per touched amplitude     */
+                                  executed item (a gate, a qubit pair applied as one class, or a
+                                  factored pair of general gates with d_a d_b <= 8)               */
+    double pass_flops;         /* FP64 flops of the general items: 8 d per touched amplitude
+                                  (8 (d_a + d_b) for a factored pair)                            */
     double pass_state_bytes;   /* 2 x elem x the local state per pass                           */
     double plan_ms;            /* host planning time (SV_BLOCK merge + pass planning) since the
                                   last reset                                                    */

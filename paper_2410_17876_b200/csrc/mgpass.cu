@@ -44,12 +44,17 @@ constexpr int kMaxMembers = 128;
 constexpr int kPoolC = 768;
 constexpr int kMaxPassCtrl = 4;
 constexpr int kMaxIns = 2 + kMaxPassCtrl;   // inserted in-tile digits: the target(s) + pinned controls
-constexpr int kMaxPairDim = 4;             // pair gates: d_a d_b <= 4 (qubit pairs)
+constexpr int kMaxPairDim = 4;             // dense pair gates (any kinds): d_a d_b <= 4 (qubit pairs)
+constexpr int kMaxFactoredPair = 8;        // factored general pairs: d_a <= d_b, d_a d_b <= 8, i.e.
+                                           //   (2,2), (2,3), (2,4); (3,3) spilled at 96 registers and
+                                           //   slowed every gate (c4 +8%, profiles/r02/ab/r02ae)
 constexpr int kGDesc = 16;                 // words of a gate's shared-memory descriptor
 
 // in-pass gate kinds: general y = U x (§2.3), monomial y_{sigma(j)} = c_j x_j (§2.1-2.2),
 // and the pure permutation (every moving coefficient exactly 1: no arithmetic at all)
-enum PassKind : int32_t { kPGeneral = 0, kPMonomial = 1, kPPerm = 2 };
+// and the factored pair (two general gates on two in-tile digits, U_b (x) U_a applied to the
+// d_a d_b-member class in registers as U_a on each digit-a column, then U_b on each digit-b row)
+enum PassKind : int32_t { kPGeneral = 0, kPMonomial = 1, kPPerm = 2, kPPair = 3 };
 
 // a control decided at run time (in-tile controls on H / low-prefix digits are enumerated)
 // Run-digit controls (digits below min H and above the low prefix) come in two forms:
@@ -77,6 +82,7 @@ enum PassFlags : uint32_t { kFRunCtrl = 4 };
 
 struct PassGateP {
     int32_t d, kind, nctrl, uoff;
+    int32_t da;           // kPPair: dimension of digit a (d = da * db)
     uint32_t flags;       // PassFlags: which in-tile control checks the gate needs
     uint32_t st, mst;     // smem stride of the target (+ magic)
     uint32_t ncls;        // classes per full tile: M LT / (d prod of the inserted control dims)
@@ -569,6 +575,78 @@ __device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const Pas
     }
 }
 
+// One factored pair gate on one tile (PAPER.md:222 applied twice): the class's DA*DB members
+// x[jb][ja] (member ja + DA jb) are gathered once; U_a (DA x DA, pool offset 0) acts on every
+// column jb, then U_b (DB x DB, offset DA*DA) on every row ja, and the results are scattered
+// once: one shared-memory round trip for two gates, DA^2 + DB^2 matrix reads per class (a dense
+// DA DB x DA DB Kronecker matrix would read (DA DB)^2 and cost DA DB / (DA + DB) times the FLOPs).
+template <int DA, int DB, int NT, bool CHECK, typename V>
+__device__ __forceinline__ void gate_tile_pair(const TileGate &tg, const PassGateP &g, V *__restrict__ buf,
+                                               const V *__restrict__ U, uint32_t cbeg, uint32_t cend,
+                                               uint32_t ncls, bool needck, int tid, uint32_t trash) {
+    constexpr int D = DA * DB;
+    uint32_t mo[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) mo[j] = lds_u32(tg.moff_s + 4u * j) * (uint32_t)sizeof(V);
+    const uint32_t sb = smem_u32(buf);
+    const Ins2 first = tg.first;
+    const bool more = tg.nins > 2;          // the pair's two target digits are always inserted
+#pragma unroll 1
+    for (uint32_t c0 = cbeg + (uint32_t)tid; c0 < cend; c0 += (uint32_t)NT) {
+        uint32_t e[1];
+        bool ok[1];
+        if (CHECK) {
+            class_batch<1, NT>(tg, g, first, more || true, c0, ncls, needck, e, ok);
+        } else {
+            e[0] = class_e0(c0, g, first, true);
+            ok[0] = true;
+        }
+        const uint32_t a = sb + e[0] * (uint32_t)sizeof(V);
+        V x[DB][DA];
+#pragma unroll
+        for (int jb = 0; jb < DB; ++jb)
+#pragma unroll
+            for (int ja = 0; ja < DA; ++ja) {
+                SV_DCHECK(e[0] * (uint32_t)sizeof(V) + mo[ja + DA * jb] + (uint32_t)sizeof(V) <= tg.tbytes);
+                x[jb][ja] = lds2<V>(a + mo[ja + DA * jb]);
+            }
+        // matrix entries re-read (broadcast) per column / row: holding U_a or U_b across the
+        // class's columns would cost up to 4 DB^2 registers on top of the 4 D of the class
+#pragma unroll
+        for (int jb = 0; jb < DB; ++jb) {          // U_a on column jb
+            const V *__restrict__ Ua = U + opaque_zero(c0 + (uint32_t)jb);
+            V t[DA];
+#pragma unroll
+            for (int i = 0; i < DA; ++i) {
+                V acc = cz<V>();
+#pragma unroll
+                for (int j = 0; j < DA; ++j) cfma(acc, Ua[i * DA + j], x[jb][j]);
+                t[i] = acc;
+            }
+#pragma unroll
+            for (int i = 0; i < DA; ++i) x[jb][i] = t[i];
+        }
+#pragma unroll
+        for (int ja = 0; ja < DA; ++ja) {          // U_b on row ja, scattered
+            const V *__restrict__ Ub = U + opaque_zero(c0 + (uint32_t)ja) + DA * DA;
+#pragma unroll
+            for (int i = 0; i < DB; ++i) {
+                V acc = cz<V>();
+#pragma unroll
+                for (int j = 0; j < DB; ++j) cfma(acc, Ub[i * DB + j], x[j][ja]);
+                sts2(CHECK ? (ok[0] ? a + mo[ja + DA * i] : trash) : a + mo[ja + DA * i], acc);
+            }
+        }
+    }
+}
+
+template <int DA, int DB, int NTG, typename V>
+__device__ __forceinline__ void apply_pair_tile(const TileGate &tg, const PassGateP &g, V *buf, const V *U,
+                                                uint32_t ncls, bool needck, int tid, uint32_t trash) {
+    if (needck) gate_tile_pair<DA, DB, NTG, true, V>(tg, g, buf, U, 0, ncls, ncls, true, tid, trash);
+    else gate_tile_pair<DA, DB, NTG, false, V>(tg, g, buf, U, 0, ncls, ncls, false, tid, trash);
+}
+
 // generic dimension (fused or d > 5): out of line so its 16-wide register arrays do not
 // inflate the kernel
 template <typename V>
@@ -684,7 +762,7 @@ __global__ void __launch_bounds__(NT + kPassExtra, 1) k_gate_pass(const __grid_c
         uint32_t *d = gdesc + tid * kGDesc;
         d[0] = (uint32_t)g.d; d[1] = (uint32_t)g.kind; d[2] = g.ncls; d[3] = g.flags;
         d[4] = (uint32_t)g.nins; d[5] = (uint32_t)g.uoff; d[6] = g.active; d[7] = g.ins_s[0];
-        d[8] = g.ins_m[0]; d[9] = g.ins_sd[0]; d[10] = g.ins_ps[0]; d[11] = 0;
+        d[8] = g.ins_m[0]; d[9] = g.ins_sd[0]; d[10] = g.ins_ps[0]; d[11] = (uint32_t)g.da;
         const int i1 = g.nins > 1 ? 1 : 0;                // the second insertion (if any)
         d[12] = g.ins_s[i1]; d[13] = g.ins_m[i1]; d[14] = g.ins_sd[i1]; d[15] = g.ins_ps[i1];
     }
@@ -753,7 +831,7 @@ __global__ void __launch_bounds__(NT + kPassExtra, 1) k_gate_pass(const __grid_c
             if ((int)h0.y == SV_AB_SKIP_KIND || (SV_AB_SKIP_KIND == 3 && h0.y != 0)) continue;
 #endif
             const uint4 h1 = lds_u128(ga + 16u);   // nins, uoff, active, s
-            const uint4 h2 = lds_u128(ga + 32u);   // m, sd, ps
+            const uint4 h2 = lds_u128(ga + 32u);   // m, sd, ps, da
             const uint4 h3 = lds_u128(ga + 48u);   // second insertion: s, m, sd, ps
             TileGate tg;
             tg.LT = LT;
@@ -773,7 +851,13 @@ __global__ void __launch_bounds__(NT + kPassExtra, 1) k_gate_pass(const __grid_c
             const bool needck = h0.w != 0 || len < LT;
             const V *U = Us + h1.y;
             const uint32_t ncls = h0.z;
-            switch (h0.x) {
+            if (h0.y == kPPair) {
+                switch (h2.w * 8u + h0.x / h2.w) {     // (d_a, d_b), d_a <= d_b
+                    case 2 * 8 + 2: apply_pair_tile<2, 2, NTG, V>(tg, g, buf, U, ncls, needck, gtid, trash); break;
+                    case 2 * 8 + 3: apply_pair_tile<2, 3, NTG, V>(tg, g, buf, U, ncls, needck, gtid, trash); break;
+                    default: apply_pair_tile<2, 4, NTG, V>(tg, g, buf, U, ncls, needck, gtid, trash); break;
+                }
+            } else switch (h0.x) {
                 case 2: apply_gate_tile<2, NT, NTG, V>(tg, g, (int)h0.y, buf, U, ncls, needck, gtid, trash); break;
                 case 3: apply_gate_tile<3, NT, NTG, V>(tg, g, (int)h0.y, buf, U, ncls, needck, gtid, trash); break;
                 case 4: apply_gate_tile<4, NT, NTG, V>(tg, g, (int)h0.y, buf, U, ncls, needck, gtid, trash); break;
@@ -1157,16 +1241,24 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
     // with the same controls (neither target controlling the other) when every gate in between
     // commutes with it; the two then act as one gate on the two digits, U_b (x) U_a, with
     // d_a d_b <= kMaxPairDim classes members: one shared-memory round trip instead of two.
+    // Two general gates may also pair up to d_a d_b <= kMaxFactoredPair: they are then applied
+    // factored (kPPair), U_a and U_b one after the other on the class held in registers.
     struct Item { int a, b; };          // gate indices (b = -1: single)
     std::vector<Item> items;
+    auto is_general = [&](int i) {
+        GatePlan gp;
+        std::string err;
+        return plan_gate(reg, gates[i], false, &gp, &err) == SV_OK && gp.kind == kGeneral;
+    };
     for (int i : pp.gates) {
         const GateSpec &g = gates[i];
         bool paired = false;
         for (int j = (int)items.size() - 1; j >= 0; --j) {
             Item &it = items[j];
             const GateSpec &h = gates[it.a];
-            if (it.b < 0 && h.target != g.target && h.d <= 5 && g.d <= 5 && h.d * g.d <= kMaxPairDim &&
-                same_controls(h, g)) {
+            const int dd = h.d * g.d;
+            if (it.b < 0 && h.target != g.target && h.d <= 5 && g.d <= 5 && same_controls(h, g) &&
+                (dd <= kMaxPairDim || (dd <= kMaxFactoredPair && is_general(it.a) && is_general(i)))) {
                 bool cross = false;
                 for (const auto &c : g.ctrl) cross = cross || c.q == h.target;
                 for (const auto &c : h.ctrl) cross = cross || c.q == g.target;
@@ -1208,6 +1300,28 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
             q.active = gp.active;
             const int need = gp.kind == kGeneral ? D * D : D;
             Ud.assign(gp.U, gp.U + need);
+        } else if (is_general(items[gi].a) && is_general(items[gi].b)) {
+            // factored general pair: digit a = the smaller dimension (the Kronecker member order
+            // is a layout choice; the two gates commute)
+            const GateSpec &h = gates[items[gi].b];
+            GatePlan hp;
+            if (plan_gate(reg, h, false, &hp, &err) != SV_OK || hp.kind != kGeneral) return false;
+            work->touched += (double)hp.touched;
+            const bool sw = hp.d < gp.d;
+            const GateSpec &ga = sw ? h : g, &gb = sw ? g : h;
+            const int da = ga.d, db = gb.d;
+            D = da * db;
+            const uint64_t sta = tile_stride(ga.target), stb = tile_stride(gb.target);
+            ins.assign({{sta, (uint32_t)da, 0u}, {stb, (uint32_t)db, 0u}});
+            cls_div = (uint64_t)D;
+            for (int jb = 0; jb < db; ++jb)
+                for (int ja = 0; ja < da; ++ja) moff[ja + da * jb] = (uint32_t)(ja * sta + jb * stb);
+            for (int J = 0; J < D; ++J) sig[J] = (uint32_t)J;
+            kind = -1;                                   // kPPair (set below)
+            q.da = da;
+            q.active = (1u << D) - 1u;
+            Ud.assign(ga.U.begin(), ga.U.end());
+            Ud.insert(Ud.end(), gb.U.begin(), gb.U.end());
         } else {
             const GateSpec &h = gates[items[gi].b];      // h acts on digit b (second), g on a
             GatePlan hp;
@@ -1249,7 +1363,7 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
             }
         }
         q.d = D;
-        q.kind = kind == kGeneral ? kPGeneral : kPMonomial;
+        q.kind = kind < 0 ? kPPair : kind == kGeneral ? kPGeneral : kPMonomial;
         {   // executed work of this item: its control-satisfying classes x moving members
             double cprod = 1.0;
             for (const auto &c : g.ctrl) cprod *= (double)reg.dims[c.q];
@@ -1257,6 +1371,7 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
             const double it = (double)reg.D / ((double)D * cprod) * nact;
             work->item_touched += it;
             if (kind == kGeneral) work->flops += 8.0 * D * it;
+            if (kind < 0) work->flops += 8.0 * (q.da + D / q.da) * it;     // U_a then U_b
         }
         if (q.kind == kPMonomial) {            // every moving coefficient exactly 1: pure data movement
             bool perm = true;

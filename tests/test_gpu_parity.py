@@ -520,6 +520,45 @@ def test_block_passes_random_sweep(P, pass_tile, pass_cfg):
         assert np.max(np.abs(got - ref)) <= 1e-12, (dims, s)
 
 
+@pytest.mark.parametrize("pass_cfg", [(512, 4, 4), (512, 2, 3), (256, 1, 2)])
+@pytest.mark.parametrize("dims", [[2, 3, 2, 4, 3, 2, 2, 3], [4, 2, 2, 3, 2, 4, 2], [3, 2, 3, 2, 2, 2, 3, 2, 2]])
+def test_block_passes_factored_pairs(P, dims, pass_cfg):
+    """Factored pair items (two general gates on different in-tile digits with the same controls,
+    d_a d_b <= 8: U_a then U_b on the class held in registers): layers of uncontrolled and
+    identically controlled Haar gates on qubit / qutrit / ququart targets, interleaved with
+    permutations that do or do not commute with them; ragged tiles (small tile caps); against
+    O-2, and the pass work shows fewer shared-memory round trips than gates."""
+    rng = np.random.default_rng(sum(dims) * 7 + pass_cfg[1])
+    n, D = len(dims), int(np.prod(dims))
+    gates = []
+    for layer in range(12):
+        ctrl = () if layer % 3 else (int(rng.integers(n)),)
+        vals = tuple(int(rng.integers(dims[c])) for c in ctrl)
+        for t in rng.permutation([q for q in range(n) if q not in ctrl]):
+            gates.append(Gate(int(t), ctrl, vals, haar_unitary(dims[int(t)], rng)))
+        t = int(rng.integers(n))
+        c = (t + 1) % n
+        gates.append(Gate(t, (c,), (dims[c] - 1,), shift_x(dims[t], 1)))
+    psi0 = random_state(D, 11)
+    ref = O2.run(dims, gates, psi0)
+    for tile in (512, 1280, 3200):
+        with P.State(dims) as st:
+            threads, groups, stages = pass_cfg
+            st.set_option(P.sv.SV_OPT_PASS_TILE, tile)
+            st.set_option(P.sv.SV_OPT_PASS_THREADS, threads)
+            st.set_option(P.sv.SV_OPT_PASS_GROUPS, groups)
+            st.set_option(P.sv.SV_OPT_PASS_STAGES, stages)
+            st.set_option(P.sv.SV_OPT_PASS_MERGE, 0)          # keep every gate (pairs, not products)
+            st.set_option(P.sv.SV_OPT_PROFILE, 1)
+            st.set_amplitudes(0, psi0)
+            st.apply_circuit(gates, block=True)
+            got = st.amplitudes()
+            prof = st.profile_read()
+        assert np.max(np.abs(got - ref)) <= 1e-12, tile
+        assert prof.pass_launches > 0
+        assert prof.pass_item_touched < 0.9 * prof.pass_touched, (prof.pass_item_touched, prof.pass_touched)
+
+
 @pytest.mark.parametrize("pass_cfg", PASS_CFGS)
 def test_block_passes_labelled_bit_exact(P, pass_cfg):
     """Permutation-only circuits through multi-gate passes: bit-exact against O-2."""
