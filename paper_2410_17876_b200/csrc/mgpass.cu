@@ -584,10 +584,10 @@ template <int DA, int DB, int NT, bool CHECK, typename V>
 __device__ __forceinline__ void gate_tile_pair(const TileGate &tg, const PassGateP &g, V *__restrict__ buf,
                                                const V *__restrict__ U, uint32_t cbeg, uint32_t cend,
                                                uint32_t ncls, bool needck, int tid, uint32_t trash) {
-    constexpr int D = DA * DB;
-    uint32_t mo[D];
-#pragma unroll
-    for (int j = 0; j < D; ++j) mo[j] = lds_u32(tg.moff_s + 4u * j) * (uint32_t)sizeof(V);
+    // member (ja, jb) sits at ja sa + jb sb from member 0 (two strides instead of a D-entry
+    // offset table: fewer live registers)
+    const uint32_t sa = lds_u32(tg.moff_s + 4u) * (uint32_t)sizeof(V);
+    const uint32_t sbb = lds_u32(tg.moff_s + 4u * DA) * (uint32_t)sizeof(V);
     const uint32_t sb = smem_u32(buf);
     const Ins2 first = tg.first;
     const bool more = tg.nins > 2;          // the pair's two target digits are always inserted
@@ -607,8 +607,8 @@ __device__ __forceinline__ void gate_tile_pair(const TileGate &tg, const PassGat
         for (int jb = 0; jb < DB; ++jb)
 #pragma unroll
             for (int ja = 0; ja < DA; ++ja) {
-                SV_DCHECK(e[0] * (uint32_t)sizeof(V) + mo[ja + DA * jb] + (uint32_t)sizeof(V) <= tg.tbytes);
-                x[jb][ja] = lds2<V>(a + mo[ja + DA * jb]);
+                SV_DCHECK(e[0] * (uint32_t)sizeof(V) + ja * sa + jb * sbb + (uint32_t)sizeof(V) <= tg.tbytes);
+                x[jb][ja] = lds2<V>(a + (uint32_t)ja * sa + (uint32_t)jb * sbb);
             }
         // matrix entries re-read (broadcast) per column / row: holding U_a or U_b across the
         // class's columns would cost up to 4 DB^2 registers on top of the 4 D of the class
@@ -634,7 +634,8 @@ __device__ __forceinline__ void gate_tile_pair(const TileGate &tg, const PassGat
                 V acc = cz<V>();
 #pragma unroll
                 for (int j = 0; j < DB; ++j) cfma(acc, Ub[i * DB + j], x[j][ja]);
-                sts2(CHECK ? (ok[0] ? a + mo[ja + DA * i] : trash) : a + mo[ja + DA * i], acc);
+                const uint32_t o = a + (uint32_t)ja * sa + (uint32_t)i * sbb;
+                sts2(CHECK ? (ok[0] ? o : trash) : o, acc);
             }
         }
     }
@@ -691,21 +692,22 @@ template <int D, int NT, int NTG, typename V>
 __device__ __forceinline__ void apply_gate_tile(const TileGate &tg, const PassGateP &g, int kind, V *buf,
                                                 const V *U, uint32_t ncls, bool needck, int tid, uint32_t trash) {
     constexpr int K = PassK<D, NT>::value;
-    // full batches of K classes per thread (no predicates at all without checks), then the
-    // remainder one class per thread (a predicated K-batch for the remainder was measured slower:
-    // its idle slots cost more than the interleaving gains, profiles/r02/ab)
-    const uint32_t full = ncls / (uint32_t)(NTG * K) * (uint32_t)(NTG * K);
+    // Gates that need per-class checks (ragged tile, run-digit controls) run one class per
+    // thread with the checks; the others take full batches of K classes per thread without any
+    // predicate, then the remainder one class per thread through the same checked code.  (A
+    // checked K-batch variant measured slower: c4 1246 -> 1200 ms, c3 343 -> 331 ms without it,
+    // profiles/r02/ab/r02af — one code path fewer per gate kind in the hot instruction stream;
+    // a predicated K-batch for the remainder was slower too: its idle slots cost more than the
+    // interleaving gains.)
+    const uint32_t full = needck ? 0u : ncls / (uint32_t)(NTG * K) * (uint32_t)(NTG * K);
     if (kind == kPGeneral) {
-        if (needck) gate_tile_general<D, K, NTG, true, V>(tg, g, buf, U, 0, full, ncls, true, tid, trash);
-        else gate_tile_general<D, K, NTG, false, V>(tg, g, buf, U, 0, full, ncls, false, tid, trash);
+        if (full) gate_tile_general<D, K, NTG, false, V>(tg, g, buf, U, 0, full, ncls, false, tid, trash);
         gate_tile_general<D, 1, NTG, true, V>(tg, g, buf, U, full, ncls, ncls, needck, tid, trash);
     } else if (kind == kPPerm) {
-        if (needck) gate_tile_monomial<D, K, NTG, true, true, V>(tg, g, buf, U, 0, full, ncls, true, tid, trash);
-        else gate_tile_monomial<D, K, NTG, true, false, V>(tg, g, buf, U, 0, full, ncls, false, tid, trash);
+        if (full) gate_tile_monomial<D, K, NTG, true, false, V>(tg, g, buf, U, 0, full, ncls, false, tid, trash);
         gate_tile_monomial<D, 1, NTG, true, true, V>(tg, g, buf, U, full, ncls, ncls, needck, tid, trash);
     } else {
-        if (needck) gate_tile_monomial<D, K, NTG, false, true, V>(tg, g, buf, U, 0, full, ncls, true, tid, trash);
-        else gate_tile_monomial<D, K, NTG, false, false, V>(tg, g, buf, U, 0, full, ncls, false, tid, trash);
+        if (full) gate_tile_monomial<D, K, NTG, false, false, V>(tg, g, buf, U, 0, full, ncls, false, tid, trash);
         gate_tile_monomial<D, 1, NTG, false, true, V>(tg, g, buf, U, full, ncls, ncls, needck, tid, trash);
     }
 }
