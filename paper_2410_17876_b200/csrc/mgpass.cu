@@ -680,11 +680,15 @@ __device__ __noinline__ void gate_tile_generic(const TileGate tg, const PassGate
 // two classes for d <= 3 and one for d = 4, 5 measured best (c4 1816 -> 1628 ms, c3 439 -> 394 ms
 // against the earlier 4/3/2/2, same box; profiles/r02/ab/r02m_ksweep, r02n_ksweep2): fewer
 // in-flight classes, no spills.  384 threads (128 registers) keep the larger batches.
+#ifndef SV_PASSK512               // K for d = 2, 3, 4, 5 at 512+ threads as 4 decimal digits
+#define SV_PASSK512 2211          //   (timing builds override; 2221 / 4211 / 2111 / 1111 measured
+#endif                            //   slower, profiles/r02/ab/r02ai)
+constexpr int kPassK512[4] = {SV_PASSK512 / 1000 % 10, SV_PASSK512 / 100 % 10, SV_PASSK512 / 10 % 10, SV_PASSK512 % 10};
 template <int D, int NT> struct PassK { static constexpr int value = 1; };
-template <int NT> struct PassK<2, NT> { static constexpr int value = NT >= 512 ? 2 : 4; };
-template <int NT> struct PassK<3, NT> { static constexpr int value = NT >= 512 ? 2 : 4; };
-template <int NT> struct PassK<4, NT> { static constexpr int value = NT >= 512 ? 1 : 3; };
-template <int NT> struct PassK<5, NT> { static constexpr int value = NT >= 512 ? 1 : (NT >= 384 ? 2 : 3); };
+template <int NT> struct PassK<2, NT> { static constexpr int value = NT >= 512 ? kPassK512[0] : 4; };
+template <int NT> struct PassK<3, NT> { static constexpr int value = NT >= 512 ? kPassK512[1] : 4; };
+template <int NT> struct PassK<4, NT> { static constexpr int value = NT >= 512 ? kPassK512[2] : 3; };
+template <int NT> struct PassK<5, NT> { static constexpr int value = NT >= 512 ? kPassK512[3] : (NT >= 384 ? 2 : 3); };
 
 // NT = compute threads of the CTA (sets the register budget), NTG = threads of one consumer
 // group (the class stride)
