@@ -184,3 +184,31 @@ def test_loopback_relabel_and_phase_c64(P, nranks):
             got = st.amplitudes()
             assert st.info().exchanges == 0
         assert np.linalg.norm(got - ref) <= bound(gates, dims, np.sqrt(2) * U32), block
+
+
+def test_c64_factored_pairs(P):
+    """Factored pair items in the complex64 pass kernel (two general gates on different in-tile
+    digits with the same controls, U_a then U_b on the class in registers): against the fp64
+    oracle within the fp32 bound (each factor rounds like a separate gate), with fewer
+    shared-memory round trips than gates in the pass work."""
+    dims = [4, 2, 2, 3, 2, 4, 2, 2]            # L = b_4 = 48: 16-byte aligned complex64 tiles
+    rng = np.random.default_rng(21)
+    n, D = len(dims), int(np.prod(dims))
+    gates = []
+    for layer in range(10):
+        ctrl = () if layer % 3 else (int(rng.integers(n)),)
+        vals = tuple(int(rng.integers(dims[c])) for c in ctrl)
+        for t in rng.permutation([q for q in range(n) if q not in ctrl]):
+            gates.append(Gate(int(t), ctrl, vals, haar_unitary(dims[int(t)], rng)))
+    psi0 = random_state(D, 5)
+    ref = O2.run(dims, gates, psi0)
+    with P.State(dims, dtype="c64") as st:
+        st.set_option(P.sv.SV_OPT_PASS_MERGE, 0)
+        st.set_option(P.sv.SV_OPT_PROFILE, 1)
+        st.set_amplitudes(0, psi0)
+        st.apply_circuit(gates, block=True)
+        got = st.amplitudes()
+        prof = st.profile_read()
+    assert np.linalg.norm(got - ref) <= bound(gates, dims, np.sqrt(2) * U32)
+    assert prof.pass_launches > 0
+    assert prof.pass_item_touched < 0.9 * prof.pass_touched
