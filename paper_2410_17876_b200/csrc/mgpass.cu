@@ -78,7 +78,8 @@ struct PassCtrl {
 // or none (mode 0); t < 2^30 is clamped (tiles are at most 8192 positions long).
 constexpr uint32_t kCls3Mask = (1u << 30) - 1u;
 
-enum PassFlags : uint32_t { kFRunCtrl = 4 };
+// kFTrans: the gate's classes are enumerated target-run-major (class_idx<true>)
+enum PassFlags : uint32_t { kFRunCtrl = 4, kFTrans = 8 };
 
 struct PassGateP {
     int32_t d, kind, nctrl, uoff;
@@ -329,6 +330,23 @@ __device__ __forceinline__ uint32_t class_e0(uint32_t c, const PassGateP &g, con
     return e;
 }
 
+// Class index -> member-0 tile index.  TR (kFTrans gates: a lone low-prefix target of stride
+// st < 8 with st d odd and d = 3 or 5, no enumerated control): class c = r O + o sits at
+// o (st d) + r (o < O = ncls / st, r < st; O in the second insertion slot), so consecutive lanes
+// step st d (odd) 16-byte slots and hit distinct banks, where the natural order (r fastest) puts
+// runs of st lanes st d apart (st = 5, d = 5: 2-way conflicts).  A template parameter, so the
+// other gates' class loops carry no extra instruction.
+template <bool TR>
+__device__ __forceinline__ uint32_t class_idx(uint32_t c, const PassGateP &g, const Ins2 &ins, bool more) {
+    if constexpr (TR) {
+        uint32_t o;
+        const uint32_t r = tdiv(c, ins.b.s, ins.b.m, o);
+        return o * ins.a.sd + r;
+    } else {
+        return class_e0(c, g, ins, more);
+    }
+}
+
 // What one gate needs to decide its classes inside the current tile.
 struct TileGate {
     uint32_t LT, mLT, len, flags;
@@ -371,7 +389,7 @@ __device__ __forceinline__ bool class_ok(const TileGate &tg, const PassGateP &g,
 // The K classes c0, c0+NT, ..., c0+(K-1)NT of one thread iteration (a warp's accesses stay
 // contiguous for strides >= 32): member-0 smem index and whether the class exists and fires.
 // Classes past ncls read index 0 and do not store.
-template <int K, int NT>
+template <int K, int NT, bool TR = false>
 __device__ __forceinline__ void class_batch(const TileGate &tg, const PassGateP &g, const Ins2 &first, bool more,
                                             uint32_t c0, uint32_t ncls, bool needck, uint32_t (&e)[K],
                                             bool (&ok)[K]) {
@@ -379,7 +397,7 @@ __device__ __forceinline__ void class_batch(const TileGate &tg, const PassGateP 
     for (int k = 0; k < K; ++k) {
         const uint32_t c = c0 + (uint32_t)(k * NT);
         ok[k] = c < ncls;
-        e[k] = ok[k] ? class_e0(c, g, first, more) : 0u;
+        e[k] = ok[k] ? class_idx<TR>(c, g, first, more) : 0u;
         if (needck && ok[k]) ok[k] = class_ok(tg, g, e[k]);
     }
 }
@@ -428,7 +446,7 @@ template <int D> struct PassColOuter { static constexpr bool value = (SV_COLOUTE
 // that does not exist or fire (CHECK) computes on harmless inputs and stores to the lane's trash
 // slot, so the K classes' FMA chains stay in one basic block and interleave (with a branch per
 // store, ptxas ran the classes' dependent DFMA chains one after another).
-template <int D, int K, int NT, bool CHECK, typename V>
+template <int D, int K, int NT, bool CHECK, typename V, bool TR = false>
 __device__ __forceinline__ void gate_tile_general(const TileGate &tg, const PassGateP &g, V *__restrict__ buf,
                                                   const V *__restrict__ U, uint32_t cbeg, uint32_t cend,
                                                   uint32_t ncls, bool needck, int tid, uint32_t trash) {
@@ -445,11 +463,11 @@ __device__ __forceinline__ void gate_tile_general(const TileGate &tg, const Pass
         uint32_t e[K];
         bool ok[K];
         if (CHECK) {
-            class_batch<K, NT>(tg, g, first, more, c0, ncls, needck, e, ok);
+            class_batch<K, NT, TR>(tg, g, first, more, c0, ncls, needck, e, ok);
         } else {
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                e[k] = class_e0(c0 + (uint32_t)(k * NT), g, first, more);
+                e[k] = class_idx<TR>(c0 + (uint32_t)(k * NT), g, first, more);
                 ok[k] = true;
             }
         }
@@ -511,7 +529,7 @@ __device__ __forceinline__ void gate_tile_general(const TileGate &tg, const Pass
 // tile; PERM: every moving coefficient is exactly 1, so the gate only moves data.  Only the
 // members that move or scale are read and written (select-form predicated gathers: a branch
 // per member makes ptxas spill the array); skipped classes store to the trash slot.
-template <int D, int K, int NT, bool PERM, bool CHECK, typename V>
+template <int D, int K, int NT, bool PERM, bool CHECK, typename V, bool TR = false>
 __device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const PassGateP &g, V *__restrict__ buf,
                                                    const V *__restrict__ U, uint32_t cbeg, uint32_t cend,
                                                    uint32_t ncls, bool needck, int tid, uint32_t trash) {
@@ -533,11 +551,11 @@ __device__ __forceinline__ void gate_tile_monomial(const TileGate &tg, const Pas
         uint32_t e[K];
         bool ok[K];
         if (CHECK) {
-            class_batch<K, NT>(tg, g, first, more, c0, ncls, needck, e, ok);
+            class_batch<K, NT, TR>(tg, g, first, more, c0, ncls, needck, e, ok);
         } else {
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                e[k] = class_e0(c0 + (uint32_t)(k * NT), g, first, more);
+                e[k] = class_idx<TR>(c0 + (uint32_t)(k * NT), g, first, more);
                 ok[k] = true;
             }
         }
@@ -696,6 +714,19 @@ template <int D, int NT, int NTG, typename V>
 __device__ __forceinline__ void apply_gate_tile(const TileGate &tg, const PassGateP &g, int kind, V *buf,
                                                 const V *U, uint32_t ncls, bool needck, int tid, uint32_t trash) {
     constexpr int K = PassK<D, NT>::value;
+    if constexpr (D == 3 || D == 5) {
+        if (tg.flags & kFTrans) {      // general or permutation, see class_idx
+            const uint32_t full = needck ? 0u : ncls / (uint32_t)(NTG * K) * (uint32_t)(NTG * K);
+            if (kind == kPGeneral) {
+                if (full) gate_tile_general<D, K, NTG, false, V, true>(tg, g, buf, U, 0, full, ncls, false, tid, trash);
+                gate_tile_general<D, 1, NTG, true, V, true>(tg, g, buf, U, full, ncls, ncls, needck, tid, trash);
+            } else {
+                if (full) gate_tile_monomial<D, K, NTG, true, false, V, true>(tg, g, buf, U, 0, full, ncls, false, tid, trash);
+                gate_tile_monomial<D, 1, NTG, true, true, V, true>(tg, g, buf, U, full, ncls, ncls, needck, tid, trash);
+            }
+            return;
+        }
+    }
     // Gates that need per-class checks (ragged tile, run-digit controls) run one class per
     // thread with the checks; the others take full batches of K classes per thread without any
     // predicate, then the remainder one class per thread through the same checked code.  (A
@@ -769,7 +800,7 @@ __global__ void __launch_bounds__(NT + kPassExtra, 1) k_gate_pass(const __grid_c
         d[0] = (uint32_t)g.d; d[1] = (uint32_t)g.kind; d[2] = g.ncls; d[3] = g.flags;
         d[4] = (uint32_t)g.nins; d[5] = (uint32_t)g.uoff; d[6] = g.active; d[7] = g.ins_s[0];
         d[8] = g.ins_m[0]; d[9] = g.ins_sd[0]; d[10] = g.ins_ps[0]; d[11] = (uint32_t)g.da;
-        const int i1 = g.nins > 1 ? 1 : 0;                // the second insertion (if any)
+        const int i1 = (g.nins > 1 || (g.flags & kFTrans)) ? 1 : 0;   // the second insertion (or O)
         d[12] = g.ins_s[i1]; d[13] = g.ins_m[i1]; d[14] = g.ins_sd[i1]; d[15] = g.ins_ps[i1];
     }
     __syncthreads();
@@ -854,7 +885,7 @@ __global__ void __launch_bounds__(NT + kPassExtra, 1) k_gate_pass(const __grid_c
             tg.moff_s = smem_u32(tg.moff);
             tg.lowoff_s = smem_u32(tg.lowoff);
             tg.soff_s = smem_u32(tg.soff);
-            const bool needck = h0.w != 0 || len < LT;
+            const bool needck = (h0.w & kFRunCtrl) != 0 || len < LT;
             const V *U = Us + h1.y;
             const uint32_t ncls = h0.z;
             if (h0.y == kPPair) {
@@ -1422,6 +1453,12 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
             q.ins_ps[i] = (uint32_t)(ins[i].s * ins[i].pin);
         }
         q.ncls = (uint32_t)((uint64_t)p.M * LT / cls_div);
+        if (items[gi].b < 0 && q.nins == 1 && (D == 3 || D == 5) && (q.kind == kPGeneral || q.kind == kPPerm) &&
+            st < 8 && ((st * (uint64_t)D) & 1) && q.ncls % st == 0) {
+            q.flags |= kFTrans;                  // see class_idx: O = ncls / st in the second slot
+            q.ins_s[1] = q.ncls / (uint32_t)st;
+            q.ins_m[1] = make_fastdiv32(q.ins_s[1]).m;
+        }
     }
     return p.ntiles > 0;
 }
