@@ -241,6 +241,13 @@ SV_API sv_status sv_get_info(sv_handle h, sv_info *out);
 #define SV_OPT_PASS_LOW    18   /* SV_BLOCK: the low prefix every pass tile holds whole = the qudits whose
                                    stride is below this many amplitudes (default 32: tile runs, i.e.
                                    bulk copies, of >= 512 B for complex128)                          */
+#define SV_OPT_PASS_ABSORB 19   /* SV_BLOCK (per-gate pass kernel): 1 (default) = a pure permutation gate
+                                   (unit coefficients) whose target is a member digit
+                                   of the pass tile and whose controls are member digits or constant
+                                   over the tile is not a compute item: moved to the front of the pass
+                                   (past the earlier gates it commutes with) it relabels which global
+                                   member each tile slot is loaded from, else moved to the back it
+                                   relabels where each slot is stored; 0 = every gate is an item     */
 #define SV_OPT_PASS_KERNEL 16   /* SV_BLOCK pass kernel: 0 (default) = per-gate (k_gate_pass: every gate
                                    sweeps the shared-memory tile, one group barrier per gate); 1 =
                                    register-blocked stages (k_gate_stage: consecutive gates on a pair of

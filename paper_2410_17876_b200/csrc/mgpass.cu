@@ -95,6 +95,24 @@ struct PassGateP {
     PassCtrl c[kMaxPassCtrl];
 };
 
+// A pure permutation gate absorbed into the tile's member addressing (no compute item): its
+// target is a member digit (in H) and each control is a member digit or constant over the tile,
+// so on every tile it moves whole member runs, member x to member pi(x).  Moved to the front of
+// the pass (it commutes with every earlier item) it relabels the load sources — slot y is loaded
+// from global member pi^-1(y) — or moved to the back, the store targets — slot x is stored to
+// member pi(x).  The data never passes through the compute warps (a monomial
+// gate with unit coefficients only relabels amplitudes).
+constexpr int kMaxAbs = 8;
+constexpr int kMaxAbsOut = 2;       // out-of-tile controls per absorbed gate
+struct AbsPerm {
+    uint8_t store, d, nmc, noc;     // phase (0 load, 1 store), target dim, member / outside controls
+    uint32_t wt;                    // member radix weight of the target digit
+    uint8_t mc_w[kMaxPassCtrl], mc_d[kMaxPassCtrl], mc_v[kMaxPassCtrl];   // member controls
+    int8_t sig[kMaxDim], inv[kMaxDim];                                      // sigma, sigma^-1
+    uint64_t oc_b[kMaxAbsOut], oc_mb[kMaxAbsOut], oc_md[kMaxAbsOut];      // outside: stride, magics
+    uint32_t oc_d[kMaxAbsOut], oc_v[kMaxAbsOut];
+};
+
 struct PassParams {
     double2 *psi;
     int32_t nrem;
@@ -110,6 +128,8 @@ struct PassParams {
     uint32_t moff_t[kMaxPassGates][kMaxDim];   // per gate: tile offset of class member j
     uint32_t soff_t[kMaxPassGates][kMaxDim];   // per gate: offset of member sigma(j) (monomial)
     double2 U[kPoolC];    // general: row-major d x d; monomial: coefficient per member
+    int32_t nabs;         // absorbed permutations (load phase first, each phase in gate order)
+    AbsPerm ab[kMaxAbs];
 };
 
 static_assert(sizeof(PassParams) <= 32764, "kernel parameter space (32 KB on sm_100)");
@@ -242,8 +262,23 @@ __device__ __forceinline__ TileInfo tile_info(const PP &p, uint64_t t) {
 struct StageInfo {
     TileInfo ti;
     uint32_t fire;                                   // bit g: gate g's out-of-tile controls hold
+    uint32_t afire;                                  // bit a: absorbed permutation a's likewise
     uint32_t lowoff[kMaxPassGates][kMaxPassCtrl];    // (s0 mod b_c d_c) for run-digit controls
 };
+
+// member x after absorbed permutation a (forward sigma, or sigma^-1 when inverse): controls
+// read the label's member digits; target and controls are distinct digits, so the test holds
+// before and after the move
+__device__ __forceinline__ uint32_t abs_move(const AbsPerm &a, uint32_t x, bool inverse) {
+    for (int k = 0; k < a.nmc; ++k)
+        if ((x / a.mc_w[k]) % a.mc_d[k] != a.mc_v[k]) return x;
+    const uint32_t dig = (x / a.wt) % a.d;
+    const uint32_t to = (uint32_t)(inverse ? a.inv[dig] : a.sig[dig]);
+    return x + to * a.wt - dig * a.wt;
+}
+
+template <class PP> struct HasAbs { static constexpr bool value = false; };
+template <> struct HasAbs<PassParams> { static constexpr bool value = true; };
 
 // PP: PassParams or StageParams (same geometry fields; g[i].nctrl / g[i].c[] = the controls
 // decided per tile)
@@ -279,17 +314,39 @@ __device__ __forceinline__ void issue_loads(const PP &p, uint64_t t, V *buf, uin
         }
     }
     const uint32_t bits = __ballot_sync(0xffffffffu, fire && lane < p.ngates);
+    uint32_t abits = 0;
+    if constexpr (HasAbs<PP>::value) {       // lane a decides absorbed permutation a's out-of-tile controls
+        bool af = lane < p.nabs;
+        if (af) {
+            const AbsPerm &a = p.ab[lane];
+            for (int k = 0; k < a.noc; ++k) {
+                uint64_t r;
+                const uint64_t q = fastdiv64(ti.gbase, a.oc_b[k], a.oc_mb[k], r);
+                fastdiv64(q, a.oc_d[k], a.oc_md[k], r);
+                af = af && (r == a.oc_v[k]);
+            }
+        }
+        abits = __ballot_sync(0xffffffffu, af);
+    }
     if (lane == 0) {
         si->ti = ti;
         si->fire = bits;
+        si->afire = abits;
     }
     __syncwarp();
     SV_DCHECK(ti.len <= p.LT && ti.len > 0);
     if (lane == 0) mbar_expect_tx(bar, (uint32_t)p.M * ti.len * (uint32_t)sizeof(V));
     __syncwarp();
-    for (int m = lane; m < p.M; m += 32)
-        bulk_load(buf + (size_t)m * p.LT, reinterpret_cast<const V *>(p.psi) + ti.gbase + p.moff[m],
+    for (int m = lane; m < p.M; m += 32) {
+        uint32_t src = (uint32_t)m;
+        if constexpr (HasAbs<PP>::value) {   // load-phase permutations, last first, inverted
+            for (int a = p.nabs - 1; a >= 0; --a)
+                if (((abits >> a) & 1) && !p.ab[a].store) src = abs_move(p.ab[a], src, true);
+            SV_DCHECK(src < (uint32_t)p.M);
+        }
+        bulk_load(buf + (size_t)m * p.LT, reinterpret_cast<const V *>(p.psi) + ti.gbase + p.moff[src],
                   ti.len * (uint32_t)sizeof(V), bar);
+    }
 }
 
 // In-tile division (x < 2^16, d < 2^16): with m = floor(2^32/d) + 1, umulhi(x, m) is exact
@@ -828,9 +885,15 @@ __global__ void __launch_bounds__(NT + kPassExtra, 1) k_gate_pass(const __grid_c
         for (uint32_t j = 0; j < my; ++j, (++s == S ? (s = 0, ph ^= 1u) : 0u)) {
             mbar_wait(&done[s], ph);
             const StageInfo &si = sinfo[s];
-            for (int m = lane; m < p.M; m += 32)
-                bulk_store(reinterpret_cast<V *>(p.psi) + si.ti.gbase + p.moff[m],
+            const uint32_t abits = si.afire;
+            for (int m = lane; m < p.M; m += 32) {
+                uint32_t dst = (uint32_t)m;             // store-phase permutations, in order
+                for (int a = 0; a < p.nabs; ++a)
+                    if (((abits >> a) & 1) && p.ab[a].store) dst = abs_move(p.ab[a], dst, false);
+                SV_DCHECK(dst < (uint32_t)p.M);
+                bulk_store(reinterpret_cast<V *>(p.psi) + si.ti.gbase + p.moff[dst],
                            bufs + (size_t)s * TE + (size_t)m * p.LT, si.ti.len * (uint32_t)sizeof(V));
+            }
             bulk_commit();
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             __syncwarp();
@@ -1259,7 +1322,7 @@ static bool fill_tile_ctrl(PassCtrl &cc, const Register &reg, int c, uint32_t v,
 
 // Build the pass parameters; returns false if the pass does not fit this kernel.
 bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const PassPlan &pp, double2 *psi,
-                int TE, PassParams &p, PassWork *work) {
+                int TE, PassParams &p, PassWork *work, bool absorb) {
     std::memset(&p, 0, sizeof(p));
     if ((int)pp.gates.size() > kMaxPassGates || pp.tile > (uint64_t)TE) return false;
     std::vector<uint64_t> W;
@@ -1287,7 +1350,83 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
         std::string err;
         return plan_gate(reg, gates[i], false, &gp, &err) == SV_OK && gp.kind == kGeneral;
     };
-    for (int i : pp.gates) {
+    // Absorbed permutations (AbsPerm): a pure permutation on a member digit whose controls are
+    // member digits or constant over the tile, moved to the front of the pass past the earlier
+    // gates it commutes with (load phase), else to the back past the later ones (store phase).
+    std::vector<int> rest;              // the gates left for compute items, in pass order
+    *work = PassWork{};
+    p.nabs = 0;
+    {
+        auto member_digit = [&](int q) { return std::find(pp.H.begin(), pp.H.end(), q) != pp.H.end(); };
+        auto absorbable = [&](int i) {
+            const GateSpec &g = gates[i];
+            if (!absorb || !member_digit(g.target) || g.d > kMaxDim) return false;
+            int noc = 0;
+            for (const auto &c : g.ctrl) {
+                if (member_digit(c.q)) continue;
+                if (c.q < m0) return false;                                // low prefix: per class
+                const uint64_t bc = reg.b[c.q];
+                if (bc < R && bc % LT != 0) return false;                  // run digit: per class
+                if (++noc > kMaxAbsOut) return false;
+            }
+            if ((int)g.ctrl.size() - noc > kMaxPassCtrl) return false;
+            GatePlan gp;
+            std::string err;
+            if (plan_gate(reg, g, false, &gp, &err) != SV_OK || gp.kind != kMonomial) return false;
+            for (int j = 0; j < gp.d; ++j)
+                if (!(gp.U[j].x == 1.0 && gp.U[j].y == 0.0)) return false;
+            return true;
+        };
+        std::vector<int> load, store, mid;
+        for (int i : pp.gates) {        // front: commutes with every earlier non-absorbed gate
+            bool ok = (int)load.size() < kMaxAbs && absorbable(i);
+            for (size_t k = 0; ok && k < mid.size(); ++k) ok = commute(gates[i], gates[mid[k]]);
+            (ok ? load : mid).push_back(i);
+        }
+        std::vector<int> later;         // back: commutes with every later non-absorbed gate
+        for (int k = (int)mid.size() - 1; k >= 0; --k) {
+            const int i = mid[k];
+            bool ok = (int)(load.size() + store.size()) < kMaxAbs && absorbable(i);
+            for (size_t j = 0; ok && j < later.size(); ++j) ok = commute(gates[i], gates[later[j]]);
+            (ok ? store : later).push_back(i);
+        }
+        std::reverse(store.begin(), store.end());
+        rest.assign(later.rbegin(), later.rend());
+        auto put = [&](int i, bool st) {
+            const GateSpec &g = gates[i];
+            GatePlan gp;
+            std::string err;
+            plan_gate(reg, g, false, &gp, &err);
+            work->touched += (double)gp.touched;
+            AbsPerm &a = p.ab[p.nabs++];
+            a.store = st ? 1 : 0;
+            a.d = (uint8_t)g.d;
+            a.wt = (uint32_t)W[g.target];
+            for (int j = 0; j < kMaxDim; ++j) { a.sig[j] = (int8_t)j; a.inv[j] = (int8_t)j; }
+            for (int j = 0; j < g.d; ++j) {
+                a.sig[j] = (int8_t)gp.sigma[j];
+                a.inv[gp.sigma[j]] = (int8_t)j;
+            }
+            for (const auto &c : g.ctrl) {
+                if (member_digit(c.q)) {
+                    a.mc_w[a.nmc] = (uint8_t)W[c.q];
+                    a.mc_d[a.nmc] = (uint8_t)reg.dims[c.q];
+                    a.mc_v[a.nmc] = (uint8_t)c.v;
+                    ++a.nmc;
+                } else {
+                    a.oc_b[a.noc] = reg.b[c.q];
+                    a.oc_mb[a.noc] = make_fastdiv64(reg.b[c.q]).m;
+                    a.oc_d[a.noc] = (uint32_t)reg.dims[c.q];
+                    a.oc_md[a.noc] = make_fastdiv64((uint64_t)reg.dims[c.q]).m;
+                    a.oc_v[a.noc] = (uint32_t)c.v;
+                    ++a.noc;
+                }
+            }
+        };
+        for (int i : load) put(i, false);
+        for (int i : store) put(i, true);
+    }
+    for (int i : rest) {
         const GateSpec &g = gates[i];
         bool paired = false;
         for (int j = (int)items.size() - 1; j >= 0; --j) {
@@ -1311,7 +1450,6 @@ bool build_pass(const Register &reg, const std::vector<GateSpec> &gates, const P
     }
     // gates
     int uoff = 0;
-    *work = PassWork{};
     p.ngates = (int32_t)items.size();
     for (size_t gi = 0; gi < items.size(); ++gi) {
         const GateSpec &g = gates[items[gi].a];
@@ -1724,7 +1862,7 @@ cudaError_t run_pass(const Register &reg, const std::vector<GateSpec> &gates, co
         }
     }
     static thread_local PassParams p;   // ~23 KB; parameters are copied at launch
-    *handled = build_pass(reg, gates, pp, psi, cfg.pass_tile, p, work);
+    *handled = build_pass(reg, gates, pp, psi, cfg.pass_tile, p, work, cfg.pass_absorb != 0);
     // complex64 (8-byte elements): every bulk copy must start at a 16-byte aligned address and
     // move a multiple of 16 bytes; tile runs are multiples of L = b_{m0} and start at multiples
     // of L, so an even L suffices (the stage needs the tile plus the fp32 matrix pool)

@@ -73,6 +73,7 @@ void default_cfg(LaunchCfg &c, int device) {
     c.pass_low = 32;           // tile runs of >= 32 amplitudes (512 B bulk copies)
     c.shard_overlap = 16;      // remap overlapped with the pending local run on 132 + 16 SMs
     c.pass_kernel = 0;         // per-gate pass kernel (stages measured slower on c3/c4: profiles/r02)
+    c.pass_absorb = 1;         // permutations on member digits relabel the tile's loads / stores
 }
 
 }  // namespace
@@ -567,6 +568,9 @@ sv_status sv_set_option(sv_handle h, int32_t option, int64_t value) {
         case SV_OPT_SHARD_OVERLAP:
             if (value < 0 || value > 64) return fail(SV_ERR_INVALID_ARG, "shard overlap SMs 0..64");
             h->cfg.shard_overlap = (int)value;
+            return SV_OK;
+        case SV_OPT_PASS_ABSORB:
+            h->cfg.pass_absorb = value != 0;
             return SV_OK;
         case SV_OPT_PASS_KERNEL:
             if (value < 0 || value > 1) return fail(SV_ERR_INVALID_ARG, "pass kernel 0 or 1");

@@ -206,6 +206,7 @@ struct LaunchCfg {
     int shard_overlap; // SMs lent to a qubit remap that overlaps the pending local run (0 = off)
     int pass_kernel;   // SV_BLOCK passes: 0 = per-gate kernel (k_gate_pass); 1 = register-blocked
                        // stages (k_gate_stage) when the pass fits them, else per-gate
+    int pass_absorb;   // 1: pure permutations on member digits become load / store relabelling
 };
 
 // psi points at the state in the handle's element type (cfg.c64 / the c64 flag).

@@ -21,6 +21,7 @@ SV_OPT_KERNEL, SV_OPT_TILE_ELEMS, SV_OPT_TILE_STAGES, SV_OPT_CTAS_PER_SM, SV_OPT
 SV_OPT_PASS_STAGES, SV_OPT_PASS_THREADS, SV_OPT_PASS_GATES, SV_OPT_PASS_GROUPS = 7, 8, 9, 10
 SV_OPT_PASS_WINDOW, SV_OPT_PASS_MERGE, SV_OPT_SHARD_SWAP, SV_OPT_PASS_SEARCH = 11, 12, 13, 14
 SV_OPT_PLAN_CACHE, SV_OPT_PASS_KERNEL, SV_OPT_SHARD_OVERLAP, SV_OPT_PASS_LOW = 15, 16, 17, 18
+SV_OPT_PASS_ABSORB = 19
 
 STATUS = {0: "SV_OK", 1: "SV_ERR_INVALID_ARG", 2: "SV_ERR_DIM", 3: "SV_ERR_OVERFLOW",
           4: "SV_ERR_QUDIT_RANGE", 5: "SV_ERR_CTRL_OVERLAP", 6: "SV_ERR_CTRL_DUP",

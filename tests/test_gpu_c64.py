@@ -186,6 +186,46 @@ def test_loopback_relabel_and_phase_c64(P, nranks):
         assert np.linalg.norm(got - ref) <= bound(gates, dims, np.sqrt(2) * U32), block
 
 
+def test_c64_absorbed_permutations(P):
+    """Permutations absorbed into the complex64 pass kernel's load / store addressing
+    (SV_OPT_PASS_ABSORB): a labelled permutation circuit bit-exact, and Haar gates mixed with
+    controlled permutations within the fp32 bound, with fewer shared-memory round trips."""
+    dims = [4, 2, 2, 3, 2, 4, 2, 2, 2]          # L = 48: 16-byte aligned complex64 tiles
+    rng = np.random.default_rng(33)
+    n, D = len(dims), int(np.prod(dims))
+
+    def circuit(general_frac, ngates):
+        gates = []
+        for _ in range(ngates):
+            t = int(rng.integers(n))
+            if rng.random() < general_frac:
+                gates.append(Gate(t, (), (), haar_unitary(dims[t], rng)))
+                continue
+            others = [q for q in range(n) if q != t]
+            ctrl = tuple(int(c) for c in rng.choice(others, size=int(rng.integers(0, 3)), replace=False))
+            vals = tuple(int(rng.integers(dims[c])) for c in ctrl)
+            gates.append(Gate(t, ctrl, vals, permutation_matrix(rng.permutation(dims[t]))))
+        return gates
+
+    for general_frac in (0.0, 0.4):
+        gates = circuit(general_frac, 90)
+        psi0 = labelled_state(0, D) if general_frac == 0.0 else random_state(D, 9)
+        ref = O2.run(dims, gates, psi0)
+        with P.State(dims, dtype="c64") as st:
+            st.set_option(P.sv.SV_OPT_PASS_ABSORB, 1)
+            st.set_option(P.sv.SV_OPT_PROFILE, 1)
+            st.set_amplitudes(0, psi0)
+            st.apply_circuit(gates, block=True)
+            got = st.amplitudes()
+            prof = st.profile_read()
+        if general_frac == 0.0:
+            assert np.array_equal(got, ref)
+        else:
+            assert np.linalg.norm(got - ref) <= bound(gates, dims)
+        assert prof.pass_launches > 0
+        assert prof.pass_item_touched < prof.pass_touched
+
+
 def test_c64_factored_pairs(P):
     """Factored pair items in the complex64 pass kernel (two general gates on different in-tile
     digits with the same controls, U_a then U_b on the class in registers): against the fp64

@@ -581,6 +581,89 @@ def test_block_passes_labelled_bit_exact(P, pass_cfg):
     assert np.array_equal(got, ref)
 
 
+def _absorb_circuit(rng, dims, ngates, general_frac=0.4):
+    """Haar gates mixed with permutations (random sigma or X_{+1}) carrying 0-2 controls of any
+    value: permutations whose target and controls are member digits or out-of-tile digits get
+    absorbed at the load (front) or store (back) of their pass; the rest stay items."""
+    n = len(dims)
+    gates = []
+    for _ in range(ngates):
+        t = int(rng.integers(n))
+        if rng.random() < general_frac:
+            gates.append(Gate(t, (), (), haar_unitary(dims[t], rng)))
+            continue
+        others = [q for q in range(n) if q != t]
+        nc = int(rng.integers(0, 3))
+        ctrl = tuple(int(c) for c in rng.choice(others, size=nc, replace=False))
+        vals = tuple(int(rng.integers(dims[c])) for c in ctrl)
+        U = shift_x(dims[t], 1) if rng.random() < 0.5 else permutation_matrix(rng.permutation(dims[t]))
+        gates.append(Gate(t, ctrl, vals, U))
+    return gates
+
+
+def _run_absorb(P, dims, gates, psi0, absorb, tile, pass_cfg=(512, 4, 4), dtype="c128"):
+    with P.State(dims, dtype=dtype) as st:
+        threads, groups, stages = pass_cfg
+        st.set_option(P.sv.SV_OPT_PASS_TILE, tile)
+        st.set_option(P.sv.SV_OPT_PASS_THREADS, threads)
+        st.set_option(P.sv.SV_OPT_PASS_GROUPS, groups)
+        st.set_option(P.sv.SV_OPT_PASS_STAGES, stages)
+        st.set_option(P.sv.SV_OPT_PASS_ABSORB, absorb)
+        st.set_option(P.sv.SV_OPT_PROFILE, 1)
+        st.set_amplitudes(0, psi0)
+        st.apply_circuit(gates, block=True)
+        got = st.amplitudes()
+        prof = st.profile_read()
+    return got, prof
+
+
+@pytest.mark.parametrize("pass_cfg", [(512, 4, 4), (512, 2, 3), (256, 1, 2)])
+@pytest.mark.parametrize("tile", [3200, 1280, 512])
+def test_block_passes_absorbed_permutations(P, tile, pass_cfg):
+    """Permutations absorbed into the pass tile's load / store member addressing
+    (SV_OPT_PASS_ABSORB): random registers (c4-like low prefixes and qubit-only ones), Haar gates
+    mixed with controlled permutations; against O-2 with absorption on and off, the same applied
+    work either way, and fewer shared-memory round trips with it on (absorbed gates are no
+    compute items)."""
+    rng = np.random.default_rng(tile + pass_cfg[1])
+    regs = [[5, 5, 4, 4, 3, 3, 2, 2, 2, 2], [2] * 16, [3, 2, 4, 2, 2, 3, 2, 2, 3], [4, 3, 2, 2, 2, 2, 5, 2]]
+    work = np.zeros(2)
+    for r, dims in enumerate(regs):
+        D = int(np.prod(dims))
+        gates = _absorb_circuit(rng, dims, 120)
+        psi0 = random_state(D, r)
+        ref = O2.run(dims, gates, psi0)
+        on, pon = _run_absorb(P, dims, gates, psi0, 1, tile, pass_cfg)
+        off, poff = _run_absorb(P, dims, gates, psi0, 0, tile, pass_cfg)
+        assert np.max(np.abs(on - ref)) <= 1e-12, (dims, tile)
+        assert np.max(np.abs(off - ref)) <= 1e-12, (dims, tile)
+        assert pon.pass_launches > 0
+        assert pon.pass_touched == poff.pass_touched          # absorbed gates still count as applied
+        assert pon.pass_item_touched <= poff.pass_item_touched
+        work += [pon.pass_item_touched, poff.pass_item_touched]
+    # a small register's tile may be all run and low prefix, with no member digit to absorb on
+    assert work[0] < work[1], work
+
+
+def test_block_passes_absorbed_permutations_bit_exact(P):
+    """Permutation-only circuits on an index-labelled state with absorption: bit-exact against
+    O-2, including passes whose every gate is absorbed (no compute item at all)."""
+    rng = np.random.default_rng(17)
+    for dims in ([5, 5, 4, 2, 2, 3, 2, 2], [2] * 14):
+        D = int(np.prod(dims))
+        gates = _absorb_circuit(rng, dims, 100, general_frac=0.0)
+        lab = labelled_state(0, D)
+        ref = O2.run(dims, gates, lab)
+        work = np.zeros(2)
+        for tile in (3200, 640):
+            got, pon = _run_absorb(P, dims, gates, lab, 1, tile)
+            assert np.array_equal(got, ref), (dims, tile)
+            _, poff = _run_absorb(P, dims, gates, lab, 0, tile)
+            assert pon.pass_touched == poff.pass_touched
+            work += [pon.pass_item_touched, poff.pass_item_touched]
+        assert work[0] < work[1], (dims, work)
+
+
 @pytest.mark.parametrize("pass_cfg", [(256, 1, 3), (384, 2, 3), (512, 2, 3)])
 @pytest.mark.parametrize("pass_tile", [4096, 1024, 256])
 def test_stage_kernel_random_sweep(P, pass_tile, pass_cfg):

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--search", type=int, default=1, help="SV_OPT_PASS_SEARCH (in-tile set search)")
     ap.add_argument("--skip-noblock", action="store_true", help="do not time the single-gate mode")
     ap.add_argument("--low", type=int, default=32, help="SV_OPT_PASS_LOW (low-prefix stride threshold)")
+    ap.add_argument("--absorb", type=int, default=1, help="SV_OPT_PASS_ABSORB (permutations as load / store relabelling)")
     ap.add_argument("--pass-kernel", type=int, default=0, help="SV_OPT_PASS_KERNEL: 0 per-gate, 1 register-blocked stages")
     args = ap.parse_args()
     import torch
@@ -59,6 +60,8 @@ def main():
             st.set_option(P.sv.SV_OPT_PASS_SEARCH, args.search)
             st.set_option(P.sv.SV_OPT_PASS_KERNEL, args.pass_kernel)
             st.set_option(P.sv.SV_OPT_PASS_LOW, args.low)
+            if args.absorb >= 0:
+                st.set_option(P.sv.SV_OPT_PASS_ABSORB, args.absorb)
         st.reset(0)
         st.apply_circuit(ga, fuse=True, check=False, block=block)
         st.sync()
@@ -73,7 +76,7 @@ def main():
         ms = e0.elapsed_time(e1) / args.reps
         launches = (st.info().kernel_launches - n0) // args.reps
         print(json.dumps({"config": args.config, "D": D, "gates": len(gates), "mode": kind, "tile": te,
-                          "stages": s, "threads": nt, "groups": rest[0] if rest else 0, "window": rest[1] if rest else 0, "max_gates": ng, "pass_kernel": args.pass_kernel, "ms": ms, "launches": launches,
+                          "stages": s, "threads": nt, "groups": rest[0] if rest else 0, "window": rest[1] if rest else 0, "max_gates": ng, "pass_kernel": args.pass_kernel, "absorb": args.absorb, "ms": ms, "launches": launches,
                           "updates_per_s": T / (ms / 1e3), "equiv_GBps": 32.0 * T / (ms / 1e3) / 1e9,
                           "pass_GBps": 32.0 * D * launches / (ms / 1e3) / 1e9}), flush=True)
     st.close()
