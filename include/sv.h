@@ -218,7 +218,7 @@ SV_API sv_status sv_get_info(sv_handle h, sv_info *out);
 #define SV_OPT_PASS_STAGES  7   /* SV_BLOCK: ring capacity = this many tiles of SV_OPT_PASS_TILE (2..12,
                                    default 4); each pass re-cuts it into as many stages of its own
                                    tile size as fit (at most 8), so smaller tiles get a deeper ring */
-#define SV_OPT_PASS_THREADS 8   /* compute threads per CTA of the pass kernel (256, 384 or 512)    */
+#define SV_OPT_PASS_THREADS 8   /* compute threads per CTA of the pass kernel (256, 384, 512 or 576) */
 #define SV_OPT_PASS_GATES   9   /* max gates applied per pass (1..32)                              */
 #define SV_OPT_PASS_GROUPS 10   /* consumer warp groups of the pass kernel, each on its own tile
                                    (1, 2, 4 or 8 with 512 threads; at most the number of stages)    */

@@ -1660,6 +1660,10 @@ cudaError_t launch_pass(const PassParams &p, cudaStream_t st, const LaunchCfg &c
     while (G > 1 && S < G) G /= 2;
     if (cfg.pass_threads >= 960) return launch_pass_t<960, 2, double2>(p, st, cfg, S, TE);   // 32 warps, 64 registers
     if (cfg.pass_threads >= 768) return launch_pass_t<768, 2, double2>(p, st, cfg, S, TE);   // 26 warps, 72 registers
+    if (cfg.pass_threads == 576) {                // 18 compute warps + 2 = 5 warps per scheduler at 96 registers
+        if (cfg.pass_groups == 3 && S >= 3) return launch_pass_t<576, 3, double2>(p, st, cfg, S, TE);
+        return launch_pass_t<576, 2, double2>(p, st, cfg, S, TE);
+    }
     if (cfg.pass_threads >= 512) {
         if (G >= 8) return launch_pass_t<512, 8, double2>(p, st, cfg, S, TE);
         if (G >= 4) return launch_pass_t<512, 4, double2>(p, st, cfg, S, TE);

@@ -543,13 +543,13 @@ sv_status sv_set_option(sv_handle h, int32_t option, int64_t value) {
             h->cfg.pass_stages = (int)value;
             return SV_OK;
         case SV_OPT_PASS_THREADS:
-            if (value != 256 && value != 384 && value != 512 && value != 768 && value != 960)
-                return fail(SV_ERR_INVALID_ARG, "pass threads 256, 384, 512, 768 or 960");
+            if (value != 256 && value != 384 && value != 512 && value != 576 && value != 768 && value != 960)
+                return fail(SV_ERR_INVALID_ARG, "pass threads 256, 384, 512, 576, 768 or 960");
             h->cfg.pass_threads = (int)value;
             return SV_OK;
         case SV_OPT_PASS_GROUPS:
             if (value != 1 && value != 2 && value != 3 && value != 4 && value != 8)
-                return fail(SV_ERR_INVALID_ARG, "pass groups 1, 2, 3 (384 threads), 4 or 8");
+                return fail(SV_ERR_INVALID_ARG, "pass groups 1, 2, 3 (384 or 576 threads), 4 or 8");
             h->cfg.pass_groups = (int)value;
             return SV_OK;
         case SV_OPT_PASS_MERGE:

@@ -496,7 +496,7 @@ def test_loopback_overlapped_remap(P, nranks):
 
 # (compute threads, consumer groups, stages) of the pass kernel
 PASS_CFGS = [(256, 1, 2), (384, 1, 2), (512, 1, 2), (384, 2, 2), (256, 2, 3), (384, 2, 3), (512, 2, 3), (512, 4, 4),
-             (512, 4, 5), (512, 8, 9)]
+             (512, 4, 5), (512, 8, 9), (576, 3, 4), (576, 2, 3)]
 
 
 @pytest.mark.parametrize("pass_cfg", PASS_CFGS)
